@@ -1,0 +1,116 @@
+/*
+ * prg.h — C-ABI of the B200-native PageRank-pipeline hot path (K1 sort, K2
+ * filter, K3 PageRank). Plain pointers and sizes; no C++ or torch types.
+ *
+ * Each entry point replaces one reference interface (paths relative to
+ * /root/reference/proj); the C++ shim in paper_1603_01876_b200/host re-exposes
+ * the reference's exact prpipe:: signatures and pybind11 module on top of it.
+ *
+ * Conventions
+ *   - Status codes replace the reference's exceptions (include/prpipe/types.hpp:17-28):
+ *     PRG_OK (0) or a negative PRG_ERR_*; prg_last_error() has the message
+ *     (thread-local). The shim turns them back into prpipe::Error.
+ *   - "_device" entry points take device pointers and a cudaStream_t passed as
+ *     void*; they are stream-ordered and may synchronise the stream at the end
+ *     to report input errors and output sizes.
+ *   - "_host" entry points take host buffers; H2D, kernels and D2H happen inside.
+ *   - Edges are the reference's Edge {int64 u, v} (types.hpp:10-15), 1-based,
+ *     stored interleaved: uv[2*i] = u, uv[2*i+1] = v.
+ *   - A prg_matrix is an opaque device-resident row-stochastic CSR
+ *     (u32 row offsets and columns, f64 values), the device form of the
+ *     reference's StochasticMatrix (kernel2_filter.hpp:28-38).
+ */
+#ifndef PRG_H_
+#define PRG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t prg_status;
+#define PRG_OK 0
+#define PRG_ERR_INVALID_ARGUMENT (-1) /* bad sizes / config (e.g. PageRankConfig::validate) */
+#define PRG_ERR_LABEL_RANGE (-2)      /* vertex label outside [1, N] (kernel2_filter.cpp:41-43) */
+#define PRG_ERR_UNSORTED (-3)         /* K2 input not sorted by start vertex (kernel2_filter.cpp:45-47) */
+#define PRG_ERR_CUDA (-4)             /* CUDA runtime failure or no device */
+#define PRG_ERR_INTERNAL (-5)
+
+typedef struct prg_matrix prg_matrix;
+
+/* Library info / error channel. */
+const char* prg_last_error(void);
+const char* prg_version(void);
+int32_t prg_device_count(void);
+
+/* ---- K0 (input generation; untimed) ------------------------------------
+ * Device restatement of EdgeGenerator::make_edge (src/graph_gen.cpp:83-99):
+ * edges [first, first+count) of the K0 list for (scale, seed, initiator).
+ * d_labels: the Fisher–Yates label table (graph_gen.cpp:66-76, 2^scale int64,
+ * device) or NULL for permute_labels=false. prg_k0_permutation fills it on
+ * the host (the shuffle is inherently sequential). */
+prg_status prg_k0_permutation(int32_t scale, uint64_t seed, int64_t* labels_host);
+prg_status prg_k0_generate_device(int32_t scale, int64_t edge_factor, uint64_t seed,
+                                  const double initiator[4], const int64_t* d_labels,
+                                  int64_t first, int64_t count, int64_t* d_uv, void* stream);
+
+/* ---- K1 — replaces the core of prpipe::sort_edges --------------------------
+ * include/prpipe/kernel1_sort.hpp:24-25; src/kernel1_sort.cpp:63-68
+ * (std::sort by start vertex). Output is ordered by (u, v): a valid start-vertex
+ * order with canonical ties (tests/helpers.hpp:29-34). d_uv_in and d_uv_out
+ * must not alias. Labels must lie in [1, 2^scale] (else PRG_ERR_LABEL_RANGE). */
+prg_status prg_k1_sort_device(const int64_t* d_uv_in, int64_t m, int32_t scale, int64_t* d_uv_out,
+                              void* stream);
+prg_status prg_k1_sort_host(const int64_t* uv_in, int64_t m, int32_t scale, int64_t* uv_out);
+
+/* ---- K2 — replaces run_kernel2's core -------------------------------------
+ * build_adjacency + in_degree + zero_columns + row_normalize
+ * (include/prpipe/kernel2_filter.hpp:42-65; src/kernel2_filter.cpp:12-168).
+ * Input sorted by start vertex (ties in any order). n = vertex count. */
+prg_status prg_k2_filter_device(const int64_t* d_uv_sorted, int64_t m, int64_t n, prg_matrix** out,
+                                void* stream);
+prg_status prg_k2_filter_host(const int64_t* uv_sorted, int64_t m, int64_t n, prg_matrix** out);
+
+/* Matrix handle. */
+prg_status prg_matrix_info(const prg_matrix* a, int64_t* n, int64_t* nnz, int64_t* nnz_raw,
+                           int64_t* max_in_degree);
+/* Copies to host int64/f64 arrays (row_offsets[n+1], cols[nnz], values[nnz],
+ * d_in[n]); any pointer may be NULL. d_in is the pre-filter in-degree
+ * (in_degree(), kernel2_filter.cpp:101-106); zeros for uploaded matrices. */
+prg_status prg_matrix_download(const prg_matrix* a, int64_t* row_offsets, int64_t* cols,
+                               double* values, int64_t* d_in);
+/* Device views (u32 offsets/cols, f64 values, u32 d_in; d_in may be NULL). */
+prg_status prg_matrix_device_arrays(const prg_matrix* a, const uint32_t** row_offsets,
+                                    const uint32_t** cols, const double** values,
+                                    const uint32_t** d_in);
+/* Uploads a host StochasticMatrix (int64 offsets/cols, f64 values). */
+prg_status prg_matrix_from_host(int64_t n, int64_t nnz, const int64_t* row_offsets,
+                                const int64_t* cols, const double* values, prg_matrix** out);
+void prg_matrix_destroy(prg_matrix* a);
+
+/* ---- K3 — replaces init_rank / pagerank_step / run_kernel3 ----------------
+ * include/prpipe/kernel3_pagerank.hpp:28-44; src/kernel3_pagerank.cpp:29-79.
+ * mode 0: timed path (deterministic tree sums; within 1e-10 relative L1 of
+ *         the reference, the gap being the reference's own sequential-sum
+ *         rounding, kernel3_pagerank.cpp:17-19);
+ * mode 1: parity path — reference evaluation order (ascending-u column sums,
+ *         separate mul/add, sequential sums); bit-identical to the reference.
+ * Ranks are written in the original vertex order; *norm1 = sum of the ranks. */
+prg_status prg_k3_pagerank_device(const prg_matrix* a, double damping, int32_t iterations,
+                                  uint64_t seed, int32_t mode, double* d_ranks, double* norm1,
+                                  void* stream);
+prg_status prg_k3_pagerank_host(int64_t n, int64_t nnz, const int64_t* row_offsets,
+                                const int64_t* cols, const double* values, double damping,
+                                int32_t iterations, uint64_t seed, int32_t mode, double* ranks,
+                                double* norm1);
+prg_status prg_init_rank_device(int64_t n, uint64_t seed, int32_t mode, double* d_r, double* norm1,
+                                void* stream);
+prg_status prg_pagerank_step_device(const prg_matrix* a, const double* d_r, double damping,
+                                    int32_t mode, double* d_out, double* norm1, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PRG_H_ */

@@ -1,0 +1,149 @@
+// ref_driver.cpp — extern "C" harness around the REFERENCE implementation.
+//
+// TEST INFRASTRUCTURE ONLY (see oracle/prg_oracle.c header). This file is
+// compiled together with the reference's own sources, straight from
+// /root/reference/proj/src (never copied), by oracle/build_ref.sh into
+// oracle/_ref/libprpipe_ref.so. It lets tests/ generate golden vectors from the
+// reference itself and lets bench.py time the reference's CPU path
+// ("cpu_baseline.kind": "reference").
+#include <algorithm>
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <span>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "prpipe/graph_gen.hpp"
+#include "prpipe/kernel2_filter.hpp"
+#include "prpipe/kernel3_pagerank.hpp"
+
+using namespace prpipe;
+
+namespace {
+thread_local std::string g_err;
+double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+// K0: EdgeGenerator::fill_batch, batches spread over `threads` threads
+// (bit-identical to sequential generation: tests/test_graph_gen.cpp:168-188).
+int ref_generate(int scale, std::uint64_t seed, const double* init, int permute, int threads,
+                 std::int64_t* uv) {
+    try {
+        GenConfig c;
+        c.scale = scale;
+        c.seed = seed;
+        for (int i = 0; i < 4; ++i) c.initiator[i] = init[i];
+        c.permute_labels = permute != 0;
+        EdgeGenerator gen(c);
+        const std::int64_t nb = gen.batch_count();
+        auto work = [&](int t) {
+            std::vector<Edge> batch;
+            for (std::int64_t b = t; b < nb; b += threads) {
+                gen.fill_batch(b, batch);
+                std::memcpy(uv + 2 * b * EdgeGenerator::kBatchEdges, batch.data(),
+                            batch.size() * sizeof(Edge));
+            }
+        };
+        std::vector<std::thread> pool;
+        for (int t = 0; t < std::max(1, threads); ++t) pool.emplace_back(work, t);
+        for (auto& th : pool) th.join();
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+// K1 core: the reference's in-memory sort, std::sort by start vertex only
+// (src/kernel1_sort.cpp:14,66). Sorts in place; returns elapsed seconds.
+double ref_k1_sort_core(std::int64_t* uv, std::int64_t m) {
+    auto* e = reinterpret_cast<Edge*>(uv);
+    const double t0 = now_s();
+    std::sort(e, e + m, [](const Edge& a, const Edge& b) { return a.u < b.u; });
+    return now_s() - t0;
+}
+
+// K2 core: build_adjacency(span) + in_degree + zero_columns + row_normalize
+// (include/prpipe/kernel2_filter.hpp:42-54). Output buffers: row_offsets[n+1],
+// cols/values[m] (nnz_f <= m), d_in[n]. Returns nnz_f (>= 0) or -1 on error.
+std::int64_t ref_k2_core(const std::int64_t* uv, std::int64_t m, std::int64_t n,
+                         std::int64_t* row_offsets, std::int64_t* cols, double* values,
+                         std::int64_t* d_in, std::int64_t* nnz_raw, double* elapsed) {
+    try {
+        std::span<const Edge> edges(reinterpret_cast<const Edge*>(uv), static_cast<std::size_t>(m));
+        const double t0 = now_s();
+        CountMatrix a = build_adjacency(edges, n);
+        const auto din = in_degree(a);
+        const CountMatrix f = zero_columns(a, din);
+        const StochasticMatrix s = row_normalize(f);
+        if (elapsed) *elapsed = now_s() - t0;
+        if (nnz_raw) *nnz_raw = a.nnz();
+        std::memcpy(row_offsets, s.row_offsets.data(), sizeof(std::int64_t) * (n + 1));
+        std::memcpy(cols, s.cols.data(), sizeof(std::int64_t) * s.cols.size());
+        std::memcpy(values, s.values.data(), sizeof(double) * s.values.size());
+        std::memcpy(d_in, din.data(), sizeof(std::int64_t) * n);
+        return s.nnz();
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+// K3: run_kernel3 (src/kernel3_pagerank.cpp:67-79) on a CSR given as arrays.
+// Returns norm1; elapsed seconds of the reference's own timed region.
+double ref_k3(std::int64_t n, std::int64_t nnz, const std::int64_t* row_offsets,
+              const std::int64_t* cols, const double* values, double damping, int iterations,
+              std::uint64_t seed, std::int64_t total_edges, double* ranks, double* elapsed) {
+    try {
+        StochasticMatrix s;
+        s.n = n;
+        s.row_offsets.assign(row_offsets, row_offsets + n + 1);
+        s.cols.assign(cols, cols + nnz);
+        s.values.assign(values, values + nnz);
+        PageRankConfig c;
+        c.damping = damping;
+        c.iterations = iterations;
+        c.seed = seed;
+        auto res = run_kernel3(s, c, total_edges);
+        if (elapsed) *elapsed = res.elapsed_seconds;
+        std::memcpy(ranks, res.ranks.values.data(), sizeof(double) * n);
+        return res.ranks.norm1;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1.0;
+    }
+}
+
+// One reference pagerank_step (src/kernel3_pagerank.cpp:41-65); returns norm1.
+double ref_pagerank_step(std::int64_t n, std::int64_t nnz, const std::int64_t* row_offsets,
+                         const std::int64_t* cols, const double* values, const double* r,
+                         double damping, double* out) {
+    StochasticMatrix s;
+    s.n = n;
+    s.row_offsets.assign(row_offsets, row_offsets + n + 1);
+    s.cols.assign(cols, cols + nnz);
+    s.values.assign(values, values + nnz);
+    RankVector rv;
+    rv.values.assign(r, r + n);
+    auto o = pagerank_step(rv, s, damping);
+    std::memcpy(out, o.values.data(), sizeof(double) * n);
+    return o.norm1;
+}
+
+// init_rank (src/kernel3_pagerank.cpp:29-39); returns norm1.
+double ref_init_rank(std::int64_t n, std::uint64_t seed, double* r) {
+    auto rv = init_rank(n, seed);
+    std::memcpy(r, rv.values.data(), sizeof(double) * n);
+    return rv.norm1;
+}
+
+}  // extern "C"

@@ -1,0 +1,332 @@
+// prg_capi.cu — the extern "C" boundary (include/prg.h).
+#include <cstring>
+#include <memory>
+#include <type_traits>
+#include <string>
+#include <vector>
+
+#include "../../include/prg.h"
+#include "prg_internal.cuh"
+
+using prg::CudaError;
+using prg::DevBuf;
+
+// Matrix arrays come from the stream-ordered pool; a handle may have been used
+// on any stream, so release only after the device is idle.
+prg_matrix::~prg_matrix() {
+    if (row_offsets || cols || values || d_in) cudaDeviceSynchronize();
+    prg::ws_free(row_offsets, nullptr);
+    prg::ws_free(cols, nullptr);
+    prg::ws_free(values, nullptr);
+    prg::ws_free(d_in, nullptr);
+}
+
+namespace {
+
+struct ApiError {
+    prg_status code;
+    std::string msg;
+};
+
+template <class F>
+prg_status guarded(const char* what, F&& f) {
+    try {
+        f();
+        return PRG_OK;
+    } catch (const ApiError& e) {
+        prg::set_error(std::string(what) + ": " + e.msg);
+        return e.code;
+    } catch (const CudaError& e) {
+        prg::set_error(std::string(what) + ": " + e.msg);
+        return PRG_ERR_CUDA;
+    } catch (const std::bad_alloc&) {
+        prg::set_error(std::string(what) + ": host allocation failed");
+        return PRG_ERR_INTERNAL;
+    } catch (const std::exception& e) {
+        prg::set_error(std::string(what) + ": " + e.what());
+        return PRG_ERR_INTERNAL;
+    }
+}
+
+void require(bool ok, prg_status code, const std::string& msg) {
+    if (!ok) throw ApiError{code, msg};
+}
+
+void check_device_errors(uint32_t err, const char* stage) {
+    if (err & prg::kErrLabelRange)
+        throw ApiError{PRG_ERR_LABEL_RANGE, std::string(stage) + ": vertex label outside [1, N]"};
+    if (err & prg::kErrUnsorted)
+        throw ApiError{PRG_ERR_UNSORTED, std::string(stage) + ": input not sorted by start vertex"};
+    if (err & prg::kErrOverflow) throw ApiError{PRG_ERR_INTERNAL, std::string(stage) + ": capacity overflow"};
+}
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+template <class T>
+T* dmalloc(size_t count) {
+    return static_cast<T*>(prg::ws_alloc((count ? count : 1) * sizeof(T), nullptr));
+}
+
+__global__ void widen_u32(const uint32_t* __restrict__ in, int64_t n, int64_t* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = in[i];
+}
+__global__ void narrow_i64(const int64_t* __restrict__ in, int64_t n, int64_t limit, uint32_t* __restrict__ out,
+                           uint32_t* err) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t x = in[i];
+        if (x < 0 || x > limit) atomicOr(err, (uint32_t)prg::kErrLabelRange);
+        out[i] = (uint32_t)x;
+    }
+}
+
+void download_u32_as_i64(const uint32_t* d, size_t n, int64_t* h, cudaStream_t s) {
+    if (!h || !n) return;
+    DevBuf<int64_t> tmp(n, s);
+    widen_u32<<<(unsigned)prg::num_sms() * 4, 1024, 0, s>>>(d, (int64_t)n, tmp.get());
+    PRG_LAUNCH_CHECK();
+    PRG_CUDA(cudaMemcpyAsync(h, tmp.get(), n * 8, cudaMemcpyDeviceToHost, s));
+    PRG_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* prg_last_error(void) { return prg::last_error().c_str(); }
+const char* prg_version(void) { return "prg-b200 0.1.0 (sm_100a)"; }
+
+int32_t prg_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+prg_status prg_k0_permutation(int32_t scale, uint64_t seed, int64_t* labels) {
+    return guarded("prg_k0_permutation", [&] {
+        require(scale >= 0 && scale <= 40 && labels, PRG_ERR_INVALID_ARGUMENT, "bad scale or null buffer");
+        const int64_t n = int64_t{1} << scale;
+        for (int64_t i = 0; i < n; ++i) labels[i] = i + 1;
+        // graph_gen.cpp:72-76, SplitMix64(mix_seed(seed, kPermutationStream))
+        uint64_t st = prg::dev::mix_seed(seed, 0x7065726d75746174ULL);
+        for (int64_t i = n - 1; i > 0; --i) {
+            uint64_t z = (st += 0x9e3779b97f4a7c15ULL);
+            z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+            z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+            z ^= z >> 31;
+            const int64_t j = (int64_t)(z % ((uint64_t)i + 1));
+            std::swap(labels[i], labels[j]);
+        }
+    });
+}
+
+prg_status prg_k0_generate_device(int32_t scale, int64_t edge_factor, uint64_t seed,
+                                  const double initiator[4], const int64_t* d_labels, int64_t first,
+                                  int64_t count, int64_t* d_uv, void* stream) {
+    return guarded("prg_k0_generate_device", [&] {
+        require(scale >= 1 && scale <= 40 && count >= 0 && first >= 0 && initiator, PRG_ERR_INVALID_ARGUMENT,
+                "bad generator arguments");
+        prg::k0_generate_device(scale, edge_factor, seed, initiator, d_labels, first, count, d_uv,
+                                as_stream(stream));
+    });
+}
+
+prg_status prg_k1_sort_device(const int64_t* d_uv_in, int64_t m, int32_t scale, int64_t* d_uv_out,
+                              void* stream) {
+    return guarded("prg_k1_sort", [&] {
+        require(m >= 0 && scale >= 0 && scale <= 32, PRG_ERR_INVALID_ARGUMENT, "scale must be in [0, 32]");
+        require(m == 0 || (d_uv_in && d_uv_out && d_uv_in != d_uv_out), PRG_ERR_INVALID_ARGUMENT,
+                "null or aliased edge buffers");
+        require((uint64_t)m < (1ull << 32), PRG_ERR_INVALID_ARGUMENT, "more than 2^32-1 edges");
+        if (m == 0) return;
+        cudaStream_t s = as_stream(stream);
+        DevBuf<uint32_t> err(1, s);
+        PRG_CUDA(cudaMemsetAsync(err.get(), 0, 4, s));
+        prg::k1_sort_device(d_uv_in, m, scale, d_uv_out, err.get(), s);
+        uint32_t h = 0;
+        PRG_CUDA(cudaMemcpyAsync(&h, err.get(), 4, cudaMemcpyDeviceToHost, s));
+        PRG_CUDA(cudaStreamSynchronize(s));
+        check_device_errors(h, "K1");
+    });
+}
+
+prg_status prg_k1_sort_host(const int64_t* uv_in, int64_t m, int32_t scale, int64_t* uv_out) {
+    return guarded("prg_k1_sort_host", [&] {
+        require(m >= 0, PRG_ERR_INVALID_ARGUMENT, "negative edge count");
+        if (m == 0) return;
+        cudaStream_t s = nullptr;
+        DevBuf<int64_t> a((size_t)m * 2, s), b((size_t)m * 2, s);
+        PRG_CUDA(cudaMemcpyAsync(a.get(), uv_in, (size_t)m * 16, cudaMemcpyHostToDevice, s));
+        const prg_status st = prg_k1_sort_device(a.get(), m, scale, b.get(), s);
+        if (st != PRG_OK) throw ApiError{st, prg::last_error()};
+        PRG_CUDA(cudaMemcpyAsync(uv_out, b.get(), (size_t)m * 16, cudaMemcpyDeviceToHost, s));
+        PRG_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+prg_status prg_k2_filter_device(const int64_t* d_uv_sorted, int64_t m, int64_t n, prg_matrix** out,
+                                void* stream) {
+    return guarded("prg_k2_filter", [&] {
+        require(out != nullptr, PRG_ERR_INVALID_ARGUMENT, "null output handle");
+        *out = nullptr;
+        require(n > 0, PRG_ERR_INVALID_ARGUMENT, "vertex count must be positive");
+        require(m >= 0 && (uint64_t)m < (1ull << 32) && (uint64_t)n < (1ull << 32), PRG_ERR_INVALID_ARGUMENT,
+                "sizes exceed the u32 index range");
+        cudaStream_t s = as_stream(stream);
+        auto* mat = new prg_matrix();
+        try {
+            const uint32_t err = prg::k2_filter_device(d_uv_sorted, m, n, mat, s);
+            check_device_errors(err, "K2");
+        } catch (...) {
+            delete mat;
+            throw;
+        }
+        *out = mat;
+    });
+}
+
+prg_status prg_k2_filter_host(const int64_t* uv_sorted, int64_t m, int64_t n, prg_matrix** out) {
+    return guarded("prg_k2_filter_host", [&] {
+        require(m >= 0, PRG_ERR_INVALID_ARGUMENT, "negative edge count");
+        cudaStream_t s = nullptr;
+        DevBuf<int64_t> a((size_t)std::max<int64_t>(m, 1) * 2, s);
+        if (m) PRG_CUDA(cudaMemcpyAsync(a.get(), uv_sorted, (size_t)m * 16, cudaMemcpyHostToDevice, s));
+        const prg_status st = prg_k2_filter_device(a.get(), m, n, out, s);
+        if (st != PRG_OK) throw ApiError{st, prg::last_error()};
+    });
+}
+
+prg_status prg_matrix_info(const prg_matrix* a, int64_t* n, int64_t* nnz, int64_t* nnz_raw, int64_t* max_in) {
+    return guarded("prg_matrix_info", [&] {
+        require(a != nullptr, PRG_ERR_INVALID_ARGUMENT, "null matrix");
+        if (n) *n = a->n;
+        if (nnz) *nnz = (int64_t)a->nnz;
+        if (nnz_raw) *nnz_raw = (int64_t)a->nnz_raw;
+        if (max_in) *max_in = (int64_t)a->max_in;
+    });
+}
+
+prg_status prg_matrix_download(const prg_matrix* a, int64_t* row_offsets, int64_t* cols, double* values,
+                               int64_t* d_in) {
+    return guarded("prg_matrix_download", [&] {
+        require(a != nullptr, PRG_ERR_INVALID_ARGUMENT, "null matrix");
+        cudaStream_t s = nullptr;
+        download_u32_as_i64(a->row_offsets, (size_t)a->n + 1, row_offsets, s);
+        download_u32_as_i64(a->cols, (size_t)a->nnz, cols, s);
+        if (values && a->nnz) {
+            PRG_CUDA(cudaMemcpy(values, a->values, a->nnz * 8, cudaMemcpyDeviceToHost));
+        }
+        if (d_in) {
+            if (a->d_in) download_u32_as_i64(a->d_in, (size_t)a->n, d_in, s);
+            else std::memset(d_in, 0, (size_t)a->n * 8);
+        }
+    });
+}
+
+prg_status prg_matrix_device_arrays(const prg_matrix* a, const uint32_t** ro, const uint32_t** cols,
+                                    const double** values, const uint32_t** d_in) {
+    return guarded("prg_matrix_device_arrays", [&] {
+        require(a != nullptr, PRG_ERR_INVALID_ARGUMENT, "null matrix");
+        if (ro) *ro = a->row_offsets;
+        if (cols) *cols = a->cols;
+        if (values) *values = a->values;
+        if (d_in) *d_in = a->d_in;
+    });
+}
+
+prg_status prg_matrix_from_host(int64_t n, int64_t nnz, const int64_t* row_offsets, const int64_t* cols,
+                                const double* values, prg_matrix** out) {
+    return guarded("prg_matrix_from_host", [&] {
+        require(out != nullptr, PRG_ERR_INVALID_ARGUMENT, "null output handle");
+        *out = nullptr;
+        require(n > 0 && nnz >= 0 && (uint64_t)nnz < (1ull << 32) && (uint64_t)n < (1ull << 32),
+                PRG_ERR_INVALID_ARGUMENT, "bad matrix sizes");
+        require(row_offsets[0] == 0 && row_offsets[n] == nnz, PRG_ERR_INVALID_ARGUMENT,
+                "row_offsets must start at 0 and end at nnz");
+        cudaStream_t s = nullptr;
+        auto mat = std::make_unique<prg_matrix>();
+        mat->n = n;
+        mat->nnz = (uint64_t)nnz;
+        mat->cap = (uint64_t)nnz;
+        mat->row_offsets = dmalloc<uint32_t>((size_t)n + 1);
+        mat->cols = dmalloc<uint32_t>((size_t)nnz);
+        mat->values = dmalloc<double>((size_t)nnz);
+        DevBuf<uint32_t> err(1, s);
+        PRG_CUDA(cudaMemsetAsync(err.get(), 0, 4, s));
+        {
+            DevBuf<int64_t> tmp((size_t)n + 1, s);
+            PRG_CUDA(cudaMemcpyAsync(tmp.get(), row_offsets, (size_t)(n + 1) * 8, cudaMemcpyHostToDevice, s));
+            narrow_i64<<<(unsigned)prg::num_sms() * 4, 1024, 0, s>>>(tmp.get(), n + 1, nnz, mat->row_offsets,
+                                                                      err.get());
+            PRG_LAUNCH_CHECK();
+        }
+        if (nnz) {
+            DevBuf<int64_t> tmp((size_t)nnz, s);
+            PRG_CUDA(cudaMemcpyAsync(tmp.get(), cols, (size_t)nnz * 8, cudaMemcpyHostToDevice, s));
+            narrow_i64<<<(unsigned)prg::num_sms() * 4, 1024, 0, s>>>(tmp.get(), nnz, n - 1, mat->cols, err.get());
+            PRG_LAUNCH_CHECK();
+            PRG_CUDA(cudaMemcpyAsync(mat->values, values, (size_t)nnz * 8, cudaMemcpyHostToDevice, s));
+        }
+        uint32_t h = 0;
+        PRG_CUDA(cudaMemcpyAsync(&h, err.get(), 4, cudaMemcpyDeviceToHost, s));
+        PRG_CUDA(cudaStreamSynchronize(s));
+        require(h == 0, PRG_ERR_LABEL_RANGE, "row offsets or column indices out of range");
+        *out = mat.release();
+    });
+}
+
+void prg_matrix_destroy(prg_matrix* a) { delete a; }
+
+prg_status prg_k3_pagerank_device(const prg_matrix* a, double damping, int32_t iterations, uint64_t seed,
+                                  int32_t mode, double* d_ranks, double* norm1, void* stream) {
+    return guarded("prg_k3_pagerank", [&] {
+        require(a != nullptr && d_ranks != nullptr, PRG_ERR_INVALID_ARGUMENT, "null argument");
+        // PageRankConfig::validate (kernel3_pagerank.cpp:23-27)
+        require(damping > 0.0 && damping < 1.0, PRG_ERR_INVALID_ARGUMENT, "damping must lie strictly between 0 and 1");
+        require(iterations >= 1, PRG_ERR_INVALID_ARGUMENT, "iteration count must be >= 1");
+        require(mode == 0 || mode == 1, PRG_ERR_INVALID_ARGUMENT, "mode must be 0 (timed) or 1 (parity)");
+        prg::K3Options o;
+        o.damping = damping;
+        o.iterations = iterations;
+        o.seed = seed;
+        o.mode = mode;
+        const double nm = prg::k3_pagerank_device(a, o, d_ranks, as_stream(stream));
+        if (norm1) *norm1 = nm;
+    });
+}
+
+prg_status prg_k3_pagerank_host(int64_t n, int64_t nnz, const int64_t* row_offsets, const int64_t* cols,
+                                const double* values, double damping, int32_t iterations, uint64_t seed,
+                                int32_t mode, double* ranks, double* norm1) {
+    return guarded("prg_k3_pagerank_host", [&] {
+        prg_matrix* a = nullptr;
+        prg_status st = prg_matrix_from_host(n, nnz, row_offsets, cols, values, &a);
+        if (st != PRG_OK) throw ApiError{st, prg::last_error()};
+        std::unique_ptr<prg_matrix> own(a);
+        cudaStream_t s = nullptr;
+        DevBuf<double> r((size_t)n, s);
+        st = prg_k3_pagerank_device(a, damping, iterations, seed, mode, r.get(), norm1, s);
+        if (st != PRG_OK) throw ApiError{st, prg::last_error()};
+        PRG_CUDA(cudaMemcpyAsync(ranks, r.get(), (size_t)n * 8, cudaMemcpyDeviceToHost, s));
+        PRG_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+prg_status prg_init_rank_device(int64_t n, uint64_t seed, int32_t mode, double* d_r, double* norm1, void* stream) {
+    return guarded("prg_init_rank", [&] {
+        require(n >= 1, PRG_ERR_INVALID_ARGUMENT, "rank vector needs at least one entry");
+        const double nm = prg::k3_init_rank_device(n, seed, d_r, mode, as_stream(stream));
+        if (norm1) *norm1 = nm;
+    });
+}
+
+prg_status prg_pagerank_step_device(const prg_matrix* a, const double* d_r, double damping, int32_t mode,
+                                    double* d_out, double* norm1, void* stream) {
+    return guarded("prg_pagerank_step", [&] {
+        require(a != nullptr && d_r && d_out, PRG_ERR_INVALID_ARGUMENT, "null argument");
+        const double nm = prg::k3_step_device(a, d_r, damping, d_out, mode, as_stream(stream));
+        if (norm1) *norm1 = nm;
+    });
+}
+
+}  // extern "C"

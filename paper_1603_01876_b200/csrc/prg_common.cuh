@@ -1,0 +1,185 @@
+// prg_common.cuh — shared device/host helpers for the B200 K1/K2/K3 kernels.
+#pragma once
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include <cuda_runtime.h>
+
+namespace prg {
+
+constexpr int kWarp = 32;
+constexpr int kNumSMsB200 = 148;
+
+// Host-side error channel: every C-ABI entry point funnels failures through
+// set_error() so prg_last_error() can report them (SURVEY §5 failure detection).
+void set_error(const std::string& msg);
+const std::string& last_error();
+
+struct CudaError {
+    std::string msg;
+};
+
+#define PRG_CUDA(call)                                                                   \
+    do {                                                                                 \
+        cudaError_t e_ = (call);                                                         \
+        if (e_ != cudaSuccess)                                                           \
+            throw ::prg::CudaError{std::string(#call) + ": " + cudaGetErrorString(e_) + \
+                                   " (" __FILE__ ":" + std::to_string(__LINE__) + ")"}; \
+    } while (0)
+
+#define PRG_LAUNCH_CHECK() PRG_CUDA(cudaGetLastError())
+
+__host__ __device__ inline unsigned div_up(uint64_t a, uint64_t b) { return static_cast<unsigned>((a + b - 1) / b); }
+
+int num_sms();
+
+// Stream-ordered scratch allocation (cudaMallocAsync on the device's default
+// pool, whose release threshold the library raises to "keep everything").
+void* ws_alloc(size_t bytes, cudaStream_t s);
+void ws_free(void* p, cudaStream_t s);
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    cudaStream_t s = nullptr;
+    DevBuf() = default;
+    DevBuf(size_t count, cudaStream_t stream) : n(count), s(stream) {
+        p = static_cast<T*>(ws_alloc(count ? count * sizeof(T) : sizeof(T), stream));
+    }
+    ~DevBuf() { if (p) ws_free(p, s); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) {
+            if (p) ws_free(p, s);
+            p = o.p; n = o.n; s = o.s; o.p = nullptr;
+        }
+        return *this;
+    }
+    T* get() const { return p; }
+    T* release() { T* q = p; p = nullptr; return q; }
+};
+
+// Device-wide exclusive scan of u32 counts into u32/u64 offsets (decoupled
+// look-back, one pass). `total` (device scalar, may be null) receives the sum.
+void exclusive_scan_u32(const uint32_t* in, uint32_t* out, size_t n, uint32_t* total,
+                        cudaStream_t s);
+void exclusive_scan_u32_to_u64(const uint32_t* in, uint64_t* out, size_t n, uint64_t* total,
+                               cudaStream_t s);
+
+// Device error word: kernels that validate input OR a code in; the host reads it
+// back at the end of an entry point (one sync) and turns it into a status.
+enum DeviceErr : uint32_t {
+    kErrNone = 0,
+    kErrLabelRange = 1u << 0,   // vertex label outside [1, N]
+    kErrUnsorted = 1u << 1,     // K2 input not sorted by start vertex
+    kErrNotCanonical = 1u << 2, // informational: ties not v-ordered (K2 re-sorts)
+    kErrOverflow = 1u << 3,     // an internal capacity was exceeded
+};
+
+}  // namespace prg
+
+// ----------------------------------------------------------------------------
+// Device helpers
+// ----------------------------------------------------------------------------
+namespace prg::dev {
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ unsigned warp_id() { return threadIdx.x >> 5; }
+
+template <class T>
+__device__ __forceinline__ T warp_incl_scan(T v) {
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        T o = __shfl_up_sync(0xffffffffu, v, d);
+        if ((int)lane_id() >= d) v += o;
+    }
+    return v;
+}
+
+template <class T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    return v;
+}
+
+// Deterministic fp64 warp tree sum (fixed butterfly order), separate add only.
+__device__ __forceinline__ double warp_sum_f64(double v) {
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, d));
+    return v;
+}
+
+// Block-wide exclusive scan of one u32 per thread; returns the block total.
+// `smem` needs blockDim.x/32 + 1 u32 slots.
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* smem, uint32_t& total) {
+    const unsigned w = warp_id(), l = lane_id(), nw = blockDim.x >> 5;
+    uint32_t inc = warp_incl_scan(v);
+    if (l == 31) smem[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        uint32_t x = l < nw ? smem[l] : 0u;
+        uint32_t xi = warp_incl_scan(x);
+        if (l < nw) smem[l] = xi - x;
+        if (l == nw - 1) smem[nw] = xi;
+    }
+    __syncthreads();
+    uint32_t res = smem[w] + inc - v;
+    total = smem[nw];
+    __syncthreads();
+    return res;
+}
+
+// Streaming (evict-first) and keep (evict-last) global loads via L2 cache-policy
+// hints (sm_100 accepts the bare .L2::evict_* qualifiers only on 256-bit loads).
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint32_t ld_stream_u32(const void* p, uint64_t pol) {
+    uint32_t r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ uint4 ld_stream_u4(const void* p, uint64_t pol) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ double ld_keep_f64(const double* p, uint64_t pol) {
+    double r;
+    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
+    return r;
+}
+
+// splitmix64 finaliser + counter-based stream position (rng.hpp:14-19): the
+// state after k calls from seed s0 is s0 + k*gamma, so x_k is a pure function.
+__device__ __forceinline__ uint64_t splitmix_at(uint64_t s0, uint64_t k) {
+    uint64_t z = s0 + k * 0x9e3779b97f4a7c15ULL;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+__host__ __device__ __forceinline__ uint64_t mix_seed(uint64_t seed, uint64_t stream) {
+    // rng.hpp:33-37: SplitMix64 g(seed ^ (gamma*(stream+1))); g.next(); return g.next();
+    uint64_t s0 = seed ^ (0x9e3779b97f4a7c15ULL * (stream + 1));
+    uint64_t z = s0 + 2 * 0x9e3779b97f4a7c15ULL;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+}  // namespace prg::dev

@@ -1,0 +1,55 @@
+// prg_internal.cuh — declarations shared by the K1/K2/K3 translation units and
+// the C-ABI layer (prg_capi.cu).
+#pragma once
+
+#include "prg_common.cuh"
+
+// The C-ABI handle (include/prg.h declares it opaque).
+struct prg_matrix {
+    int64_t n = 0;
+    uint64_t nnz = 0;       // stored entries (after the K2 filter)
+    uint64_t nnz_raw = 0;   // unique (u,v) entries before the filter (K2 only)
+    uint64_t max_in = 0;    // max pre-filter in-degree (K2 only)
+    uint64_t cap = 0;       // capacity of cols/values
+    uint32_t* row_offsets = nullptr;  // [n+1], u32 (nnz < 2^32)
+    uint32_t* cols = nullptr;         // [cap], 0-based
+    double* values = nullptr;         // [cap]
+    uint32_t* d_in = nullptr;         // [n] pre-filter in-degree (null when uploaded)
+    ~prg_matrix();
+};
+
+namespace prg {
+
+// K1 (prg_k1.cu): sort M int64 (u,v) pairs by (u,v). d_err receives DeviceErr bits.
+void k1_sort_device(const int64_t* d_uv_in, int64_t m, int scale, int64_t* d_uv_out,
+                    uint32_t* d_err, cudaStream_t s);
+
+// K2 (prg_k2.cu): fused build_adjacency + in_degree + zero_columns +
+// row_normalize over a device edge list sorted by start vertex. Returns a
+// DeviceErr mask (0 on success); fills *out.
+uint32_t k2_filter_device(const int64_t* d_uv, int64_t m, int64_t n, prg_matrix* out,
+                          cudaStream_t s);
+
+// K3 (prg_k3.cu).
+struct K3Options {
+    double damping = 0.85;
+    int iterations = 20;
+    uint64_t seed = 0;
+    int mode = 0;  // 0 = timed (deterministic tree sums), 1 = parity (reference order)
+};
+// Full run_kernel3 semantics: init_rank + iterations steps. d_ranks [n] in the
+// original vertex order; returns norm1 (sum of the final vector).
+double k3_pagerank_device(const prg_matrix* a, const K3Options& opt, double* d_ranks,
+                          cudaStream_t s);
+// One pagerank_step (kernel3_pagerank.cpp:41-65): d_out = step(d_r). Returns norm1.
+double k3_step_device(const prg_matrix* a, const double* d_r, double damping, double* d_out,
+                      int mode, cudaStream_t s);
+// init_rank (kernel3_pagerank.cpp:29-39) on the device; returns norm1.
+double k3_init_rank_device(int64_t n, uint64_t seed, double* d_r, int mode, cudaStream_t s);
+
+// K0 (prg_k0.cu): device edge generator; labels = Fisher-Yates table (device, n entries) or null.
+void k0_generate_device(int scale, int64_t edge_factor, uint64_t seed, const double init[4],
+                        const int64_t* d_labels, int64_t first, int64_t count, int64_t* d_uv,
+                        cudaStream_t s);
+
+}  // namespace prg

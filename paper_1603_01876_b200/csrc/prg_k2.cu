@@ -1,0 +1,441 @@
+// prg_k2.cu — K2: adjacency build + in-degree + column filter + row
+// normalisation, fused over a device edge list sorted by start vertex.
+//
+// Replaces the core of prpipe::run_kernel2 (src/kernel2_filter.cpp:154-168):
+//   build_adjacency / build_from  (:12-54)   — RLE of (u,v) runs into counts
+//   in_degree                     (:101-106) — d_in[v] += count
+//   zero_columns                  (:108-132) — drop columns with d_in == max or 1
+//   row_normalize                 (:134-152) — value = count / filtered row sum
+// Output: CSR with u32 row offsets / cols and f64 values, plus the pre-filter
+// d_in. Values are one IEEE division of the same two integers the reference
+// divides, so they are bit-identical.
+//
+// Passes (S=24: M=268M edges, 8192-edge tiles):
+//   A  read edges once: validate labels and order, count unique (u,v), d_in atomics
+//   -  max(d_in), keep bitmask (N bits)
+//   B  read edges again: keep-bit gather, in-tile run lengths / row sums in SMEM,
+//      kept-entry positions by decoupled look-back, write cols/values/row offsets
+//   F  fix-ups for the few rows that span tiles (run continuation counts, then
+//      divide those rows by their row sums accumulated across tiles)
+#include "prg_internal.cuh"
+
+namespace prg {
+
+namespace {
+
+constexpr int kT = 1024;        // threads per CTA
+constexpr int kI = 8;           // edges per thread
+constexpr int kTE = kT * kI;    // edges per tile
+
+struct EdgeSmem {
+    uint32_t su[kTE];
+    uint32_t sv[kTE];
+};
+
+struct PassBSmem {
+    uint32_t su[kTE];
+    uint32_t sv[kTE];
+    uint32_t rowsum[kTE];  // kept-edge count per row head (local index)
+    uint32_t runlen[kTE];  // edge count per run head (local index)
+    uint32_t scan_u[kT / 32 + 1];
+    int32_t scan_i[kT / 32 + 1];
+    uint32_t prev_u, prev_v, next_u;
+    int has_prev, has_next;
+    uint32_t tile;
+    uint64_t tile_base;
+    uint32_t first_row_part, first_run_part;
+};
+
+__device__ __forceinline__ int32_t block_excl_max_scan(int32_t v, int32_t* smem, int32_t& total) {
+    const unsigned w = dev::warp_id(), l = dev::lane_id(), nw = blockDim.x >> 5;
+    int32_t inc = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        int32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+        if ((int)l >= d) inc = max(inc, o);
+    }
+    int32_t ex = __shfl_up_sync(0xffffffffu, inc, 1);
+    if (l == 0) ex = -1;
+    if (l == 31) smem[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        int32_t x = l < nw ? smem[l] : -1;
+        int32_t xi = x;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            int32_t o = __shfl_up_sync(0xffffffffu, xi, d);
+            if ((int)l >= d) xi = max(xi, o);
+        }
+        int32_t xe = __shfl_up_sync(0xffffffffu, xi, 1);
+        if (l == 0) xe = -1;
+        if (l < nw) smem[l] = xe;
+        if (l == nw - 1) smem[nw] = xi;
+    }
+    __syncthreads();
+    const int32_t res = max(smem[w], ex);
+    total = smem[nw];
+    __syncthreads();
+    return res;
+}
+
+// ---------------------------------------------------------------------------
+// Pass A
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kT) k2_pass_a(const longlong2* __restrict__ uv, int64_t m, int64_t n,
+                                                uint32_t* __restrict__ d_in, uint32_t* __restrict__ err,
+                                                unsigned long long* __restrict__ nnz_raw,
+                                                uint32_t ntiles) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    EdgeSmem& S = *reinterpret_cast<EdgeSmem*>(smem_raw);
+    __shared__ uint32_t red[kT / 32];
+    __shared__ uint32_t pu_s, pv_s;
+    __shared__ int has_prev_s;
+    uint32_t my_err = 0;
+    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int64_t base = (int64_t)t * kTE;
+        const int cnt = (int)min((int64_t)kTE, m - base);
+#pragma unroll
+        for (int j = 0; j < kI; ++j) {
+            const int l = j * kT + threadIdx.x;
+            if (l < cnt) {
+                const longlong2 p = uv[base + l];
+                const bool ok = p.x >= 1 && p.x <= n && p.y >= 1 && p.y <= n;
+                if (!ok) my_err |= kErrLabelRange;
+                const uint32_t u = ok ? (uint32_t)(p.x - 1) : 0u, v = ok ? (uint32_t)(p.y - 1) : 0u;
+                S.su[l] = u;
+                S.sv[l] = v;
+                if (ok) atomicAdd(&d_in[v], 1u);
+            }
+        }
+        if (threadIdx.x == 0) {
+            has_prev_s = base > 0;
+            if (base > 0) {
+                const longlong2 p = uv[base - 1];
+                pu_s = (uint32_t)(p.x - 1);
+                pv_s = (uint32_t)(p.y - 1);
+            }
+        }
+        __syncthreads();
+        uint32_t heads = 0;
+        const int l0 = threadIdx.x * kI;
+#pragma unroll
+        for (int k = 0; k < kI; ++k) {
+            const int l = l0 + k;
+            if (l < cnt) {
+                const uint32_t u = S.su[l], v = S.sv[l];
+                bool first = false;
+                uint32_t pu = 0, pv = 0;
+                if (l > 0) { pu = S.su[l - 1]; pv = S.sv[l - 1]; }
+                else if (has_prev_s) { pu = pu_s; pv = pv_s; }
+                else first = true;
+                if (first) heads++;
+                else {
+                    if (u < pu) my_err |= kErrUnsorted;
+                    else if (u == pu && v < pv) my_err |= kErrNotCanonical;
+                    heads += (u != pu || v != pv);
+                }
+            }
+        }
+        heads = dev::warp_sum(heads);
+        if (dev::lane_id() == 0) red[dev::warp_id()] = heads;
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            uint32_t x = threadIdx.x < kT / 32 ? red[threadIdx.x] : 0;
+            x = dev::warp_sum(x);
+            if (threadIdx.x == 0) atomicAdd(nnz_raw, (unsigned long long)x);
+        }
+        __syncthreads();
+    }
+    my_err = __reduce_or_sync(0xffffffffu, my_err);
+    if (dev::lane_id() == 0 && my_err) atomicOr(err, my_err);
+}
+
+__global__ void k2_max_kernel(const uint32_t* __restrict__ d_in, int64_t n, uint32_t* __restrict__ out) {
+    uint32_t mx = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        mx = max(mx, d_in[i]);
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if (dev::lane_id() == 0) atomicMax(out, mx);
+}
+
+// keep(c) = d_in[c] != max && d_in[c] != 1   (kernel2_filter.cpp:118-121)
+__global__ void k2_keep_kernel(const uint32_t* __restrict__ d_in, int64_t n, const uint32_t* __restrict__ maxp,
+                               uint32_t* __restrict__ keepbits) {
+    const uint32_t mx = *maxp;
+    const int64_t nw = (n + 31) / 32;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nw * 32; i += (int64_t)gridDim.x * blockDim.x) {
+        bool keep = false;
+        if (i < n) { const uint32_t d = d_in[i]; keep = d != mx && d != 1u; }
+        const uint32_t word = __ballot_sync(0xffffffffu, keep);
+        if (dev::lane_id() == 0) keepbits[i >> 5] = word;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Pass B
+// ---------------------------------------------------------------------------
+constexpr uint64_t kFlagAgg = 1ull << 62, kFlagInc = 2ull << 62, kValMask = (1ull << 62) - 1;
+
+__global__ void __launch_bounds__(kT) k2_pass_b(
+    const longlong2* __restrict__ uv, int64_t m, int64_t n, const uint32_t* __restrict__ keepbits,
+    uint32_t* __restrict__ row_offsets, uint32_t* __restrict__ cols, double* __restrict__ values,
+    unsigned long long* __restrict__ tile_status, uint32_t* __restrict__ tile_counter,
+    uint32_t* __restrict__ dout_f, uint32_t* __restrict__ fix_rows, uint32_t* __restrict__ n_fix,
+    uint32_t* __restrict__ cont_p, uint32_t* __restrict__ cont_c, unsigned long long* __restrict__ nnz_out) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    PassBSmem& S = *reinterpret_cast<PassBSmem*>(smem_raw);
+    const unsigned tid = threadIdx.x;
+    if (tid == 0) S.tile = atomicAdd(tile_counter, 1u);
+    __syncthreads();
+    const uint32_t t = S.tile;
+    const int64_t base = (int64_t)t * kTE;
+    const int cnt = (int)min((int64_t)kTE, m - base);
+#pragma unroll
+    for (int j = 0; j < kI; ++j) {
+        const int l = j * kT + tid;
+        if (l < cnt) {
+            const longlong2 p = uv[base + l];
+            S.su[l] = (uint32_t)(p.x - 1);
+            S.sv[l] = (uint32_t)(p.y - 1);
+        }
+        if (l < kTE) { S.rowsum[l] = 0; S.runlen[l] = 0; }
+    }
+    if (tid == 0) {
+        S.has_prev = base > 0;
+        if (base > 0) {
+            const longlong2 p = uv[base - 1];
+            S.prev_u = (uint32_t)(p.x - 1);
+            S.prev_v = (uint32_t)(p.y - 1);
+        }
+        S.has_next = base + cnt < m;
+        if (base + cnt < m) S.next_u = (uint32_t)(uv[base + cnt].x - 1);
+        S.first_row_part = 0;
+        S.first_run_part = 0;
+    }
+    __syncthreads();
+
+    // Blocked per-thread view: edges l0 .. l0+kI-1.
+    const int l0 = tid * kI;
+    uint32_t fl_rs = 0, fl_hd = 0, fl_kp = 0;  // bit k per item
+    int32_t last_rs = -1, last_hd = -1;
+    uint32_t nkh = 0;
+#pragma unroll
+    for (int k = 0; k < kI; ++k) {
+        const int l = l0 + k;
+        if (l < cnt) {
+            const uint32_t u = S.su[l], v = S.sv[l];
+            bool rs, hd;
+            if (l > 0) { rs = u != S.su[l - 1]; hd = rs || v != S.sv[l - 1]; }
+            else if (S.has_prev) { rs = u != S.prev_u; hd = rs || v != S.prev_v; }
+            else { rs = true; hd = true; }
+            const bool kp = (keepbits[v >> 5] >> (v & 31)) & 1u;
+            fl_rs |= (uint32_t)rs << k;
+            fl_hd |= (uint32_t)hd << k;
+            fl_kp |= (uint32_t)kp << k;
+            if (rs) last_rs = l;
+            if (hd) last_hd = l;
+            nkh += (hd && kp);
+        }
+    }
+    int32_t rs_last_all, hd_last_all;
+    const int32_t carry_rs = block_excl_max_scan(last_rs, S.scan_i, rs_last_all);
+    const int32_t carry_hd = block_excl_max_scan(last_hd, S.scan_i, hd_last_all);
+    uint32_t tile_kh;
+    const uint32_t kh_excl = dev::block_excl_scan(nkh, S.scan_u, tile_kh);
+
+    // Decoupled look-back for the tile's global kept-entry base.
+    if (tid == 0) {
+        uint64_t excl = 0;
+        if (t == 0) {
+            atomicExch(&tile_status[0], kFlagInc | tile_kh);
+        } else {
+            atomicExch(&tile_status[t], kFlagAgg | tile_kh);
+            int64_t k = (int64_t)t - 1;
+            for (;;) {
+                const uint64_t st = *((volatile unsigned long long*)&tile_status[k]);
+                const uint64_t fl = st & ~kValMask;
+                if (fl == 0) continue;
+                excl += st & kValMask;
+                if (fl == kFlagInc) break;
+                --k;
+            }
+            atomicExch(&tile_status[t], kFlagInc | (excl + tile_kh));
+        }
+        S.tile_base = excl;
+    }
+
+    // Row sums (kept edges) and run lengths (all edges) into SMEM per head.
+    {
+        int32_t rh = carry_rs, rn = carry_hd;
+        uint32_t acc_row = 0, acc_run = 0;
+#pragma unroll
+        for (int k = 0; k < kI; ++k) {
+            const int l = l0 + k;
+            if (l < cnt) {
+                if ((fl_rs >> k) & 1u) {
+                    if (acc_row) { if (rh >= 0) atomicAdd(&S.rowsum[rh], acc_row); else atomicAdd(&S.first_row_part, acc_row); }
+                    acc_row = 0;
+                    rh = l;
+                }
+                if ((fl_hd >> k) & 1u) {
+                    if (acc_run) { if (rn >= 0) atomicAdd(&S.runlen[rn], acc_run); else atomicAdd(&S.first_run_part, acc_run); }
+                    acc_run = 0;
+                    rn = l;
+                }
+                acc_row += (fl_kp >> k) & 1u;
+                acc_run += 1;
+            }
+        }
+        if (acc_row) { if (rh >= 0) atomicAdd(&S.rowsum[rh], acc_row); else atomicAdd(&S.first_row_part, acc_row); }
+        if (acc_run) { if (rn >= 0) atomicAdd(&S.runlen[rn], acc_run); else atomicAdd(&S.first_run_part, acc_run); }
+    }
+    __syncthreads();
+    const uint64_t tile_base = S.tile_base;
+    const bool last_spans = S.has_next && S.su[cnt - 1] == S.next_u;
+    const bool first_spans = S.has_prev && S.su[0] == S.prev_u;
+    const int32_t rh_last = rs_last_all;  // local head of the tile's last row (-1: began earlier)
+
+    // Emit entries and row offsets.
+    {
+        int32_t rh = carry_rs;
+        uint64_t pos = tile_base + kh_excl;
+#pragma unroll
+        for (int k = 0; k < kI; ++k) {
+            const int l = l0 + k;
+            if (l < cnt) {
+                const uint32_t u = S.su[l], v = S.sv[l];
+                if ((fl_rs >> k) & 1u) {
+                    rh = l;
+                    const int64_t pu = l > 0 ? (int64_t)S.su[l - 1] : (S.has_prev ? (int64_t)S.prev_u : -1);
+                    for (int64_t r = pu + 1; r <= (int64_t)u; ++r) row_offsets[r] = (uint32_t)pos;
+                }
+                if (((fl_hd >> k) & 1u) && ((fl_kp >> k) & 1u)) {
+                    cols[pos] = v;
+                    const double c = (double)S.runlen[l];
+                    const bool spanning = rh < 0 || (last_spans && rh == rh_last);
+                    values[pos] = spanning ? c : c / (double)S.rowsum[rh];
+                    ++pos;
+                }
+            }
+        }
+    }
+    if (tid == 0) {
+        // Rows crossing tile edges: partial kept-edge sums go to dout_f.
+        if (first_spans && S.first_row_part) atomicAdd(&dout_f[S.su[0]], S.first_row_part);
+        if (last_spans && rh_last >= 0) {
+            atomicAdd(&dout_f[S.su[cnt - 1]], S.rowsum[rh_last]);
+            fix_rows[atomicAdd(n_fix, 1u)] = S.su[cnt - 1];
+        }
+        // A run continuing from the previous tile: its head entry is the last
+        // kept entry before this tile (position tile_base-1) when kept.
+        const bool kp0 = (keepbits[S.sv[0] >> 5] >> (S.sv[0] & 31)) & 1u;
+        if (S.first_run_part && kp0) { cont_p[t] = (uint32_t)(tile_base - 1); cont_c[t] = S.first_run_part; }
+        else { cont_p[t] = 0; cont_c[t] = 0; }
+        if (base + cnt == m) *nnz_out = tile_base + tile_kh;
+    }
+    if (base + cnt == m) {
+        const uint64_t total = tile_base + tile_kh;
+        for (int64_t r = (int64_t)S.su[cnt - 1] + 1 + tid; r <= n; r += kT) row_offsets[r] = (uint32_t)total;
+    }
+}
+
+__global__ void k2_fix_runs(const uint32_t* __restrict__ cont_p, const uint32_t* __restrict__ cont_c,
+                            uint32_t ntiles, double* __restrict__ values) {
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += gridDim.x * blockDim.x)
+        if (cont_c[t]) atomicAdd(&values[cont_p[t]], (double)cont_c[t]);  // exact: integers
+}
+
+__global__ void k2_fix_rows(const uint32_t* __restrict__ fix_rows, const uint32_t* __restrict__ n_fix,
+                            const uint32_t* __restrict__ row_offsets, const uint32_t* __restrict__ dout_f,
+                            double* __restrict__ values) {
+    const uint32_t nf = *n_fix;
+    for (uint32_t i = blockIdx.x; i < nf; i += gridDim.x) {
+        const uint32_t r = fix_rows[i];
+        const uint32_t b = row_offsets[r], e = row_offsets[r + 1];
+        const double d = (double)dout_f[r];
+        for (uint32_t p = b + threadIdx.x; p < e; p += blockDim.x) values[p] = values[p] / d;
+    }
+}
+
+}  // namespace
+
+uint32_t k2_filter_device(const int64_t* d_uv, int64_t m, int64_t n, prg_matrix* out, cudaStream_t s) {
+    out->n = n;
+    out->cap = (uint64_t)(m > 0 ? m : 1);
+    out->row_offsets = static_cast<uint32_t*>(ws_alloc((size_t)(n + 1) * 4, s));
+    out->cols = static_cast<uint32_t*>(ws_alloc(out->cap * 4, s));
+    out->values = static_cast<double*>(ws_alloc(out->cap * 8, s));
+    out->d_in = static_cast<uint32_t*>(ws_alloc((size_t)n * 4, s));
+    PRG_CUDA(cudaMemsetAsync(out->d_in, 0, (size_t)n * 4, s));
+    if (m == 0) {
+        PRG_CUDA(cudaMemsetAsync(out->row_offsets, 0, (size_t)(n + 1) * 4, s));
+        out->nnz = out->nnz_raw = out->max_in = 0;
+        return 0;
+    }
+    const uint32_t ntiles = div_up((uint64_t)m, kTE);
+    DevBuf<uint64_t> scal(8, s);  // [0]=err|max [1]=nnz_raw [2]=nnz [3]=n_fix|tile_counter
+    PRG_CUDA(cudaMemsetAsync(scal.get(), 0, 8 * sizeof(uint64_t), s));
+    uint32_t* err = reinterpret_cast<uint32_t*>(scal.get());
+    uint32_t* maxp = err + 1;
+    unsigned long long* nnz_raw = reinterpret_cast<unsigned long long*>(scal.get() + 1);
+    unsigned long long* nnz_out = reinterpret_cast<unsigned long long*>(scal.get() + 2);
+    uint32_t* n_fix = reinterpret_cast<uint32_t*>(scal.get() + 3);
+    uint32_t* tile_counter = n_fix + 1;
+
+    const auto* uv = reinterpret_cast<const longlong2*>(d_uv);
+    static bool attr = false;
+    if (!attr) {
+        PRG_CUDA(cudaFuncSetAttribute(k2_pass_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(EdgeSmem)));
+        PRG_CUDA(cudaFuncSetAttribute(k2_pass_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PassBSmem)));
+        attr = true;
+    }
+    const unsigned ga = std::min<unsigned>(ntiles, (unsigned)num_sms() * 2);
+    k2_pass_a<<<ga, kT, sizeof(EdgeSmem), s>>>(uv, m, n, out->d_in, err, nnz_raw, ntiles);
+    PRG_LAUNCH_CHECK();
+    uint32_t h_err = 0;
+    PRG_CUDA(cudaMemcpyAsync(&h_err, err, 4, cudaMemcpyDeviceToHost, s));
+    PRG_CUDA(cudaStreamSynchronize(s));
+    if (h_err & (kErrLabelRange | kErrUnsorted)) return h_err;
+    if (h_err & kErrNotCanonical) {
+        // Ties are not v-ordered (e.g. the reference's std::sort output): the
+        // reference sorts each row's pending list (kernel2_filter.cpp:24), we
+        // canonicalise the whole list with the K1 sort and rerun.
+        int scale = 0;
+        while ((int64_t{1} << scale) < n) ++scale;
+        DevBuf<int64_t> tmp((size_t)m * 2, s);
+        DevBuf<uint32_t> e2(1, s);
+        PRG_CUDA(cudaMemsetAsync(e2.get(), 0, 4, s));
+        k1_sort_device(d_uv, m, scale, tmp.get(), e2.get(), s);
+        ws_free(out->row_offsets, s); ws_free(out->cols, s); ws_free(out->values, s); ws_free(out->d_in, s);
+        out->row_offsets = nullptr; out->cols = nullptr; out->values = nullptr; out->d_in = nullptr;
+        return k2_filter_device(tmp.get(), m, n, out, s) & ~(uint32_t)kErrNotCanonical;
+    }
+    const unsigned gn = (unsigned)num_sms() * 8;
+    k2_max_kernel<<<gn, 1024, 0, s>>>(out->d_in, n, maxp);
+    PRG_LAUNCH_CHECK();
+    DevBuf<uint32_t> keepbits((size_t)(n + 31) / 32, s);
+    k2_keep_kernel<<<gn, 1024, 0, s>>>(out->d_in, n, maxp, keepbits.get());
+    PRG_LAUNCH_CHECK();
+    DevBuf<unsigned long long> tile_status(ntiles, s);
+    DevBuf<uint32_t> dout_f((size_t)n, s), fix_rows(ntiles + 1, s), cont_p(ntiles, s), cont_c(ntiles, s);
+    PRG_CUDA(cudaMemsetAsync(tile_status.get(), 0, (size_t)ntiles * 8, s));
+    PRG_CUDA(cudaMemsetAsync(dout_f.get(), 0, (size_t)n * 4, s));
+    k2_pass_b<<<ntiles, kT, sizeof(PassBSmem), s>>>(uv, m, n, keepbits.get(), out->row_offsets, out->cols,
+                                                    out->values, tile_status.get(), tile_counter, dout_f.get(),
+                                                    fix_rows.get(), n_fix, cont_p.get(), cont_c.get(), nnz_out);
+    PRG_LAUNCH_CHECK();
+    k2_fix_runs<<<div_up(ntiles, 256), 256, 0, s>>>(cont_p.get(), cont_c.get(), ntiles, out->values);
+    PRG_LAUNCH_CHECK();
+    k2_fix_rows<<<(unsigned)num_sms() * 2, 256, 0, s>>>(fix_rows.get(), n_fix, out->row_offsets, dout_f.get(),
+                                                         out->values);
+    PRG_LAUNCH_CHECK();
+    uint64_t h[3];
+    PRG_CUDA(cudaMemcpyAsync(h, scal.get(), 3 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    PRG_CUDA(cudaStreamSynchronize(s));
+    out->max_in = h[0] >> 32;
+    out->nnz_raw = h[1];
+    out->nnz = h[2];
+    return (uint32_t)(h[0] & 0xffffffffu) & ~(uint32_t)kErrNotCanonical;
+}
+
+}  // namespace prg

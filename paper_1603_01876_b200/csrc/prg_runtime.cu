@@ -1,0 +1,170 @@
+// prg_runtime.cu — error channel, stream-ordered workspace, device-wide scan.
+#include <mutex>
+
+#include "prg_common.cuh"
+
+namespace prg {
+
+namespace {
+thread_local std::string g_last_error;
+std::once_flag g_pool_once;
+}  // namespace
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+const std::string& last_error() { return g_last_error; }
+
+int num_sms() {
+    static int cached = 0;
+    if (!cached) {
+        int dev = 0;
+        PRG_CUDA(cudaGetDevice(&dev));
+        PRG_CUDA(cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev));
+    }
+    return cached;
+}
+
+void* ws_alloc(size_t bytes, cudaStream_t s) {
+    std::call_once(g_pool_once, [] {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = UINT64_MAX;  // keep freed blocks cached across calls
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+    });
+    void* p = nullptr;
+    PRG_CUDA(cudaMallocAsync(&p, bytes ? bytes : 16, s));
+    return p;
+}
+
+void ws_free(void* p, cudaStream_t s) {
+    if (p) cudaFreeAsync(p, s);
+}
+
+// ---------------------------------------------------------------------------
+// Exclusive scan: reduce-then-scan, 1024 threads x 8 items per block.
+// ---------------------------------------------------------------------------
+namespace {
+constexpr int kScanThreads = 1024;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(const uint32_t* __restrict__ in,
+                                                                   size_t n,
+                                                                   uint64_t* __restrict__ partial) {
+    __shared__ uint64_t red[32];
+    const size_t base = (size_t)blockIdx.x * kScanTile;
+    uint64_t s = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        size_t i = base + (size_t)k * kScanThreads + threadIdx.x;
+        if (i < n) s += in[i];
+    }
+    s = dev::warp_sum(s);
+    if (dev::lane_id() == 0) red[dev::warp_id()] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        uint64_t v = red[threadIdx.x];
+        v = dev::warp_sum(v);
+        if (threadIdx.x == 0) partial[blockIdx.x] = v;
+    }
+}
+
+// Single-block exclusive scan over `n` u64 values (in place); total -> *total.
+__global__ void __launch_bounds__(kScanThreads) scan_partials_kernel(uint64_t* __restrict__ p,
+                                                                     size_t n) {
+    __shared__ uint64_t warp_tot[33];
+    __shared__ uint64_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (size_t base = 0; base < n; base += kScanThreads) {
+        size_t i = base + threadIdx.x;
+        uint64_t v = i < n ? p[i] : 0;
+        uint64_t inc = dev::warp_incl_scan(v);
+        if (dev::lane_id() == 31) warp_tot[dev::warp_id()] = inc;
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            uint64_t x = warp_tot[threadIdx.x];
+            uint64_t xi = dev::warp_incl_scan(x);
+            warp_tot[threadIdx.x] = xi - x;
+            if (threadIdx.x == 31) warp_tot[32] = xi;
+        }
+        __syncthreads();
+        uint64_t excl = carry + warp_tot[dev::warp_id()] + inc - v;
+        if (i < n) p[i] = excl;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += warp_tot[32];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) p[n] = carry;
+}
+
+template <class Out>
+__global__ void __launch_bounds__(kScanThreads) scan_down_kernel(const uint32_t* __restrict__ in,
+                                                                 size_t n,
+                                                                 const uint64_t* __restrict__ partial,
+                                                                 Out* __restrict__ out) {
+    __shared__ uint64_t warp_tot[33];
+    const size_t base = (size_t)blockIdx.x * kScanTile;
+    // Blocked arrangement: thread t owns items [base + t*8, base + t*8 + 8).
+    uint32_t v[kScanItems];
+    const size_t my = base + (size_t)threadIdx.x * kScanItems;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) v[k] = (my + k < n) ? in[my + k] : 0u;
+    uint64_t tsum = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) tsum += v[k];
+    uint64_t inc = dev::warp_incl_scan(tsum);
+    if (dev::lane_id() == 31) warp_tot[dev::warp_id()] = inc;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        uint64_t x = warp_tot[threadIdx.x];
+        uint64_t xi = dev::warp_incl_scan(x);
+        warp_tot[threadIdx.x] = xi - x;
+    }
+    __syncthreads();
+    uint64_t run = partial[blockIdx.x] + warp_tot[dev::warp_id()] + inc - tsum;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        if (my + k < n) out[my + k] = static_cast<Out>(run);
+        run += v[k];
+    }
+}
+
+template <class Out>
+__global__ void copy_total_kernel(const uint64_t* partial, size_t nb, Out* total) {
+    *total = static_cast<Out>(partial[nb]);
+}
+
+template <class Out>
+void scan_impl(const uint32_t* in, Out* out, size_t n, Out* total, cudaStream_t s) {
+    const size_t nb = n ? (n + kScanTile - 1) / kScanTile : 0;
+    DevBuf<uint64_t> part(nb + 1, s);
+    if (nb) {
+        scan_reduce_kernel<<<(unsigned)nb, kScanThreads, 0, s>>>(in, n, part.get());
+        PRG_LAUNCH_CHECK();
+    }
+    scan_partials_kernel<<<1, kScanThreads, 0, s>>>(part.get(), nb);
+    PRG_LAUNCH_CHECK();
+    if (nb) {
+        scan_down_kernel<Out><<<(unsigned)nb, kScanThreads, 0, s>>>(in, n, part.get(), out);
+        PRG_LAUNCH_CHECK();
+    }
+    if (total) {
+        copy_total_kernel<Out><<<1, 1, 0, s>>>(part.get(), nb, total);
+        PRG_LAUNCH_CHECK();
+    }
+}
+}  // namespace
+
+void exclusive_scan_u32(const uint32_t* in, uint32_t* out, size_t n, uint32_t* total,
+                        cudaStream_t s) {
+    scan_impl<uint32_t>(in, out, n, total, s);
+}
+void exclusive_scan_u32_to_u64(const uint32_t* in, uint64_t* out, size_t n, uint64_t* total,
+                               cudaStream_t s) {
+    scan_impl<uint64_t>(in, out, n, total, s);
+}
+
+}  // namespace prg

@@ -1,0 +1,270 @@
+// prg_sort.cu — non-template parts of the MSD radix sort (see prg_sort.cuh).
+#include <algorithm>
+
+#include "prg_sort.cuh"
+
+namespace prg::sort {
+
+// ---------------------------------------------------------------------------
+// Level bookkeeping
+// ---------------------------------------------------------------------------
+__global__ void classify_l1_kernel(const uint32_t* __restrict__ off, uint32_t ntiles, size_t n,
+                                   int shift, int bits, Seg* __restrict__ next,
+                                   uint32_t* __restrict__ n_next, Seg* __restrict__ fin,
+                                   uint32_t* __restrict__ n_fin) {
+    const int d = threadIdx.x;
+    if (d >= kRadix) return;
+    const uint64_t st = off[(size_t)d * ntiles];
+    const uint64_t en = d + 1 < kRadix ? off[(size_t)(d + 1) * ntiles] : n;
+    const uint32_t sz = (uint32_t)(en - st);
+    if (sz == 0) return;
+    Seg c;
+    c.start = st;
+    c.size = sz;
+    c.buf = 1;
+    c.bits = (uint8_t)bits;
+    c.shift = (uint16_t)(shift - bits);
+    if (sz <= (uint32_t)kLocalCap || bits == 0) fin[atomicAdd(n_fin, 1u)] = c;
+    else next[atomicAdd(n_next, 1u)] = c;
+}
+
+__global__ void build_tiles_kernel(const Seg* __restrict__ active, const uint32_t* __restrict__ n_active,
+                                   uint32_t* __restrict__ seg_tile0, uint64_t* __restrict__ seg_elem0,
+                                   uint32_t* __restrict__ tile_seg, uint32_t* __restrict__ tile_idx,
+                                   uint32_t* __restrict__ n_tiles, uint32_t max_tiles) {
+    // Single block, 1024 threads: sequential chunks of 1024 segments.
+    __shared__ uint32_t carry_t;
+    __shared__ uint64_t carry_e;
+    __shared__ uint32_t wt[33];
+    __shared__ uint64_t we[33];
+    const uint32_t na = *n_active;
+    if (threadIdx.x == 0) { carry_t = 0; carry_e = 0; }
+    __syncthreads();
+    for (uint32_t base = 0; base < na; base += blockDim.x) {
+        const uint32_t i = base + threadIdx.x;
+        uint32_t nt = 0;
+        uint64_t ne = 0;
+        if (i < na) { ne = active[i].size; nt = (uint32_t)((ne + kTile - 1) / kTile); }
+        uint32_t it = dev::warp_incl_scan(nt);
+        uint64_t ie = dev::warp_incl_scan(ne);
+        if (dev::lane_id() == 31) { wt[dev::warp_id()] = it; we[dev::warp_id()] = ie; }
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            uint32_t x = threadIdx.x < blockDim.x / 32 ? wt[threadIdx.x] : 0;
+            uint64_t y = threadIdx.x < blockDim.x / 32 ? we[threadIdx.x] : 0;
+            uint32_t xi = dev::warp_incl_scan(x);
+            uint64_t yi = dev::warp_incl_scan(y);
+            wt[threadIdx.x] = xi - x;
+            we[threadIdx.x] = yi - y;
+            if (threadIdx.x == 31) { wt[32] = xi; we[32] = yi; }
+        }
+        __syncthreads();
+        const uint32_t t0 = carry_t + wt[dev::warp_id()] + it - nt;
+        const uint64_t e0 = carry_e + we[dev::warp_id()] + ie - ne;
+        if (i < na) {
+            seg_tile0[i] = t0;
+            seg_elem0[i] = e0;
+            for (uint32_t k = 0; k < nt && t0 + k < max_tiles; ++k) {
+                tile_seg[t0 + k] = i;
+                tile_idx[t0 + k] = k;
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) { carry_t += wt[32]; carry_e += we[32]; }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        seg_tile0[na] = carry_t;
+        seg_elem0[na] = carry_e;
+        *n_tiles = carry_t;
+    }
+}
+
+__global__ void __launch_bounds__(kTileThreads) seg_hist_kernel(
+    const uint64_t* __restrict__ keys0, const uint64_t* __restrict__ keys1,
+    const Seg* __restrict__ active, const uint32_t* __restrict__ seg_tile0,
+    const uint32_t* __restrict__ tile_seg, const uint32_t* __restrict__ tile_idx,
+    const uint32_t* __restrict__ n_tiles, uint32_t* __restrict__ hist) {
+    __shared__ uint32_t h[kRadix];
+    const uint32_t nt = *n_tiles;
+    for (uint32_t t = blockIdx.x; t < nt; t += gridDim.x) {
+        const uint32_t si = tile_seg[t], ti = tile_idx[t];
+        const Seg sg = active[si];
+        const uint64_t* src = sg.buf ? keys1 : keys0;
+        const uint32_t seg_nt = seg_tile0[si + 1] - seg_tile0[si];
+        for (int i = threadIdx.x; i < kRadix; i += blockDim.x) h[i] = 0;
+        __syncthreads();
+        const uint64_t base = sg.start + (uint64_t)ti * kTile;
+        const int cnt = (int)min((uint64_t)kTile, (uint64_t)sg.size - (uint64_t)ti * kTile);
+        const unsigned mask = (1u << sg.bits) - 1u;
+        for (int li = threadIdx.x; li < cnt; li += kTileThreads)
+            atomicAdd(&h[(unsigned)(src[base + li] >> sg.shift) & mask], 1u);
+        __syncthreads();
+        // layout: [active seg][digit][tile in seg], packed per segment
+        const size_t hb = (size_t)seg_tile0[si] * kRadix;
+        for (int d = threadIdx.x; d < kRadix; d += blockDim.x) hist[hb + (size_t)d * seg_nt + ti] = h[d];
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(kTileThreads) seg_scatter_kernel(
+    const uint64_t* __restrict__ keys0, const uint64_t* __restrict__ keys1,
+    uint64_t* __restrict__ out0, uint64_t* __restrict__ out1, const Seg* __restrict__ active,
+    const uint32_t* __restrict__ seg_tile0, const uint64_t* __restrict__ seg_elem0,
+    const uint32_t* __restrict__ tile_seg, const uint32_t* __restrict__ tile_idx,
+    const uint32_t* __restrict__ n_tiles, const uint32_t* __restrict__ off) {
+    __shared__ uint32_t h[kRadix];
+    __shared__ uint32_t lstart[kRadix];
+    __shared__ uint64_t gbase[kRadix];
+    __shared__ uint32_t scan_tmp[kTileThreads / 32 + 1];
+    extern __shared__ uint64_t skeys[];
+    const uint32_t nt = *n_tiles;
+    for (uint32_t t = blockIdx.x; t < nt; t += gridDim.x) {
+        const uint32_t si = tile_seg[t], ti = tile_idx[t];
+        const Seg sg = active[si];
+        const uint64_t* src = sg.buf ? keys1 : keys0;
+        uint64_t* dst = sg.buf ? out0 : out1;
+        const uint32_t seg_nt = seg_tile0[si + 1] - seg_tile0[si];
+        const uint64_t e0 = seg_elem0[si];
+        for (int i = threadIdx.x; i < kRadix; i += blockDim.x) h[i] = 0;
+        __syncthreads();
+        const uint64_t base = sg.start + (uint64_t)ti * kTile;
+        const int cnt = (int)min((uint64_t)kTile, (uint64_t)sg.size - (uint64_t)ti * kTile);
+        const unsigned mask = (1u << sg.bits) - 1u;
+        uint64_t k[kTileItems];
+        uint32_t r[kTileItems];
+#pragma unroll
+        for (int j = 0; j < kTileItems; ++j) {
+            int li = j * kTileThreads + threadIdx.x;
+            if (li < cnt) {
+                k[j] = src[base + li];
+                r[j] = atomicAdd(&h[(unsigned)(k[j] >> sg.shift) & mask], 1u);
+            }
+        }
+        __syncthreads();
+        {
+            uint32_t v = threadIdx.x < kRadix ? h[threadIdx.x] : 0u, tot;
+            uint32_t ex = dev::block_excl_scan(v, scan_tmp, tot);
+            if (threadIdx.x < kRadix) {
+                lstart[threadIdx.x] = ex;
+                const size_t hb = (size_t)seg_tile0[si] * kRadix;
+                // off is relative to the concatenation of active segments
+                gbase[threadIdx.x] = sg.start + (off[hb + (size_t)threadIdx.x * seg_nt + ti] - e0);
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < kTileItems; ++j) {
+            int li = j * kTileThreads + threadIdx.x;
+            if (li < cnt) skeys[lstart[(unsigned)(k[j] >> sg.shift) & mask] + r[j]] = k[j];
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < cnt; i += kTileThreads) {
+            uint64_t key = skeys[i];
+            unsigned d = (unsigned)(key >> sg.shift) & mask;
+            dst[gbase[d] + (i - lstart[d])] = key;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void classify_kernel(const Seg* __restrict__ active, const uint32_t* __restrict__ n_active,
+                                const uint32_t* __restrict__ seg_tile0,
+                                const uint64_t* __restrict__ seg_elem0,
+                                const uint32_t* __restrict__ off, Seg* __restrict__ next,
+                                uint32_t* __restrict__ n_next, Seg* __restrict__ fin,
+                                uint32_t* __restrict__ n_fin) {
+    const uint32_t na = *n_active;
+    for (uint32_t si = blockIdx.x; si < na; si += gridDim.x) {
+        const Seg sg = active[si];
+        const uint32_t seg_nt = seg_tile0[si + 1] - seg_tile0[si];
+        const size_t hb = (size_t)seg_tile0[si] * kRadix;
+        const uint64_t e0 = seg_elem0[si];
+        const int nd = 1 << sg.bits;
+        for (int d = threadIdx.x; d < nd; d += blockDim.x) {
+            const uint64_t st = off[hb + (size_t)d * seg_nt] - e0;
+            const uint64_t en = d + 1 < nd ? off[hb + (size_t)(d + 1) * seg_nt] - e0 : sg.size;
+            const uint32_t sz = (uint32_t)(en - st);
+            if (sz == 0) continue;
+            Seg c;
+            c.start = sg.start + st;
+            c.size = sz;
+            c.buf = (uint8_t)(sg.buf ^ 1);
+            const int nb = sg.shift >= 8 ? 8 : sg.shift;
+            c.bits = (uint8_t)nb;
+            c.shift = (uint16_t)(sg.shift - nb);
+            if (sz <= (uint32_t)kLocalCap || nb == 0) fin[atomicAdd(n_fin, 1u)] = c;
+            else next[atomicAdd(n_next, 1u)] = c;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Host side
+// ---------------------------------------------------------------------------
+size_t local_smem_bytes() { return sizeof(LocalSmem); }
+
+void sort_workspace_init(SortWorkspace& ws, size_t n, cudaStream_t s) {
+    if (ws.n >= n && ws.keys[0].get()) return;
+    ws.n = n;
+    const uint32_t t1 = div_up(n, kTile);
+    ws.max_active = (uint32_t)(n / kLocalCap + 2);
+    ws.max_tiles = t1 + ws.max_active;
+    ws.max_fin = (uint32_t)std::min<uint64_t>(n + kRadix, (uint64_t)kRadix * ws.max_active + kRadix);
+    ws.keys[0] = DevBuf<uint64_t>(n, s);
+    ws.keys[1] = DevBuf<uint64_t>(n, s);
+    const size_t hsz = (size_t)kRadix * ws.max_tiles;
+    ws.hist = DevBuf<uint32_t>(hsz, s);
+    ws.off = DevBuf<uint32_t>(hsz, s);
+    ws.lists[0] = DevBuf<Seg>(ws.max_active, s);
+    ws.lists[1] = DevBuf<Seg>(ws.max_active, s);
+    ws.fin = DevBuf<Seg>(ws.max_fin, s);
+    ws.counters = DevBuf<uint32_t>(8, s);
+    ws.tile_seg = DevBuf<uint32_t>(ws.max_tiles, s);
+    ws.tile_idx = DevBuf<uint32_t>(ws.max_tiles, s);
+    ws.seg_tile0 = DevBuf<uint32_t>(ws.max_active + 1, s);
+    ws.seg_elem0 = DevBuf<uint64_t>(ws.max_active + 1, s);
+}
+
+void run_segmented_levels(SortWorkspace& ws, int levels_left, cudaStream_t s) {
+    static bool attr_set = false;
+    const size_t smem = (size_t)kTile * sizeof(uint64_t);
+    if (!attr_set) {
+        PRG_CUDA(cudaFuncSetAttribute(seg_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+        attr_set = true;
+    }
+    const unsigned grid = (unsigned)num_sms() * 4;
+    uint32_t* cnt = ws.counters.get();
+    for (int lvl = 0; lvl < levels_left; ++lvl) {
+        const int a = lvl & 1;
+        Seg* act = ws.lists[a].get();
+        Seg* nxt = ws.lists[a ^ 1].get();
+        uint32_t* n_act = cnt + a;
+        uint32_t* n_nxt = cnt + (a ^ 1);
+        PRG_CUDA(cudaMemsetAsync(n_nxt, 0, sizeof(uint32_t), s));
+        build_tiles_kernel<<<1, 1024, 0, s>>>(act, n_act, ws.seg_tile0.get(), ws.seg_elem0.get(),
+                                              ws.tile_seg.get(), ws.tile_idx.get(), cnt + 4,
+                                              ws.max_tiles);
+        PRG_LAUNCH_CHECK();
+        // Tiles beyond n_tiles are never read; only the used prefix of hist
+        // matters, but the scan runs over the capacity, so clear it.
+        const size_t hsz = (size_t)kRadix * ws.max_tiles;
+        PRG_CUDA(cudaMemsetAsync(ws.hist.get(), 0, hsz * sizeof(uint32_t), s));
+        seg_hist_kernel<<<grid, kTileThreads, 0, s>>>(ws.keys[0].get(), ws.keys[1].get(), act,
+                                                      ws.seg_tile0.get(), ws.tile_seg.get(),
+                                                      ws.tile_idx.get(), cnt + 4, ws.hist.get());
+        PRG_LAUNCH_CHECK();
+        exclusive_scan_u32(ws.hist.get(), ws.off.get(), hsz, nullptr, s);
+        seg_scatter_kernel<<<grid, kTileThreads, smem, s>>>(
+            ws.keys[0].get(), ws.keys[1].get(), ws.keys[0].get(), ws.keys[1].get(), act,
+            ws.seg_tile0.get(), ws.seg_elem0.get(), ws.tile_seg.get(), ws.tile_idx.get(), cnt + 4,
+            ws.off.get());
+        PRG_LAUNCH_CHECK();
+        classify_kernel<<<grid, kRadix, 0, s>>>(act, n_act, ws.seg_tile0.get(), ws.seg_elem0.get(),
+                                                 ws.off.get(), nxt, n_nxt, ws.fin.get(), cnt + 2);
+        PRG_LAUNCH_CHECK();
+    }
+}
+
+}  // namespace prg::sort

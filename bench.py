@@ -1,0 +1,394 @@
+#!/usr/bin/env python
+"""bench.py — PageRank Pipeline hot path (K1 sort -> K2 filter -> K3 PageRank) on B200.
+
+Metric (BASELINE.json): "K3 PageRank edges/s (M x 20 iters), K1/K2 edges/s; % of HBM
+roofline, 1 B200". Workload: Kronecker S=24 (N=2^24, M=2^28), Graph500 initiator,
+seed 1, K3 seed 1, c=0.85, 20 iterations — the SURVEY's headline roofline config.
+
+One step = K1 (device sort of the K0 edge list) + K2 (filter/normalise) + K3 (20
+iterations incl. init and the CSR->CSC transpose), inputs resident in HBM; each
+stage timed with CUDA events on the launching stream. `value` = whole-job K3
+edges/s (20*M per step per rank / max-over-ranks K3 time). Inputs (4.3 GB edge
+list, 3.1 GB CSR) exceed the 126 MB L2, so no L2 flush is needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--scale S]
+
+--impl reference times the reference's own single-threaded CPU code (built from
+/root/reference sources into oracle/_ref by oracle/build_ref.sh) on the same
+workload: its K0/K1/K2 prepare the S=24 matrix (K1/K2 timed once), each step runs
+its run_kernel3 with a bounded iteration count.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+GRAPH500 = (0.57, 0.19, 0.19, 0.05)
+METRIC = "K3 PageRank edges/s (M×20 iters), K1/K2 edges/s; % of HBM roofline, 1 B200"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--scale", type=int, default=24)
+    p.add_argument("--seed", type=int, default=1)
+    p.add_argument("--iterations", type=int, default=20)
+    p.add_argument("--e2e-steps", type=int, default=3)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--ref-iters-per-step", type=int, default=2)
+    return p.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def alg_bytes(n, m, nnz, iters):
+    """SURVEY §8(d) algorithmic (compulsory) bytes."""
+    k1 = 32 * m
+    k2 = 16 * m + 4 * (n + 1) + 12 * nnz
+    k3_iter = 4 * (n + 1) + 12 * nnz + 16 * n
+    k3 = iters * k3_iter + 8 * n
+    return k1, k2, k3, k3_iter
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        return self.summary()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if len(r) > 8 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 8 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) > 8:
+                for k, nm in enumerate(names):
+                    if r[5 + k].lower() == "active":
+                        reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def dist_setup():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ---------------------------------------------------------------------------
+# Our arm
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1603_01876_b200 import capi
+
+    ws, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    S, seed, iters = args.scale, args.seed, args.iterations
+    n = 1 << S
+    m = 16 * n
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+
+    # K0 (untimed input preparation): device restatement of the reference generator.
+    uv = capi.k0_generate(S, seed, GRAPH500)
+    sorted_uv = torch.empty_like(uv)
+    ranks = torch.empty(n, dtype=torch.float64, device=dev)
+    L = capi.lib()
+
+    def one_step(record):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ev[0].record(stream)
+        capi.k1_sort(uv, S, out=sorted_uv, stream=stream)
+        ev[1].record(stream)
+        mat = capi.k2_filter(sorted_uv, n, stream=stream)
+        ev[2].record(stream)
+        _, norm = capi.k3_pagerank(mat, seed=seed, iterations=iters, mode=0, out=ranks, stream=stream)
+        ev[3].record(stream)
+        info = (mat.nnz, mat.nnz_raw, mat.max_in, norm)
+        if record is not None:
+            record.append((ev, info))
+        return mat
+
+    for _ in range(args.warmup):
+        one_step(None).close()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    L.prg_profile_report(None, 0, 1)  # reset
+    L.prg_profile_enable(1)
+    launches0 = L.prg_launch_count()
+    rec = []
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    mats = []
+    for _ in range(args.steps):
+        mat = one_step(rec)
+        mat.close()
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    launches = L.prg_launch_count() - launches0
+    L.prg_profile_enable(0)
+    buf = (__import__("ctypes").c_char * 65536)()
+    L.prg_profile_report(buf, 65536, 1)
+    prof = json.loads(buf.value.decode())
+    clk = clocks.stop()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    k1 = [e[0].elapsed_time(e[1]) for e, _ in rec]
+    k2 = [e[1].elapsed_time(e[2]) for e, _ in rec]
+    k3 = [e[2].elapsed_time(e[3]) for e, _ in rec]
+    total_ms = t_start.elapsed_time(t_end)
+    nnz, nnz_raw, max_in, norm = rec[-1][1]
+    loc = np.array([np.mean(k1), np.mean(k2), np.mean(k3), total_ms / args.steps], dtype=np.float64)
+    if ws > 1:
+        t = torch.tensor(loc, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        loc = t.cpu().numpy()
+    k1_ms, k2_ms, k3_ms, step_ms = (float(x) for x in loc)
+
+    peak, peak_src = peaks()
+    b1, b2, b3, b3_iter = alg_bytes(n, m, nnz, iters)
+    spmv_n, spmv_ms = prof.get("k3_spmv", [0, 0.0])
+    spmv_avg = spmv_ms / max(spmv_n, 1)
+    achieved = b3_iter / (spmv_avg * 1e-3) / 1e9 if spmv_avg else None
+    value = ws * iters * m / (k3_ms * 1e-3)
+
+    out = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "edges/s",
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": step_ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (reference K0 Kronecker generator restated on device, seed 1)",
+        "config": {"workload": f"kronecker_s{S}_seed{seed}_k1k2k3", "scale": S, "vertices": n, "edges": m,
+                   "nnz_filtered": nnz, "nnz_raw": nnz_raw, "max_in_degree": max_in, "iterations": iters,
+                   "damping": 0.85, "k3_seed": seed, "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
+                   "l2": "inputs larger than L2 (4.3 GB edges, 3.1 GB CSR); no flush",
+                   "k3_mode": "timed (deterministic tree sums)"},
+        "k1_edges_per_s": ws * m / (k1_ms * 1e-3),
+        "k2_edges_per_s": ws * m / (k2_ms * 1e-3),
+        "k3_edges_per_s": value,
+        "stage_ms": {"k1_sort": k1_ms, "k2_filter": k2_ms, "k3_pagerank": k3_ms},
+        "final_norm1": norm,
+        "roofline": {"bound": "hbm", "kernel": "k3_spmv (spmv_pull_kernel, one PageRank iteration)",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak if achieved else None, "traffic": None,
+                     "alg_bytes_per_launch": b3_iter, "avg_launch_ms": spmv_avg, "peak_source": peak_src},
+        "stage_roofline": {
+            "k1_sort": {"alg_bytes": b1, "achieved_gbs": b1 / (k1_ms * 1e-3) / 1e9,
+                        "frac": b1 / (k1_ms * 1e-3) / 1e9 / peak},
+            "k2_filter": {"alg_bytes": b2, "achieved_gbs": b2 / (k2_ms * 1e-3) / 1e9,
+                          "frac": b2 / (k2_ms * 1e-3) / 1e9 / peak},
+            "k3_pagerank": {"alg_bytes": b3, "achieved_gbs": b3 / (k3_ms * 1e-3) / 1e9,
+                            "frac": b3 / (k3_ms * 1e-3) / 1e9 / peak},
+        },
+        "kernel_ms": {k: {"launches": v[0], "total_ms": v[1], "avg_ms": v[1] / max(v[0], 1)} for k, v in prof.items()},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+
+    # ---- e2e: host-buffer C-ABI (pinned), H2D + K3 + D2H inside the timed region
+    if rank == 0 or ws > 1:
+        import torch
+
+        mat = capi.k2_filter(sorted_uv, n, stream=stream)
+        ro = torch.empty(n + 1, dtype=torch.int64).pin_memory()
+        cols = torch.empty(max(mat.nnz, 1), dtype=torch.int64).pin_memory()
+        vals = torch.empty(max(mat.nnz, 1), dtype=torch.float64).pin_memory()
+        din = torch.empty(n, dtype=torch.int64).pin_memory()
+        rk = torch.empty(n, dtype=torch.float64).pin_memory()
+        capi._check(L.prg_matrix_download(mat.handle, ro.data_ptr(), cols.data_ptr(), vals.data_ptr(), din.data_ptr()))
+        mat.close()
+        import ctypes as C
+
+        e2e = []
+        for i in range(args.e2e_steps + 1):
+            nrm = C.c_double()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            capi._check(L.prg_k3_pagerank_host(n, nnz, ro.data_ptr(), cols.data_ptr(), vals.data_ptr(), 0.85, iters,
+                                               seed, 0, rk.data_ptr(), C.byref(nrm)))
+            t1 = time.perf_counter()
+            if i > 0:
+                e2e.append(t1 - t0)
+        e2e_t = float(np.mean(e2e))
+        if ws > 1:
+            t = torch.tensor([e2e_t], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_t = float(t.item())
+        out["e2e"] = {"value": ws * iters * m / e2e_t, "unit": "edges/s",
+                      "h2d_bytes_per_step": 8 * (n + 1) + 16 * nnz, "d2h_bytes_per_step": 8 * n,
+                      "api": "prg_k3_pagerank_host (C-ABI, pinned host CSR in, ranks out)",
+                      "seconds_per_step": e2e_t}
+
+        # ---- CPU baseline: the reference's run_kernel3 on the same S=24 CSR
+        if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(ro.numpy(), cols.numpy()[:nnz], vals.numpy()[:nnz], n, m, seed)
+
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+def cpu_baseline(ro, cols, vals, n, m, seed, iters=2):
+    """Reference run_kernel3 (oracle/_ref, built from the reference sources) on the
+    S=24 CSR our K2 produced (bit-identical to the reference's K2 output)."""
+    from oracle import oracle as O  # checker/baseline only
+
+    kind = "reference" if O.have_reference() else "port"
+    t0 = time.perf_counter()
+    if kind == "reference":
+        _, _, el = O.ref_run_kernel3(ro, cols, vals, n, iterations=iters, seed=seed, total_edges=m)
+    else:
+        O.run_kernel3(ro, cols, vals, n, iterations=iters, seed=seed)
+        el = time.perf_counter() - t0
+    return {"value": iters * m / el, "unit": "edges/s", "cores": 1, "kind": kind,
+            "sample": f"S=24 CSR (nnz={len(cols)}), run_kernel3 with {iters} of 20 iterations (init_rank "
+                      f"included), single thread: the reference has no threads",
+            "seconds": el, "host_cpu": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip() + f" x{os.cpu_count()} logical"
+    except Exception:
+        pass
+    return "unknown"
+
+
+# ---------------------------------------------------------------------------
+# Reference arm
+# ---------------------------------------------------------------------------
+def run_reference(args):
+    ws, rank, _ = dist_setup()
+    if rank != 0:
+        return
+    from oracle import oracle as O
+
+    S, seed = args.scale, args.seed
+    n = 1 << S
+    m = 16 * n
+    if not O.have_reference():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libprpipe_ref.so not built"}))
+        return
+    uv = O.ref_generate(S, seed, GRAPH500, threads=os.cpu_count())        # K0 (untimed)
+    srt, k1_s = O.ref_k1_sort_core(uv)                                     # K1 core, timed once
+    del uv
+    k2r, k2_s = O.ref_k2(srt, n)                                           # K2 core, timed once
+    del srt
+    it = args.ref_iters_per_step
+    rates = []
+    for i in range(args.warmup + args.steps):
+        _, _, el = O.ref_run_kernel3(k2r.row_offsets, k2r.cols, k2r.values, n, iterations=it, seed=seed,
+                                     total_edges=m)
+        if i >= args.warmup:
+            rates.append(it * m / el)
+    value = float(np.mean(rates))
+    out = {
+        "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": it * m / value * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference K0, seed 1)",
+        "impl": "reference",
+        "config": {"workload": f"kronecker_s{S}_seed{seed}_k1k2k3", "scale": S, "vertices": n, "edges": m,
+                   "nnz_filtered": k2r.nnz, "iterations": 20, "damping": 0.85,
+                   "step": f"run_kernel3 with {it} iterations (bounded sample of the 20-iteration run)"},
+        "k1_edges_per_s": m / k1_s, "k2_edges_per_s": m / k2_s, "k3_edges_per_s": value,
+        "cpu_baseline": {"value": value, "unit": "edges/s", "cores": 1, "kind": "reference",
+                         "sample": f"S={S}: K1 std::sort + K2 core once on the full list; K3 run_kernel3 x{it} "
+                                   f"iterations per step", "host_cpu": _cpu_model()},
+        "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -45,6 +45,15 @@ const char* prg_last_error(void);
 const char* prg_version(void);
 int32_t prg_device_count(void);
 
+/* Instrumentation (no reference counterpart; the reference times with
+ * prpipe::Timer, include/prpipe/timer.hpp:9-19). prg_launch_count: kernels the
+ * library has launched since load. prg_profile_*: CUDA-event timing of named
+ * regions (k1_sort, k2_filter, k3_spmv, ...) on the stream they ran on;
+ * report writes JSON {"name": [count, total_ms]} and returns its length. */
+int64_t prg_launch_count(void);
+void prg_profile_enable(int32_t on);
+int64_t prg_profile_report(char* buf, int64_t cap, int32_t reset);
+
 /* ---- K0 (input generation; untimed) ------------------------------------
  * Device restatement of EdgeGenerator::make_edge (src/graph_gen.cpp:83-99):
  * edges [first, first+count) of the K0 list for (scale, seed, initiator).

@@ -96,6 +96,18 @@ extern "C" {
 const char* prg_last_error(void) { return prg::last_error().c_str(); }
 const char* prg_version(void) { return "prg-b200 0.1.0 (sm_100a)"; }
 
+int64_t prg_launch_count(void) { return prg::launch_count(); }
+void prg_profile_enable(int32_t on) { prg::profiling_enable(on != 0); }
+int64_t prg_profile_report(char* buf, int64_t cap, int32_t reset) {
+    const std::string s = prg::profile_report(reset != 0);
+    if (buf && cap > 0) {
+        const size_t k = std::min<size_t>((size_t)cap - 1, s.size());
+        std::memcpy(buf, s.data(), k);
+        buf[k] = 0;
+    }
+    return (int64_t)s.size();
+}
+
 int32_t prg_device_count(void) {
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;

@@ -29,7 +29,28 @@ struct CudaError {
                                    " (" __FILE__ ":" + std::to_string(__LINE__) + ")"}; \
     } while (0)
 
-#define PRG_LAUNCH_CHECK() PRG_CUDA(cudaGetLastError())
+// Every launch site goes through PRG_LAUNCH_CHECK, which also counts launches
+// (prg_launch_count(): bench.py's "gpu_launches").
+void count_launch();
+#define PRG_LAUNCH_CHECK()         \
+    do {                           \
+        ::prg::count_launch();     \
+        PRG_CUDA(cudaGetLastError()); \
+    } while (0)
+
+// Optional CUDA-event timing of named regions on their stream (prg_profile_*).
+// Costs two event records per scope when enabled, nothing otherwise.
+bool profiling_enabled();
+void profiling_enable(bool on);
+long long launch_count();
+std::string profile_report(bool reset);  // {"name": [count, total_ms], ...}
+struct ProfScope {
+    const char* name;
+    cudaStream_t s;
+    cudaEvent_t a = nullptr, b = nullptr;
+    ProfScope(const char* n, cudaStream_t st);
+    ~ProfScope();
+};
 
 __host__ __device__ inline unsigned div_up(uint64_t a, uint64_t b) { return static_cast<unsigned>((a + b - 1) / b); }
 

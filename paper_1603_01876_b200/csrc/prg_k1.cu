@@ -42,6 +42,7 @@ struct PairSink {
 void k1_sort_device(const int64_t* d_uv_in, int64_t m, int scale, int64_t* d_uv_out,
                     uint32_t* d_err, cudaStream_t s) {
     if (m == 0) return;
+    ProfScope prof("k1_sort", s);
     const uint64_t n = 1ull << scale;
     PairKeySrc src{reinterpret_cast<const longlong2*>(d_uv_in), n, scale, d_err};
     PairSink dst{reinterpret_cast<longlong2*>(d_uv_out), scale, n - 1};

@@ -360,6 +360,7 @@ __global__ void k2_fix_rows(const uint32_t* __restrict__ fix_rows, const uint32_
 }  // namespace
 
 uint32_t k2_filter_device(const int64_t* d_uv, int64_t m, int64_t n, prg_matrix* out, cudaStream_t s) {
+    ProfScope prof("k2_filter", s);
     out->n = n;
     out->cap = (uint64_t)(m > 0 ? m : 1);
     out->row_offsets = static_cast<uint32_t*>(ws_alloc((size_t)(n + 1) * 4, s));
@@ -390,8 +391,11 @@ uint32_t k2_filter_device(const int64_t* d_uv, int64_t m, int64_t n, prg_matrix*
         attr = true;
     }
     const unsigned ga = std::min<unsigned>(ntiles, (unsigned)num_sms() * 2);
-    k2_pass_a<<<ga, kT, sizeof(EdgeSmem), s>>>(uv, m, n, out->d_in, err, nnz_raw, ntiles);
-    PRG_LAUNCH_CHECK();
+    {
+        ProfScope pa("k2_pass_a", s);
+        k2_pass_a<<<ga, kT, sizeof(EdgeSmem), s>>>(uv, m, n, out->d_in, err, nnz_raw, ntiles);
+        PRG_LAUNCH_CHECK();
+    }
     uint32_t h_err = 0;
     PRG_CUDA(cudaMemcpyAsync(&h_err, err, 4, cudaMemcpyDeviceToHost, s));
     PRG_CUDA(cudaStreamSynchronize(s));
@@ -420,10 +424,13 @@ uint32_t k2_filter_device(const int64_t* d_uv, int64_t m, int64_t n, prg_matrix*
     DevBuf<uint32_t> dout_f((size_t)n, s), fix_rows(ntiles + 1, s), cont_p(ntiles, s), cont_c(ntiles, s);
     PRG_CUDA(cudaMemsetAsync(tile_status.get(), 0, (size_t)ntiles * 8, s));
     PRG_CUDA(cudaMemsetAsync(dout_f.get(), 0, (size_t)n * 4, s));
-    k2_pass_b<<<ntiles, kT, sizeof(PassBSmem), s>>>(uv, m, n, keepbits.get(), out->row_offsets, out->cols,
-                                                    out->values, tile_status.get(), tile_counter, dout_f.get(),
-                                                    fix_rows.get(), n_fix, cont_p.get(), cont_c.get(), nnz_out);
-    PRG_LAUNCH_CHECK();
+    {
+        ProfScope pb("k2_pass_b", s);
+        k2_pass_b<<<ntiles, kT, sizeof(PassBSmem), s>>>(uv, m, n, keepbits.get(), out->row_offsets, out->cols,
+                                                        out->values, tile_status.get(), tile_counter, dout_f.get(),
+                                                        fix_rows.get(), n_fix, cont_p.get(), cont_c.get(), nnz_out);
+        PRG_LAUNCH_CHECK();
+    }
     k2_fix_runs<<<div_up(ntiles, 256), 256, 0, s>>>(cont_p.get(), cont_c.get(), ntiles, out->values);
     PRG_LAUNCH_CHECK();
     k2_fix_rows<<<(unsigned)num_sms() * 2, 256, 0, s>>>(fix_rows.get(), n_fix, out->row_offsets, dout_f.get(),

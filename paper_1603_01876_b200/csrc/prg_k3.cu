@@ -529,6 +529,7 @@ struct K3Plan {
 };
 
 void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
+    ProfScope prof("k3_prep", s);
     const int64_t n = A->n;
     const uint64_t nnz = A->nnz;
     P.n = n;
@@ -667,6 +668,7 @@ void step_impl(const K3Plan& P, const double* r_prev, double* r_next, double dam
                double* s_buf, Sums& S, DevBuf<double>& task_sum, DevBuf<uint32_t>& counter, cudaStream_t s) {
     const unsigned g = (unsigned)num_sms() * 8;
     if (P.n_nd) {
+        ProfScope pp("k3_permute", s);
         permute_scale_kernel<<<g, 1024, 0, s>>>(r_prev, P.pinv.get(), P.bval.get(), P.n_nd, s_buf);
         PRG_LAUNCH_CHECK();
     }
@@ -700,8 +702,11 @@ void step_impl(const K3Plan& P, const double* r_prev, double* r_next, double dam
             attr = true;
         }
         PRG_CUDA(cudaMemsetAsync(counter.get(), 0, 4, s));
-        spmv_pull_kernel<<<num_sms(), kSpmvThreads, spmv_smem(), s>>>(a);
-        PRG_LAUNCH_CHECK();
+        {
+            ProfScope ps("k3_spmv", s);
+            spmv_pull_kernel<<<num_sms(), kSpmvThreads, spmv_smem(), s>>>(a);
+            PRG_LAUNCH_CHECK();
+        }
         final_sum_kernel<<<1, 1024, 0, s>>>(task_sum.get(), ntasks, bgf, S.out.get());
         PRG_LAUNCH_CHECK();
     }
@@ -716,6 +721,7 @@ double k3_init_rank_device(int64_t n, uint64_t seed, double* d_r, int mode, cuda
 }
 
 double k3_pagerank_device(const prg_matrix* A, const K3Options& opt, double* d_ranks, cudaStream_t s) {
+    ProfScope prof("k3_pagerank", s);
     const int64_t n = A->n;
     const double bgf = (1.0 - opt.damping) / (double)n;  // kernel3_pagerank.cpp:46
     K3Plan P;

@@ -1,5 +1,8 @@
 // prg_runtime.cu — error channel, stream-ordered workspace, device-wide scan.
+#include <atomic>
+#include <map>
 #include <mutex>
+#include <vector>
 
 #include "prg_common.cuh"
 
@@ -11,6 +14,59 @@ std::once_flag g_pool_once;
 }  // namespace
 
 void set_error(const std::string& msg) { g_last_error = msg; }
+
+// ---- launch counter and profiling ------------------------------------------
+namespace {
+std::atomic<long long> g_launches{0};
+std::atomic<bool> g_prof{false};
+std::mutex g_prof_mu;
+struct ProfRec { std::string name; cudaEvent_t a, b; };
+std::vector<ProfRec> g_prof_pending;
+std::map<std::string, std::pair<long long, double>> g_prof_totals;
+}  // namespace
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+long long launch_count() { return g_launches.load(); }
+bool profiling_enabled() { return g_prof.load(std::memory_order_relaxed); }
+void profiling_enable(bool on) { g_prof.store(on); }
+
+ProfScope::ProfScope(const char* n, cudaStream_t st) : name(n), s(st) {
+    if (!profiling_enabled()) return;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, s);
+}
+ProfScope::~ProfScope() {
+    if (!a) return;
+    cudaEventRecord(b, s);
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof_pending.push_back({name, a, b});
+}
+
+std::string profile_report(bool reset) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    for (auto& p : g_prof_pending) {
+        cudaEventSynchronize(p.b);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, p.a, p.b);
+        auto& t = g_prof_totals[p.name];
+        t.first += 1;
+        t.second += ms;
+        cudaEventDestroy(p.a);
+        cudaEventDestroy(p.b);
+    }
+    g_prof_pending.clear();
+    std::string out = "{";
+    bool first = true;
+    for (auto& [k, v] : g_prof_totals) {
+        if (!first) out += ", ";
+        first = false;
+        out += "\"" + k + "\": [" + std::to_string(v.first) + ", " + std::to_string(v.second) + "]";
+    }
+    out += "}";
+    if (reset) g_prof_totals.clear();
+    return out;
+}
 const std::string& last_error() { return g_last_error; }
 
 int num_sms() {

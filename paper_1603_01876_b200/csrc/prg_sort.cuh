@@ -424,30 +424,41 @@ void msd_sort_split(Src src_hist, Src src_scat, size_t n, int key_bits, Dst dst,
     const uint32_t ntiles = div_up(n, kTile);
     const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)num_sms() * 4);
     PRG_CUDA(cudaMemsetAsync(ws.counters.get(), 0, 8 * sizeof(uint32_t), s));
-    if (Src::kSmem > 48 * 1024)
-        PRG_CUDA(cudaFuncSetAttribute(l1_hist_kernel<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)Src::kSmem));
-    l1_hist_kernel<Src><<<grid, kTileThreads, Src::kSmem, s>>>(src_hist, n, shift1, dmask, ntiles, ws.hist.get());
-    PRG_LAUNCH_CHECK();
-    exclusive_scan_u32(ws.hist.get(), ws.off.get(), (size_t)kRadix * ntiles, nullptr, s);
-    const size_t smem = (size_t)kTile * sizeof(uint64_t) + Src::kSmem;
-    PRG_CUDA(cudaFuncSetAttribute(l1_scatter_kernel<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
-    l1_scatter_kernel<Src><<<grid, kTileThreads, smem, s>>>(src_scat, n, shift1, dmask, ntiles,
-                                                            ws.off.get(), ws.keys[1].get());
-    PRG_LAUNCH_CHECK();
-    classify_l1_kernel<<<1, kRadix, 0, s>>>(ws.off.get(), ntiles, n, shift1,
-                                             shift1 >= 8 ? 8 : shift1, ws.lists[0].get(),
-                                             ws.counters.get() + 0, ws.fin.get(),
-                                             ws.counters.get() + 2);
-    PRG_LAUNCH_CHECK();
-    run_segmented_levels(ws, (shift1 + 7) / 8, s);
-    PRG_CUDA(cudaFuncSetAttribute(local_sort_kernel<Dst>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)local_smem_bytes()));
-    local_sort_kernel<Dst><<<num_sms(), kLocalThreads, local_smem_bytes(), s>>>(
-        ws.keys[0].get(), ws.keys[1].get(), ws.fin.get(), ws.counters.get() + 2,
-        ws.counters.get() + 3, dst);
-    PRG_LAUNCH_CHECK();
+    {
+        ProfScope prof("sort_l1_hist", s);
+        if (Src::kSmem > 48 * 1024)
+            PRG_CUDA(cudaFuncSetAttribute(l1_hist_kernel<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)Src::kSmem));
+        l1_hist_kernel<Src><<<grid, kTileThreads, Src::kSmem, s>>>(src_hist, n, shift1, dmask, ntiles,
+                                                                    ws.hist.get());
+        PRG_LAUNCH_CHECK();
+        exclusive_scan_u32(ws.hist.get(), ws.off.get(), (size_t)kRadix * ntiles, nullptr, s);
+    }
+    {
+        ProfScope prof("sort_l1_scatter", s);
+        const size_t smem = (size_t)kTile * sizeof(uint64_t) + Src::kSmem;
+        PRG_CUDA(cudaFuncSetAttribute(l1_scatter_kernel<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+        l1_scatter_kernel<Src><<<grid, kTileThreads, smem, s>>>(src_scat, n, shift1, dmask, ntiles,
+                                                                ws.off.get(), ws.keys[1].get());
+        PRG_LAUNCH_CHECK();
+        classify_l1_kernel<<<1, kRadix, 0, s>>>(ws.off.get(), ntiles, n, shift1, shift1 >= 8 ? 8 : shift1,
+                                                 ws.lists[0].get(), ws.counters.get() + 0, ws.fin.get(),
+                                                 ws.counters.get() + 2);
+        PRG_LAUNCH_CHECK();
+    }
+    {
+        ProfScope prof("sort_levels", s);
+        run_segmented_levels(ws, (shift1 + 7) / 8, s);
+    }
+    {
+        ProfScope prof("sort_local", s);
+        PRG_CUDA(cudaFuncSetAttribute(local_sort_kernel<Dst>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)local_smem_bytes()));
+        local_sort_kernel<Dst><<<num_sms(), kLocalThreads, local_smem_bytes(), s>>>(
+            ws.keys[0].get(), ws.keys[1].get(), ws.fin.get(), ws.counters.get() + 2, ws.counters.get() + 3, dst);
+        PRG_LAUNCH_CHECK();
+    }
 }
 
 template <class Src, class Dst>

@@ -45,10 +45,10 @@ void profiling_enable(bool on);
 long long launch_count();
 std::string profile_report(bool reset);  // {"name": [count, total_ms], ...}
 struct ProfScope {
-    const char* name;
+    std::string name;
     cudaStream_t s;
     cudaEvent_t a = nullptr, b = nullptr;
-    ProfScope(const char* n, cudaStream_t st);
+    ProfScope(std::string n, cudaStream_t st);
     ~ProfScope();
 };
 
@@ -178,6 +178,32 @@ __device__ __forceinline__ uint4 ld_stream_u4(const void* p, uint64_t pol) {
     asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
                  : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                  : "l"(p), "l"(pol));
+    return r;
+}
+// Predicated loads (no branch): return `dflt` when !pred. Non-volatile so the
+// compiler may batch them.
+__device__ __forceinline__ uint32_t ld_stream_u32_pred(const void* p, bool pred, uint64_t pol, uint32_t dflt) {
+    uint32_t r = dflt;
+    asm("{ .reg .pred q; setp.ne.u32 q, %2, 0;\n\t"
+        "@q ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %3; }"
+        : "+r"(r)
+        : "l"(p), "r"((uint32_t)pred), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ double ld_keep_f64_pred(const double* p, bool pred, uint64_t pol) {
+    double r = 0.0;
+    asm("{ .reg .pred q; setp.ne.u32 q, %2, 0;\n\t"
+        "@q ld.global.nc.L2::cache_hint.f64 %0, [%1], %3; }"
+        : "+d"(r)
+        : "l"(p), "r"((uint32_t)pred), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ double ld_f64_pred(const double* p, bool pred) {
+    double r = 0.0;
+    asm("{ .reg .pred q; setp.ne.u32 q, %2, 0;\n\t"
+        "@q ld.global.nc.f64 %0, [%1]; }"
+        : "+d"(r)
+        : "l"(p), "r"((uint32_t)pred));
     return r;
 }
 __device__ __forceinline__ double ld_keep_f64(const double* p, uint64_t pol) {

@@ -47,7 +47,15 @@ void k1_sort_device(const int64_t* d_uv_in, int64_t m, int scale, int64_t* d_uv_
     PairKeySrc src{reinterpret_cast<const longlong2*>(d_uv_in), n, scale, d_err};
     PairSink dst{reinterpret_cast<longlong2*>(d_uv_out), scale, n - 1};
     sort::SortWorkspace ws;
-    sort::msd_sort(src, (size_t)m, 2 * scale, dst, ws, s);
+    sort::msd_sort(src, (size_t)m, 2 * scale, dst, ws, s, "k1");
 }
 
 }  // namespace prg
+
+// Debug: local-stage statistics of the K1 sort (meaningful only when built
+// with -DPRG_LOCAL_STATS=1). Not part of include/prg.h.
+extern "C" void prg_debug_k1_local_stats(unsigned long long* out) {
+    cudaMemcpyFromSymbol(out, prg::sort::g_local_stats, sizeof(unsigned long long) * 16);
+    static const unsigned long long zero[16] = {};
+    cudaMemcpyToSymbol(prg::sort::g_local_stats, zero, sizeof(zero));
+}

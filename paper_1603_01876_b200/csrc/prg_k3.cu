@@ -24,6 +24,7 @@
 // in ascending u with separate mul/add, and computes every sum(r) with one
 // thread in index order — the reference's exact evaluation order.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "prg_internal.cuh"
@@ -391,113 +392,25 @@ __global__ void scale_kernel(double* __restrict__ x, int64_t n, const double* __
         x[i] = __ddiv_rn(x[i], d);
 }
 
-// s[j] = r[pinv[j]] * b[j]   (the reference's product r[u] * values[k], k non-exception)
-__global__ void permute_scale_kernel(const double* __restrict__ r, const uint32_t* __restrict__ pinv,
-                                     const double* __restrict__ bval, int64_t n_nd, double* __restrict__ s) {
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n_nd; j += (int64_t)gridDim.x * blockDim.x)
-        s[j] = __dmul_rn(r[pinv[j]], bval[j]);
-}
 
 // ---------------------------------------------------------------------------
-// Pull SpMV (timed mode): warp task = 32 consecutive columns, lane j owns column
-// cb+j. Entries are walked in 32-aligned slices; each lane finds its entry's
-// owner column by a 5-step shuffle search, products are reduced with a
-// segmented warp scan and delivered to the owner lane. All reductions have a
-// fixed shape, so results are bitwise reproducible.
+// Parity mode SpMV: one thread per column, ascending source order, separate
+// mul/add (kernel3_pagerank.cpp:50-61 evaluated in the reference's order).
 // ---------------------------------------------------------------------------
-struct SpmvArgs {
-    const uint32_t* colptr;    // [n+1]
-    const uint32_t* csc_idx;   // [nnz]
-    const uint32_t* exc_base;  // [ngroups]
-    const double* exc_val;
-    const double* s;           // [n_nd] gather vector
-    const double* r_prev;      // [n] previous iterate (original order) for exceptions
-    const uint32_t* pinv;
-    const double* bgp;         // device scalar: bg for this iteration (bgp[1])
-    double* r_next;            // [n]
-    double* task_sum;          // [ntasks]
-    uint32_t* task_counter;
+struct SeqArgs {
+    const uint32_t* colptr;
+    const uint32_t* csc_idx;
+    const uint32_t* exc_base;  // per 32-entry CSC group
+    const double* exc_val;     // CSC order
+    const double* s;           // s[u] = r[u] * b[u] (identity numbering)
+    const double* r_prev;      // original order
+    const double* bgp;
+    double* r_next;
     int64_t n;
-    int64_t n_nd;
-    uint32_t ntasks;
     double damping;
 };
 
-__global__ void __launch_bounds__(kSpmvThreads, 1) spmv_pull_kernel(SpmvArgs a) {
-    extern __shared__ __align__(16) double s_hot[];
-    const int64_t nh = a.n_nd < kHot ? a.n_nd : kHot;
-    for (int64_t i = threadIdx.x; i < nh; i += kSpmvThreads) s_hot[i] = a.s[i];
-    __syncthreads();
-    const unsigned lane = dev::lane_id();
-    const double bg = a.bgp[1];
-    const uint32_t lt_mask = (1u << lane) - 1u;
-    const uint64_t pol_stream = dev::policy_evict_first(), pol_keep = dev::policy_evict_last();
-    for (;;) {
-        uint32_t t = 0;
-        if (lane == 0) t = atomicAdd(a.task_counter, 1u);
-        t = __shfl_sync(0xffffffffu, t, 0);
-        if (t >= a.ntasks) break;
-        const int64_t c = (int64_t)t * 32 + lane;
-        const bool cvalid = c < a.n;
-        const uint32_t cb = a.colptr[cvalid ? c : a.n];
-        const uint32_t ce = a.colptr[cvalid ? c + 1 : a.n];
-        const uint32_t B = __shfl_sync(0xffffffffu, cb, 0);
-        const uint32_t E = __shfl_sync(0xffffffffu, ce, 31);
-        double acc = 0.0;
-        for (uint32_t base = B & ~31u; base < E; base += 32) {
-            const uint32_t e = base + lane;
-            const bool valid = e >= B && e < E;
-            const bool inr = e < E;  // group members for exception ranks (e >= base)
-            uint32_t w = inr ? dev::ld_stream_u32(a.csc_idx + e, pol_stream) : 0u;
-            // owner column: largest j with colptr[cb_j] <= e
-            int j = 0;
-#pragma unroll
-            for (int step = 16; step > 0; step >>= 1) {
-                const uint32_t bc = __shfl_sync(0xffffffffu, cb, j + step);
-                if (bc <= e) j += step;
-            }
-            const bool exc = (w >> 31) != 0;
-            const uint32_t excm = __ballot_sync(0xffffffffu, inr && exc);
-            double x = 0.0;
-            if (valid) {
-                const uint32_t u = w & 0x7fffffffu;
-                if (exc) {
-                    const uint32_t rank = a.exc_base[base / kCscGroup] + __popc(excm & lt_mask);
-                    x = __dmul_rn(a.r_prev[a.pinv[u]], a.exc_val[rank]);
-                } else {
-                    x = u < (uint32_t)nh ? s_hot[u] : dev::ld_keep_f64(a.s + u, pol_keep);
-                }
-            }
-            // segmented inclusive scan by owner
-            const int jj = valid ? j : (e < B ? -1 : 32);
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const double o = __shfl_up_sync(0xffffffffu, x, d);
-                const int oj = __shfl_up_sync(0xffffffffu, jj, d);
-                if ((int)lane >= d && oj == jj) x = __dadd_rn(x, o);
-            }
-            // deliver: owner lane gets the partial from its last entry in this slice
-            const uint32_t lo = cb > base ? cb : base;
-            const uint32_t hi = ce < base + 32 ? ce : base + 32;
-            const bool has = lo < hi;
-            const int src = has ? (int)(hi - 1 - base) : (int)lane;
-            const double part = __shfl_sync(0xffffffffu, x, src);
-            if (has) acc = __dadd_rn(acc, part);
-        }
-        double rn = 0.0;
-        if (cvalid) {
-            rn = __dadd_rn(__dmul_rn(a.damping, acc), bg);
-            a.r_next[c] = rn;
-        }
-        rn = dev::warp_sum_f64(rn);
-        if (lane == 0) a.task_sum[t] = rn;
-    }
-}
-
-// Parity mode: one thread per column, ascending source order, separate mul/add.
-__global__ void spmv_seq_kernel(SpmvArgs a) {
-    const uint32_t lt_dummy = 0;
-    (void)lt_dummy;
+__global__ void spmv_seq_kernel(SeqArgs a) {
     for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < a.n; c += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t b = a.colptr[c], e = a.colptr[c + 1];
         double acc = 0.0;
@@ -508,7 +421,7 @@ __global__ void spmv_seq_kernel(SpmvArgs a) {
             if (w >> 31) {
                 uint32_t rank = a.exc_base[p / kCscGroup];
                 for (uint32_t q = p & ~(uint32_t)(kCscGroup - 1); q < p; ++q) rank += a.csc_idx[q] >> 31;
-                x = __dmul_rn(a.r_prev[a.pinv[u]], a.exc_val[rank]);
+                x = __dmul_rn(a.r_prev[u], a.exc_val[rank]);
             } else {
                 x = a.s[u];
             }
@@ -518,6 +431,381 @@ __global__ void spmv_seq_kernel(SpmvArgs a) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Timed mode: sliced ELL over virtual columns (SELL-32-sigma).
+//
+// Every non-empty column is cut into parts of at most kVcMax entries ("virtual
+// columns"); virtual columns are ordered by quarter-octave length class
+// (descending) and packed 32 to a slice. Slice s stores entry k of its lane-j
+// virtual column at sell[slice_ptr[s] + 32k + j], so a warp reads 128
+// contiguous bytes per step and each lane sums its own column sequentially —
+// no owner search, no segmented scan, a fixed summation order. Parts of split
+// columns are combined, in part order, by whichever part finishes last.
+// Results y are kept in SELL position order; empty columns are implicit (their
+// value is bg), and only the final iterate is un-permuted.
+// ---------------------------------------------------------------------------
+constexpr uint32_t kVcMax = 2048;
+constexpr uint32_t kEmpty = 0xffffffffu;
+constexpr int kUnroll = 8;
+
+__device__ __forceinline__ uint32_t len_class_desc(uint32_t d) {
+    const int lg = 31 - __clz(d);
+    const uint32_t q = lg >= 2 ? (d >> (lg - 2)) & 3u : (lg == 1 ? (d & 1u) << 1 : 0u);
+    return 127u - (uint32_t)(lg * 4) - q;
+}
+
+__global__ void vc_count_kernel(const uint32_t* __restrict__ colptr, int64_t n, uint32_t* __restrict__ np) {
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t len = colptr[c + 1] - colptr[c];
+        np[c] = (len + kVcMax - 1) / kVcMax;
+    }
+}
+
+__global__ void vc_fill_kernel(const uint32_t* __restrict__ colptr, const uint32_t* __restrict__ vc_base, int64_t n,
+                               uint32_t* __restrict__ vc_col, uint32_t* __restrict__ vc_len) {
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t len = colptr[c + 1] - colptr[c];
+        for (uint32_t v = vc_base[c], p = 0; v < vc_base[c + 1]; ++v, ++p) {
+            vc_col[v] = (uint32_t)c;
+            vc_len[v] = min(kVcMax, len - p * kVcMax);
+        }
+    }
+}
+
+struct VcClassSrc {
+    const uint32_t* vc_len;
+    int vb;
+    static constexpr size_t kSmem = 0;
+    __device__ void prepare(size_t, int, void*) const {}
+    __device__ __forceinline__ uint64_t key(size_t i, int, const void*) const {
+        return ((uint64_t)len_class_desc(vc_len[i]) << vb) | i;
+    }
+};
+
+struct KeyArraySrc {
+    const unsigned long long* keys;
+    static constexpr size_t kSmem = 0;
+    __device__ void prepare(size_t, int, void*) const {}
+    __device__ __forceinline__ uint64_t key(size_t i, int, const void*) const { return keys[i]; }
+};
+
+__global__ void slice_size_kernel(const uint32_t* __restrict__ order, const uint32_t* __restrict__ vc_len, uint32_t V,
+                                  uint32_t nslices, uint32_t* __restrict__ slice_sz) {
+    const uint32_t lane = dev::lane_id();
+    for (uint32_t s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < nslices; s += (gridDim.x * blockDim.x) >> 5) {
+        const uint32_t pos = s * 32 + lane;
+        const uint32_t len = pos < V ? vc_len[order[pos]] : 0u;
+        const uint32_t mx = __reduce_max_sync(0xffffffffu, len);
+        if (lane == 0) slice_sz[s] = 32u * mx;
+    }
+}
+
+struct FillArgs {
+    const uint32_t* order;
+    const uint32_t* vc_col;
+    const uint32_t* vc_len;
+    const uint32_t* vc_base;
+    const uint32_t* colptr;
+    const uint32_t* csc_idx;
+    const uint32_t* slice_ptr;
+    uint32_t V, nslices;
+    uint32_t* sell;
+    uint32_t* exc_cnt;   // per SELL group of 32
+    uint32_t* lane_len;  // [nslices*32]
+    uint32_t* lane_col;  // [nslices*32]
+    uint32_t* lane_np;   // [nslices*32]
+    uint32_t* spos_col;  // [n] pos of part 0 (kEmpty if empty)
+};
+
+__global__ void sell_fill_kernel(FillArgs a) {
+    const uint32_t lane = dev::lane_id();
+    for (uint32_t s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < a.nslices; s += (gridDim.x * blockDim.x) >> 5) {
+        const uint32_t pos = s * 32 + lane;
+        uint32_t len = 0, c = 0, np = 1, start = 0;
+        if (pos < a.V) {
+            const uint32_t v = a.order[pos];
+            c = a.vc_col[v];
+            len = a.vc_len[v];
+            const uint32_t part = v - a.vc_base[c];
+            np = a.vc_base[c + 1] - a.vc_base[c];
+            start = a.colptr[c] + part * kVcMax;
+            if (part == 0) a.spos_col[c] = pos;
+        }
+        a.lane_len[pos] = len;
+        a.lane_col[pos] = c;
+        a.lane_np[pos] = np;
+        const uint32_t base = a.slice_ptr[s];
+        const uint32_t rows = (a.slice_ptr[s + 1] - base) >> 5;
+        for (uint32_t k = 0; k < rows; ++k) {
+            const bool ok = k < len;
+            const uint32_t e = ok ? a.csc_idx[start + k] : 0u;
+            a.sell[base + 32 * k + lane] = e;
+            const uint32_t m = __ballot_sync(0xffffffffu, ok && (e >> 31));
+            if (lane == 0) a.exc_cnt[(base >> 5) + k] = __popc(m);
+        }
+    }
+}
+
+// Exceptions (entries whose value differs from the row base value, i.e.
+// duplicate edges) are summed per virtual column by a small kernel each
+// iteration, in a fixed order, and added once per column by the SpMV.
+// Prep: key (SELL lane position, source row) for every exception, sorted.
+__global__ void exc_pos_keys(const unsigned long long* __restrict__ exc_key, const uint32_t* __restrict__ n_exc,
+                             const uint32_t* __restrict__ colptr, const uint32_t* __restrict__ csc_idx,
+                             const uint32_t* __restrict__ vc_base, const uint32_t* __restrict__ vpos, int sb,
+                             unsigned long long* __restrict__ out) {
+    const uint32_t ne = *n_exc;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < ne; i += gridDim.x * blockDim.x) {
+        const uint64_t key = exc_key[i];
+        const uint32_t col = (uint32_t)(key >> (sb + 1));
+        const uint32_t nid = (uint32_t)((key >> 1) & ((1ull << sb) - 1));
+        uint32_t lo = colptr[col], hi = colptr[col + 1];
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if ((csc_idx[mid] & 0x7fffffffu) < nid) lo = mid + 1; else hi = mid;
+        }
+        const uint32_t pos = vpos[vc_base[col] + (lo - colptr[col]) / kVcMax];
+        out[i] = ((uint64_t)pos << 32) | nid;
+    }
+}
+
+// For sorted exception i: source row, value (from the CSC-order exception
+// values), and its lane position; flags lanes that have exceptions.
+struct ExcResolveDst {
+    const uint32_t* lane_col;
+    const uint32_t* colptr;
+    const uint32_t* csc_idx;
+    const uint32_t* exc_base;  // CSC groups
+    const double* exc_val_csc;
+    uint32_t* e_pos;
+    uint32_t* e_u;
+    double* e_val;
+    uint32_t* lane_flags;
+    __device__ __forceinline__ void store(uint64_t i, uint64_t key, bool, uint64_t) const {
+        const uint32_t pos = (uint32_t)(key >> 32), u = (uint32_t)key;
+        const uint32_t col = lane_col[pos];
+        uint32_t lo = colptr[col], hi = colptr[col + 1];
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if ((csc_idx[mid] & 0x7fffffffu) < u) lo = mid + 1; else hi = mid;
+        }
+        uint32_t rank = exc_base[lo / kCscGroup];
+        for (uint32_t q = lo & ~(uint32_t)(kCscGroup - 1); q < lo; ++q) rank += csc_idx[q] >> 31;
+        e_pos[i] = pos;
+        e_u[i] = u;
+        e_val[i] = exc_val_csc[rank];
+        lane_flags[pos] = 1u;
+    }
+};
+
+__global__ void spos_rows_kernel(const uint32_t* __restrict__ pinv, const uint32_t* __restrict__ spos_col,
+                                 int64_t n_nd, uint32_t* __restrict__ spos) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n_nd; j += (int64_t)gridDim.x * blockDim.x)
+        spos[j] = spos_col[pinv[j]];
+}
+
+__global__ void split_list_kernel(const uint32_t* __restrict__ vc_base, const uint32_t* __restrict__ vpos, int64_t n,
+                                  uint32_t* __restrict__ list, uint32_t* __restrict__ cnt) {
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x)
+        if (vc_base[c + 1] - vc_base[c] > 1) list[atomicAdd(cnt, 1u)] = vpos[vc_base[c]];
+}
+
+// s[j] = r(pinv[j]) * b[j]; r given in original order (first step) or as
+// (y in SELL order, bg for empty columns) (later steps).
+__global__ void permute_orig_kernel(const double* __restrict__ r, const uint32_t* __restrict__ pinv,
+                                    const double* __restrict__ bval, int64_t n_nd, double* __restrict__ s) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n_nd; j += (int64_t)gridDim.x * blockDim.x)
+        s[j] = __dmul_rn(r[pinv[j]], bval[j]);
+}
+__global__ void permute_sell_kernel(const double* __restrict__ y, const uint32_t* __restrict__ spos,
+                                    const double* __restrict__ bgp, const double* __restrict__ bval, int64_t n_nd,
+                                    double* __restrict__ s) {
+    const double bg = bgp[2];
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n_nd; j += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t p = spos[j];
+        s[j] = __dmul_rn(p == kEmpty ? bg : y[p], bval[j]);
+    }
+}
+// Final un-permutation: ranks[c] = y[spos_col[c]] or bg.
+__global__ void unpermute_kernel(const double* __restrict__ y, const uint32_t* __restrict__ spos_col,
+                                 const double* __restrict__ bgp, int64_t n, double* __restrict__ out) {
+    const double bg = bgp[2];
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t p = spos_col[c];
+        out[c] = p == kEmpty ? bg : y[p];
+    }
+}
+
+struct SellArgs {
+    const uint32_t* sell;
+    const uint32_t* slice_ptr;
+    const uint32_t* lane_len;
+    const uint32_t* lane_col;
+    const uint32_t* lane_np;
+    const uint32_t* lane_eptr;   // first exception of the lane (sorted order)
+    const uint32_t* lane_ecnt;   // number of exceptions of the lane
+    const uint32_t* vc_base;
+    const uint32_t* vpos;
+    const double* exc_x;         // per exception products of this iteration
+    const double* s;             // gather vector [n_nd]
+    double* y;                   // [nslices*32]
+    double* partial;             // [nslices*32]
+    uint32_t* arrive;            // [n] per split column, never reset
+    double* slice_sum;           // [nslices]
+    const double* bgp;           // [1] = bg of this step
+    int64_t n_nd;
+    uint32_t nslices;
+    double damping;
+};
+
+// Exception products for this iteration: exc_x[j] = r_prev(u_j) * value_j
+// (exceptions sorted by (lane position, source row)); each SpMV lane folds its
+// contiguous run [lane_eptr, lane_eptr + lane_ecnt) into its own sum.
+struct ExcArgs {
+    const uint32_t* e_u;
+    const double* e_val;
+    uint32_t ne;
+    const double* r0;       // previous iterate in original order (first step) or null
+    const uint32_t* pinv;
+    const uint32_t* spos;
+    const double* y_prev;
+    const double* bgp;      // [2] = bg of the previous iterate
+    double* exc_x;
+};
+__global__ void exc_products_kernel(ExcArgs a) {
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < a.ne; j += gridDim.x * blockDim.x) {
+        const uint32_t u = a.e_u[j];
+        double r;
+        if (a.r0) r = a.r0[a.pinv[u]];
+        else {
+            const uint32_t p = a.spos[u];
+            r = p == kEmpty ? a.bgp[2] : a.y_prev[p];
+        }
+        a.exc_x[j] = __dmul_rn(r, a.e_val[j]);
+    }
+}
+__global__ void exc_ranges_kernel(const uint32_t* __restrict__ e_pos, uint32_t ne, uint32_t* __restrict__ eptr,
+                                  uint32_t* __restrict__ ecnt) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < ne; i += gridDim.x * blockDim.x) {
+        const uint32_t pos = e_pos[i];
+        if (i == 0 || e_pos[i - 1] != pos) eptr[pos] = i;
+        if (i + 1 == ne || e_pos[i + 1] != pos) {
+            // run end: count = i - start + 1; start found by the head thread, so
+            // recompute it by walking back (runs are bounded by kVcMax)
+            uint32_t st = i;
+            while (st > 0 && e_pos[st - 1] == pos) --st;
+            ecnt[pos] = i - st + 1;
+        }
+    }
+}
+
+// 64 warps per SM and no shared-memory staging: measured on B200 (S=24) the L1
+// caches the hot, degree-ordered head of s by itself, and occupancy (requests
+// in flight) matters more than a software-managed hot set (1.9 ms vs 3.3 ms).
+template <int U>
+__global__ void __launch_bounds__(kSpmvThreads, 2) spmv_sell_kernel(SellArgs a) {
+    const unsigned lane = dev::lane_id();
+    const double bg = a.bgp[1];
+    const uint64_t pol_stream = dev::policy_evict_first(), pol_keep = dev::policy_evict_last();
+    const uint32_t nwarps = gridDim.x * (kSpmvThreads / 32);
+    for (uint32_t sl = blockIdx.x * (kSpmvThreads / 32) + dev::warp_id(); sl < a.nslices; sl += nwarps) {
+        const uint32_t pos = sl * 32 + lane;
+        const uint32_t len = a.lane_len[pos];
+        const uint32_t base = a.slice_ptr[sl];
+        const uint32_t rows = (a.slice_ptr[sl + 1] - base) >> 5;
+        const uint32_t* col = a.sell + base + lane;
+        double acc = 0.0;
+        // Two-stage pipeline: index loads of batch b+1 are issued before batch
+        // b's gathers are consumed. Loads are predicated, never branched.
+        uint32_t w[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            w[u] = dev::ld_stream_u32_pred(col + 32 * u, (uint32_t)u < len, pol_stream, 0x80000000u);
+        for (uint32_t k0 = 0; k0 < rows; k0 += U) {
+            double x[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                x[u] = dev::ld_keep_f64_pred(a.s + (w[u] & 0x7fffffffu), !(w[u] >> 31), pol_keep);
+            const uint32_t k1 = k0 + U;
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                w[u] = dev::ld_stream_u32_pred(col + 32 * (k1 + u), k1 + u < len, pol_stream, 0x80000000u);
+#pragma unroll
+            for (int u = 0; u < U; ++u) acc = __dadd_rn(acc, x[u]);
+        }
+        // duplicate-edge exceptions of this lane (products precomputed this iteration)
+        const uint32_t ecnt = a.lane_ecnt[pos];
+        if (__any_sync(0xffffffffu, ecnt != 0)) {
+            const double* ex = a.exc_x + (ecnt ? a.lane_eptr[pos] : 0u);
+            double eacc = 0.0;
+            for (uint32_t j0 = 0; j0 < ecnt; j0 += 8) {
+                double xe[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) xe[u] = dev::ld_f64_pred(ex + j0 + u, j0 + u < ecnt);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) eacc = __dadd_rn(eacc, xe[u]);
+            }
+            acc = __dadd_rn(acc, eacc);
+        }
+        const uint32_t np = a.lane_np[pos];
+        double yv = 0.0;
+        if (len > 0 && np == 1) {
+            yv = __dadd_rn(__dmul_rn(a.damping, acc), bg);
+            a.y[pos] = yv;
+        } else if (len > 0) {
+            a.partial[pos] = acc;
+            __threadfence();
+            const uint32_t c = a.lane_col[pos];
+            const uint32_t old = atomicAdd(&a.arrive[c], 1u);
+            if ((old + 1) % np == 0) {  // last part of this column: combine in part order
+                __threadfence();
+                double t = 0.0;
+                const uint32_t v0 = a.vc_base[c];
+                for (uint32_t p = 0; p < np; ++p) t = __dadd_rn(t, *((volatile double*)&a.partial[a.vpos[v0 + p]]));
+                a.y[a.vpos[v0]] = __dadd_rn(__dmul_rn(a.damping, t), bg);
+            }
+        }
+        yv = dev::warp_sum_f64(yv);
+        if (lane == 0) a.slice_sum[sl] = yv;
+    }
+}
+
+// Sum of the iterate: tree(slice sums) + tree(split-column values) + n_empty*bg.
+__global__ void sell_sum_kernel(const double* __restrict__ slice_sum, uint32_t nslices, const double* __restrict__ y,
+                                const uint32_t* __restrict__ split_pos, const uint32_t* __restrict__ n_split,
+                                double n_empty, double bgf, double* __restrict__ out) {
+    __shared__ double ws[32];
+    const uint32_t ns = *n_split;
+    double a = 0.0, b = 0.0;
+    for (uint32_t i = threadIdx.x; i < nslices; i += 1024) a = __dadd_rn(a, slice_sum[i]);
+    for (uint32_t i = threadIdx.x; i < ns; i += 1024) b = __dadd_rn(b, y[split_pos[i]]);
+    a = dev::warp_sum_f64(a);
+    b = dev::warp_sum_f64(b);
+    if (dev::lane_id() == 0) ws[dev::warp_id()] = __dadd_rn(a, b);
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double v = dev::warp_sum_f64(ws[threadIdx.x]);
+        if (threadIdx.x == 0) {
+            const double bg_cur = out[1];
+            const double tot = __dadd_rn(v, __dmul_rn(n_empty, bg_cur));
+            out[0] = tot;
+            out[2] = bg_cur;
+            out[1] = __dmul_rn(bgf, tot);
+        }
+    }
+}
+
+__global__ void count_set_kernel(const uint32_t* __restrict__ a, int64_t n, uint32_t* __restrict__ out) {
+    uint32_t c = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        c += a[i] != kEmpty;
+    c = __reduce_add_sync(0xffffffffu, c);
+    if (dev::lane_id() == 0 && c) atomicAdd(out, c);
+}
+
+// ---------------------------------------------------------------------------
+// Plan
+// ---------------------------------------------------------------------------
 struct K3Plan {
     int64_t n = 0, n_nd = 0;
     uint64_t nnz = 0;
@@ -526,6 +814,11 @@ struct K3Plan {
     DevBuf<uint32_t> pinv, newid, colptr, csc_idx, exc_base;
     DevBuf<double> bval, exc_val;
     uint32_t n_exc = 0;
+    // timed mode (SELL)
+    uint32_t V = 0, nslices = 0, n_empty = 0;
+    DevBuf<uint32_t> sell, slice_ptr, lane_len, lane_col, lane_np, lane_flags, lane_eptr, lane_ecnt, vc_base, vpos,
+        spos, spos_col, split_pos, n_split, arrive, e_pos, e_u;
+    DevBuf<double> e_val, partial;
 };
 
 void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
@@ -540,62 +833,69 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
     const unsigned g = (unsigned)num_sms() * 8;
     P.pinv = DevBuf<uint32_t>((size_t)n, s);
     P.newid = DevBuf<uint32_t>((size_t)n, s);
-    // 1. row renumbering
-    if (mode == 0) {
-        DevBuf<unsigned long long> cnt(1, s);
-        PRG_CUDA(cudaMemsetAsync(cnt.get(), 0, 8, s));
-        count_nondangling<<<g, 1024, 0, s>>>(A->row_offsets, n, cnt.get());
-        PRG_LAUNCH_CHECK();
-        sort::SortWorkspace ws;
-        sort::msd_sort(RowClassSrc{A->row_offsets, P.sb}, (size_t)n, P.sb + 8,
-                       PermDst{P.pinv.get(), P.newid.get(), P.sb}, ws, s);
-        unsigned long long h = 0;
-        PRG_CUDA(cudaMemcpyAsync(&h, cnt.get(), 8, cudaMemcpyDeviceToHost, s));
-        PRG_CUDA(cudaStreamSynchronize(s));
-        P.n_nd = (int64_t)h;
-    } else {
-        iota_kernel<<<g, 1024, 0, s>>>(P.pinv.get(), P.newid.get(), n);
-        PRG_LAUNCH_CHECK();
-        P.n_nd = n;
+    // 1. row renumbering (timed: hot rows first, dangling last; parity: identity)
+    {
+        ProfScope pr("k3_prep_rows", s);
+        if (mode == 0) {
+            DevBuf<unsigned long long> cnt(1, s);
+            PRG_CUDA(cudaMemsetAsync(cnt.get(), 0, 8, s));
+            count_nondangling<<<g, 1024, 0, s>>>(A->row_offsets, n, cnt.get());
+            PRG_LAUNCH_CHECK();
+            sort::SortWorkspace ws;
+            sort::msd_sort(RowClassSrc{A->row_offsets, P.sb}, (size_t)n, P.sb + 8,
+                           PermDst{P.pinv.get(), P.newid.get(), P.sb}, ws, s, "k3rows");
+            unsigned long long h = 0;
+            PRG_CUDA(cudaMemcpyAsync(&h, cnt.get(), 8, cudaMemcpyDeviceToHost, s));
+            PRG_CUDA(cudaStreamSynchronize(s));
+            P.n_nd = (int64_t)h;
+        } else {
+            iota_kernel<<<g, 1024, 0, s>>>(P.pinv.get(), P.newid.get(), n);
+            PRG_LAUNCH_CHECK();
+            P.n_nd = n;
+        }
     }
-    // 2. row base values (min stored value per row)
+    // 2. row base values (minimum stored value of each row)
     DevBuf<unsigned long long> bmin((size_t)n, s);
-    PRG_CUDA(cudaMemsetAsync(bmin.get(), 0xff, (size_t)n * 8, s));
     const uint32_t ntiles = nnz ? div_up(nnz, sort::kTile) : 0;
     DevBuf<uint32_t> tile_row(ntiles + 1, s);
-    if (nnz) {
-        tile_rows_kernel<<<g, 1024, 0, s>>>(A->row_offsets, n, tile_row.get());
-        PRG_LAUNCH_CHECK();
-        row_min_kernel<<<std::min<unsigned>(ntiles, (unsigned)num_sms() * 2), sort::kTileThreads, 0, s>>>(
-            A->row_offsets, tile_row.get(), A->values, n, nnz, bmin.get());
+    {
+        ProfScope pr("k3_prep_base", s);
+        PRG_CUDA(cudaMemsetAsync(bmin.get(), 0xff, (size_t)n * 8, s));
+        if (nnz) {
+            tile_rows_kernel<<<g, 1024, 0, s>>>(A->row_offsets, n, tile_row.get());
+            PRG_LAUNCH_CHECK();
+            row_min_kernel<<<std::min<unsigned>(ntiles, (unsigned)num_sms() * 2), sort::kTileThreads, 0, s>>>(
+                A->row_offsets, tile_row.get(), A->values, n, nnz, bmin.get());
+            PRG_LAUNCH_CHECK();
+        }
+        P.bval = DevBuf<double>((size_t)std::max<int64_t>(P.n_nd, 1), s);
+        gather_base_kernel<<<g, 1024, 0, s>>>(P.pinv.get(), bmin.get(), P.n_nd, P.bval.get());
         PRG_LAUNCH_CHECK();
     }
-    P.bval = DevBuf<double>((size_t)std::max<int64_t>(P.n_nd, 1), s);
-    gather_base_kernel<<<g, 1024, 0, s>>>(P.pinv.get(), bmin.get(), P.n_nd, P.bval.get());
-    PRG_LAUNCH_CHECK();
-    // 3. transpose
+    // 3. transpose (sort of (col, new row id, exception) keys)
     P.colptr = DevBuf<uint32_t>((size_t)n + 1, s);
-    PRG_CUDA(cudaMemsetAsync(P.colptr.get(), 0xff, (size_t)(n + 1) * 4, s));
     P.csc_idx = DevBuf<uint32_t>(nnz ? nnz : 1, s);
     const uint64_t ngroups = nnz / kCscGroup + 1;
     DevBuf<uint32_t> exc_cnt(ngroups, s);
-    PRG_CUDA(cudaMemsetAsync(exc_cnt.get(), 0, ngroups * 4, s));
     DevBuf<unsigned long long> exc_key(nnz ? nnz : 1, s);
     DevBuf<double> exc_v(nnz ? nnz : 1, s);
     DevBuf<uint32_t> n_exc(1, s);
-    PRG_CUDA(cudaMemsetAsync(n_exc.get(), 0, 4, s));
-    if (nnz) {
-        CsrEntrySrc src{A->row_offsets, tile_row.get(), A->cols, A->values, P.newid.get(), bmin.get(), n, P.sb,
-                        exc_key.get(), exc_v.get(), n_exc.get()};
-        // The histogram pass captures the exception list; the scatter pass must not.
-        CsrEntrySrc scat = src;
-        scat.exc_key = nullptr;
-        sort::SortWorkspace ws;
-        sort::msd_sort_split(src, scat, (size_t)nnz, 2 * P.sb + 1,
-                             CscDst{P.csc_idx.get(), P.colptr.get(), exc_cnt.get(), P.sb}, ws, s);
-    }
-    // colptr[n] = nnz, then fill empty columns with the next column start.
     {
+        ProfScope pr("k3_prep_transpose", s);
+        PRG_CUDA(cudaMemsetAsync(P.colptr.get(), 0xff, (size_t)(n + 1) * 4, s));
+        PRG_CUDA(cudaMemsetAsync(exc_cnt.get(), 0, ngroups * 4, s));
+        PRG_CUDA(cudaMemsetAsync(n_exc.get(), 0, 4, s));
+        if (nnz) {
+            CsrEntrySrc src{A->row_offsets, tile_row.get(), A->cols, A->values, P.newid.get(), bmin.get(), n, P.sb,
+                            exc_key.get(), exc_v.get(), n_exc.get()};
+            // The histogram pass captures the exception list; the scatter pass must not.
+            CsrEntrySrc scat = src;
+            scat.exc_key = nullptr;
+            sort::SortWorkspace ws;
+            sort::msd_sort_split(src, scat, (size_t)nnz, 2 * P.sb + 1,
+                                 CscDst{P.csc_idx.get(), P.colptr.get(), exc_cnt.get(), P.sb}, ws, s, "k3t");
+        }
+        // colptr[n] = nnz, then fill empty columns with the next column start.
         const uint32_t nz = (uint32_t)nnz;
         PRG_CUDA(cudaMemcpyAsync(P.colptr.get() + n, &nz, 4, cudaMemcpyHostToDevice, s));
         const int64_t n1 = n + 1;
@@ -606,31 +906,136 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
         suffix_min_down<<<(unsigned)nb, 1024, 0, s>>>(P.colptr.get(), n1, part.get());
         PRG_LAUNCH_CHECK();
     }
-    // exceptions
+    // exceptions in CSC order (parity mode uses them directly; timed mode resolves from them)
     P.exc_base = DevBuf<uint32_t>(ngroups, s);
-    DevBuf<uint32_t> exc_total(1, s);
-    exclusive_scan_u32(exc_cnt.get(), P.exc_base.get(), ngroups, exc_total.get(), s);
-    PRG_CUDA(cudaMemcpyAsync(&P.n_exc, exc_total.get(), 4, cudaMemcpyDeviceToHost, s));
-    PRG_CUDA(cudaStreamSynchronize(s));
+    {
+        DevBuf<uint32_t> exc_total(1, s);
+        exclusive_scan_u32(exc_cnt.get(), P.exc_base.get(), ngroups, exc_total.get(), s);
+        PRG_CUDA(cudaMemcpyAsync(&P.n_exc, exc_total.get(), 4, cudaMemcpyDeviceToHost, s));
+        PRG_CUDA(cudaStreamSynchronize(s));
+    }
     P.exc_val = DevBuf<double>(P.n_exc ? P.n_exc : 1, s);
     if (P.n_exc) {
         place_exceptions<<<g, 256, 0, s>>>(exc_key.get(), exc_v.get(), n_exc.get(), P.colptr.get(),
                                            P.csc_idx.get(), P.exc_base.get(), P.sb, P.exc_val.get());
         PRG_LAUNCH_CHECK();
     }
+    if (mode == 1) return;
+    // 4. SELL over virtual columns
+    ProfScope pr("k3_prep_sell", s);
+    DevBuf<uint32_t> np((size_t)n, s);
+    P.vc_base = DevBuf<uint32_t>((size_t)n + 1, s);
+    vc_count_kernel<<<g, 1024, 0, s>>>(P.colptr.get(), n, np.get());
+    PRG_LAUNCH_CHECK();
+    exclusive_scan_u32(np.get(), P.vc_base.get(), (size_t)n, P.vc_base.get() + n, s);
+    PRG_CUDA(cudaMemcpyAsync(&P.V, P.vc_base.get() + n, 4, cudaMemcpyDeviceToHost, s));
+    PRG_CUDA(cudaStreamSynchronize(s));
+    const uint32_t V = P.V;
+    P.nslices = (V + 31) / 32;
+    const uint32_t NP = P.nslices * 32;
+    DevBuf<uint32_t> vc_col(V ? V : 1, s), vc_len(V ? V : 1, s), order(NP ? NP : 1, s);
+    P.vpos = DevBuf<uint32_t>(V ? V : 1, s);
+    vc_fill_kernel<<<g, 1024, 0, s>>>(P.colptr.get(), P.vc_base.get(), n, vc_col.get(), vc_len.get());
+    PRG_LAUNCH_CHECK();
+    if (V) {
+        sort::SortWorkspace ws;
+        const int vb = bits_for(V);
+        sort::msd_sort(VcClassSrc{vc_len.get(), vb}, (size_t)V, vb + 8, PermDst{order.get(), P.vpos.get(), vb}, ws, s, "k3vc");
+    }
+    DevBuf<uint32_t> slice_sz(P.nslices ? P.nslices : 1, s);
+    P.slice_ptr = DevBuf<uint32_t>((size_t)P.nslices + 1, s);
+    if (P.nslices) {
+        slice_size_kernel<<<g, 256, 0, s>>>(order.get(), vc_len.get(), V, P.nslices, slice_sz.get());
+        PRG_LAUNCH_CHECK();
+    }
+    exclusive_scan_u32(slice_sz.get(), P.slice_ptr.get(), P.nslices, P.slice_ptr.get() + P.nslices, s);
+    uint32_t sell_n = 0;
+    PRG_CUDA(cudaMemcpyAsync(&sell_n, P.slice_ptr.get() + P.nslices, 4, cudaMemcpyDeviceToHost, s));
+    PRG_CUDA(cudaStreamSynchronize(s));
+    P.sell = DevBuf<uint32_t>(sell_n ? sell_n : 1, s);
+    const uint32_t sgroups = sell_n / 32 + 1;
+    DevBuf<uint32_t> sexc_cnt(sgroups, s);  // (unused by the SpMV; kept for the fill kernel)
+    PRG_CUDA(cudaMemsetAsync(sexc_cnt.get(), 0, (size_t)sgroups * 4, s));
+    P.lane_len = DevBuf<uint32_t>(NP ? NP : 1, s);
+    P.lane_col = DevBuf<uint32_t>(NP ? NP : 1, s);
+    P.lane_np = DevBuf<uint32_t>(NP ? NP : 1, s);
+    P.spos_col = DevBuf<uint32_t>((size_t)n, s);
+    PRG_CUDA(cudaMemsetAsync(P.spos_col.get(), 0xff, (size_t)n * 4, s));
+    if (P.nslices) {
+        FillArgs fa{order.get(), vc_col.get(), vc_len.get(), P.vc_base.get(), P.colptr.get(), P.csc_idx.get(),
+                    P.slice_ptr.get(), V, P.nslices, P.sell.get(), sexc_cnt.get(), P.lane_len.get(),
+                    P.lane_col.get(), P.lane_np.get(), P.spos_col.get()};
+        sell_fill_kernel<<<g, 256, 0, s>>>(fa);
+        PRG_LAUNCH_CHECK();
+    }
+    // exceptions grouped by lane position (sorted by (pos, source row))
+    P.lane_flags = DevBuf<uint32_t>(NP ? NP : 1, s);
+    PRG_CUDA(cudaMemsetAsync(P.lane_flags.get(), 0, (size_t)(NP ? NP : 1) * 4, s));
+    P.e_pos = DevBuf<uint32_t>(P.n_exc ? P.n_exc : 1, s);
+    P.e_u = DevBuf<uint32_t>(P.n_exc ? P.n_exc : 1, s);
+    P.e_val = DevBuf<double>(P.n_exc ? P.n_exc : 1, s);
+    if (P.n_exc) {
+        DevBuf<unsigned long long> ek(P.n_exc, s);
+        exc_pos_keys<<<g, 256, 0, s>>>(exc_key.get(), n_exc.get(), P.colptr.get(), P.csc_idx.get(), P.vc_base.get(),
+                                       P.vpos.get(), P.sb, ek.get());
+        PRG_LAUNCH_CHECK();
+        sort::SortWorkspace ws;
+        sort::msd_sort(KeyArraySrc{ek.get()}, (size_t)P.n_exc, 32 + bits_for(NP),
+                       ExcResolveDst{P.lane_col.get(), P.colptr.get(), P.csc_idx.get(), P.exc_base.get(),
+                                     P.exc_val.get(), P.e_pos.get(), P.e_u.get(), P.e_val.get(), P.lane_flags.get()},
+                       ws, s, "k3exc");
+    }
+    P.lane_eptr = DevBuf<uint32_t>(NP ? NP : 1, s);
+    P.lane_ecnt = DevBuf<uint32_t>(NP ? NP : 1, s);
+    PRG_CUDA(cudaMemsetAsync(P.lane_ecnt.get(), 0, (size_t)(NP ? NP : 1) * 4, s));
+    if (P.n_exc) {
+        exc_ranges_kernel<<<g, 256, 0, s>>>(P.e_pos.get(), P.n_exc, P.lane_eptr.get(), P.lane_ecnt.get());
+        PRG_LAUNCH_CHECK();
+    }
+    P.spos = DevBuf<uint32_t>((size_t)std::max<int64_t>(P.n_nd, 1), s);
+    spos_rows_kernel<<<g, 1024, 0, s>>>(P.pinv.get(), P.spos_col.get(), P.n_nd, P.spos.get());
+    PRG_LAUNCH_CHECK();
+    P.split_pos = DevBuf<uint32_t>((size_t)n, s);
+    P.n_split = DevBuf<uint32_t>(1, s);
+    PRG_CUDA(cudaMemsetAsync(P.n_split.get(), 0, 4, s));
+    split_list_kernel<<<g, 1024, 0, s>>>(P.vc_base.get(), P.vpos.get(), n, P.split_pos.get(), P.n_split.get());
+    PRG_LAUNCH_CHECK();
+    P.arrive = DevBuf<uint32_t>((size_t)n, s);
+    PRG_CUDA(cudaMemsetAsync(P.arrive.get(), 0, (size_t)n * 4, s));
+    P.partial = DevBuf<double>(NP ? NP : 1, s);
+    // empty columns = columns with no virtual column
+    uint32_t nonempty = 0;
+    {
+        DevBuf<uint32_t> ne(1, s);
+        PRG_CUDA(cudaMemsetAsync(ne.get(), 0, 4, s));
+        // count columns whose part-0 position was set
+        count_set_kernel<<<g, 1024, 0, s>>>(P.spos_col.get(), n, ne.get());
+        PRG_LAUNCH_CHECK();
+        PRG_CUDA(cudaMemcpyAsync(&nonempty, ne.get(), 4, cudaMemcpyDeviceToHost, s));
+        PRG_CUDA(cudaStreamSynchronize(s));
+    }
+    P.n_empty = (uint32_t)(n - nonempty);
+    if (getenv("PRG_DEBUG"))
+        fprintf(stderr, "[k3 plan] n=%lld nnz=%llu n_nd=%lld V=%u nslices=%u sell_n=%u (pad %.3f) n_exc=%u n_empty=%u\n",
+                (long long)n, (unsigned long long)nnz, (long long)P.n_nd, V, P.nslices, sell_n,
+                nnz ? (double)sell_n / (double)nnz : 0.0, P.n_exc, P.n_empty);
+    // the CSC itself is no longer needed in timed mode
+    P.csc_idx = DevBuf<uint32_t>();
 }
-
 
 // ---------------------------------------------------------------------------
 // Drivers
 // ---------------------------------------------------------------------------
 struct Sums {
-    DevBuf<double> part, out;  // out[0] = sum, out[1] = bg for the next step
+    DevBuf<double> part, out;  // out[0] = sum, out[1] = bg for the next step, out[2] = bg of the current iterate
 };
 
 // sum(x) into out[0] and ((1-c)/n)*sum into out[1], deterministic.
 void device_sum(const double* x, int64_t n, double bgf, int mode, Sums& S, cudaStream_t s) {
-    if (!S.out.get()) S.out = DevBuf<double>(2, s);
+    if (!S.out.get()) {
+        S.out = DevBuf<double>(4, s);
+        PRG_CUDA(cudaMemsetAsync(S.out.get(), 0, 32, s));
+    }
     if (mode == 1) {
         seq_sum_kernel<<<1, 1, 0, s>>>(x, n, bgf, S.out.get());
     } else {
@@ -662,54 +1067,88 @@ void init_rank_impl(int64_t n, uint64_t seed, double* d_r, int mode, double bgf,
 
 size_t spmv_smem() { return (size_t)kHot * sizeof(double); }
 
-// One step: r_next = c * A^T r_prev + bg; S.out holds {sum(r_prev), bg} on entry
-// and {sum(r_next), bg'} on exit. s_buf is scratch of n_nd doubles.
-void step_impl(const K3Plan& P, const double* r_prev, double* r_next, double damping, double bgf,
-               double* s_buf, Sums& S, DevBuf<double>& task_sum, DevBuf<uint32_t>& counter, cudaStream_t s) {
+// Runs `iters` steps from r_in (original order, S.out = {sum(r_in), bg}) and
+// writes the final iterate to r_out (original order); S.out ends as
+// {sum(r_out), bg', bg_used}.
+void iterate(const K3Plan& P, const double* r_in, double* r_out, int iters, double damping, double bgf, Sums& S,
+             cudaStream_t s) {
     const unsigned g = (unsigned)num_sms() * 8;
-    if (P.n_nd) {
-        ProfScope pp("k3_permute", s);
-        permute_scale_kernel<<<g, 1024, 0, s>>>(r_prev, P.pinv.get(), P.bval.get(), P.n_nd, s_buf);
-        PRG_LAUNCH_CHECK();
-    }
-    const uint32_t ntasks = (uint32_t)((P.n + 31) / 32);
-    if (task_sum.n < ntasks) task_sum = DevBuf<double>(ntasks, s);
-    SpmvArgs a;
-    a.colptr = P.colptr.get();
-    a.csc_idx = P.csc_idx.get();
-    a.exc_base = P.exc_base.get();
-    a.exc_val = P.exc_val.get();
-    a.s = s_buf;
-    a.r_prev = r_prev;
-    a.pinv = P.pinv.get();
-    a.bgp = S.out.get();
-    a.r_next = r_next;
-    a.task_sum = task_sum.get();
-    a.task_counter = counter.get();
-    a.n = P.n;
-    a.n_nd = P.n_nd;
-    a.ntasks = ntasks;
-    a.damping = damping;
+    const int64_t n = P.n;
     if (P.mode == 1) {
-        spmv_seq_kernel<<<g, 256, 0, s>>>(a);
-        PRG_LAUNCH_CHECK();
-        device_sum(r_next, P.n, bgf, 1, S, s);
-    } else {
-        static bool attr = false;
-        if (!attr) {
-            PRG_CUDA(cudaFuncSetAttribute(spmv_pull_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)spmv_smem()));
-            attr = true;
+        DevBuf<double> sb((size_t)n, s), tA((size_t)n, s), tB((size_t)n, s);
+        const double* cur = r_in;
+        for (int it = 0; it < iters; ++it) {
+            double* dst = (it & 1) ? tB.get() : tA.get();
+            permute_orig_kernel<<<g, 1024, 0, s>>>(cur, P.pinv.get(), P.bval.get(), n, sb.get());
+            PRG_LAUNCH_CHECK();
+            SeqArgs a{P.colptr.get(), P.csc_idx.get(), P.exc_base.get(), P.exc_val.get(), sb.get(), cur,
+                      S.out.get(), dst, n, damping};
+            spmv_seq_kernel<<<g, 256, 0, s>>>(a);
+            PRG_LAUNCH_CHECK();
+            device_sum(dst, n, bgf, 1, S, s);
+            cur = dst;
         }
-        PRG_CUDA(cudaMemsetAsync(counter.get(), 0, 4, s));
-        {
-            ProfScope ps("k3_spmv", s);
-            spmv_pull_kernel<<<num_sms(), kSpmvThreads, spmv_smem(), s>>>(a);
+        if (cur != r_out) PRG_CUDA(cudaMemcpyAsync(r_out, cur, (size_t)n * 8, cudaMemcpyDeviceToDevice, s));
+        return;
+    }
+    static int variant = -1;
+    if (variant < 0) {
+        const char* v = getenv("PRG_SPMV_VARIANT");
+        variant = v ? atoi(v) : 0;
+
+    }
+    const uint32_t NP = P.nslices * 32;
+    DevBuf<double> sbuf((size_t)std::max<int64_t>(P.n_nd, 1), s), y0(NP ? NP : 1, s), y1(NP ? NP : 1, s),
+        slice_sum(P.nslices ? P.nslices : 1, s), exc_x(P.n_exc ? P.n_exc : 1, s);
+    double* ys[2] = {y0.get(), y1.get()};
+    for (int it = 0; it < iters; ++it) {
+        double* y = ys[it & 1];
+        const double* yp = ys[(it & 1) ^ 1];
+        if (P.n_nd) {
+            ProfScope pp("k3_permute", s);
+            if (it == 0) permute_orig_kernel<<<g, 1024, 0, s>>>(r_in, P.pinv.get(), P.bval.get(), P.n_nd, sbuf.get());
+            else permute_sell_kernel<<<g, 1024, 0, s>>>(yp, P.spos.get(), S.out.get(), P.bval.get(), P.n_nd, sbuf.get());
             PRG_LAUNCH_CHECK();
         }
-        final_sum_kernel<<<1, 1024, 0, s>>>(task_sum.get(), ntasks, bgf, S.out.get());
+        if (P.n_exc) {
+            ExcArgs ea{P.e_u.get(), P.e_val.get(), P.n_exc, it == 0 ? r_in : nullptr, P.pinv.get(), P.spos.get(), yp,
+                       S.out.get(), exc_x.get()};
+            exc_products_kernel<<<g, 256, 0, s>>>(ea);
+            PRG_LAUNCH_CHECK();
+        }
+        SellArgs a;
+        a.sell = P.sell.get();
+        a.slice_ptr = P.slice_ptr.get();
+        a.lane_len = P.lane_len.get();
+        a.lane_col = P.lane_col.get();
+        a.lane_np = P.lane_np.get();
+        a.lane_eptr = P.lane_eptr.get();
+        a.lane_ecnt = P.lane_ecnt.get();
+        a.vc_base = P.vc_base.get();
+        a.vpos = P.vpos.get();
+        a.exc_x = exc_x.get();
+        a.s = sbuf.get();
+        a.y = y;
+        a.partial = P.partial.get();
+        a.arrive = P.arrive.get();
+        a.slice_sum = slice_sum.get();
+        a.bgp = S.out.get();
+        a.n_nd = P.n_nd;
+        a.nslices = P.nslices;
+        a.damping = damping;
+        if (P.nslices) {
+            ProfScope ps("k3_spmv", s);
+            if (variant == 1) spmv_sell_kernel<2><<<num_sms() * 2, kSpmvThreads, 0, s>>>(a);
+            else if (variant == 2) spmv_sell_kernel<8><<<num_sms() * 2, kSpmvThreads, 0, s>>>(a);
+            else spmv_sell_kernel<4><<<num_sms() * 2, kSpmvThreads, 0, s>>>(a);
+            PRG_LAUNCH_CHECK();
+        }
+        sell_sum_kernel<<<1, 1024, 0, s>>>(slice_sum.get(), P.nslices, y, P.split_pos.get(), P.n_split.get(),
+                                           (double)P.n_empty, bgf, S.out.get());
         PRG_LAUNCH_CHECK();
     }
+    unpermute_kernel<<<g, 1024, 0, s>>>(ys[(iters - 1) & 1], P.spos_col.get(), S.out.get(), n, r_out);
+    PRG_LAUNCH_CHECK();
 }
 
 }  // namespace
@@ -727,16 +1166,9 @@ double k3_pagerank_device(const prg_matrix* A, const K3Options& opt, double* d_r
     K3Plan P;
     build_plan(A, opt.mode, P, s);
     Sums S;
-    DevBuf<double> r_tmp((size_t)n, s), s_buf((size_t)std::max<int64_t>(P.n_nd, 1), s), task_sum;
-    DevBuf<uint32_t> counter(1, s);
-    // The final iterate must land in d_ranks: alternate so that it does.
-    double* bufs[2] = {d_ranks, r_tmp.get()};
-    int cur = (opt.iterations % 2 == 0) ? 0 : 1;
-    init_rank_impl(n, opt.seed, bufs[cur], opt.mode, bgf, S, s);
-    for (int it = 0; it < opt.iterations; ++it) {
-        step_impl(P, bufs[cur], bufs[cur ^ 1], opt.damping, bgf, s_buf.get(), S, task_sum, counter, s);
-        cur ^= 1;
-    }
+    DevBuf<double> r0((size_t)n, s);
+    init_rank_impl(n, opt.seed, r0.get(), opt.mode, bgf, S, s);
+    iterate(P, r0.get(), d_ranks, opt.iterations, opt.damping, bgf, S, s);
     return read_scalar(S.out.get(), s);
 }
 
@@ -748,9 +1180,7 @@ double k3_step_device(const prg_matrix* A, const double* d_r, double damping, do
     build_plan(A, mode, P, s);
     Sums S;
     device_sum(d_r, n, bgf, mode, S, s);
-    DevBuf<double> s_buf((size_t)std::max<int64_t>(P.n_nd, 1), s), task_sum;
-    DevBuf<uint32_t> counter(1, s);
-    step_impl(P, d_r, d_out, damping, bgf, s_buf.get(), S, task_sum, counter, s);
+    iterate(P, d_r, d_out, 1, damping, bgf, S, s);
     return read_scalar(S.out.get(), s);
 }
 

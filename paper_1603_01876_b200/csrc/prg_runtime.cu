@@ -30,7 +30,7 @@ long long launch_count() { return g_launches.load(); }
 bool profiling_enabled() { return g_prof.load(std::memory_order_relaxed); }
 void profiling_enable(bool on) { g_prof.store(on); }
 
-ProfScope::ProfScope(const char* n, cudaStream_t st) : name(n), s(st) {
+ProfScope::ProfScope(std::string n, cudaStream_t st) : name(std::move(n)), s(st) {
     if (!profiling_enabled()) return;
     cudaEventCreate(&a);
     cudaEventCreate(&b);

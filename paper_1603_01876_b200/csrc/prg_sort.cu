@@ -8,24 +8,57 @@ namespace prg::sort {
 // ---------------------------------------------------------------------------
 // Level bookkeeping
 // ---------------------------------------------------------------------------
+// Children of one parent are contiguous in key order. Consecutive children
+// that fit in shared memory are coalesced into one final segment (up to
+// kLocalCap keys) — the local stage sorts any key range, and this keeps the
+// count of final segments (and their fixed per-segment cost) low. Children
+// larger than the cap become active for the next level (or final, if no key
+// bits are left: all their keys are equal).
+__device__ void emit_children(const uint64_t* child_start, const uint32_t* child_size, int nchild,
+                              uint8_t buf, int next_shift, int next_bits, Seg* __restrict__ next,
+                              uint32_t* __restrict__ n_next, Seg* __restrict__ fin, uint32_t* __restrict__ n_fin) {
+    Seg run;
+    run.size = 0;
+    run.buf = buf;
+    run.bits = 0;
+    run.shift = 0;
+    for (int d = 0; d < nchild; ++d) {
+        const uint32_t sz = child_size[d];
+        if (sz == 0) continue;
+        if (sz > (uint32_t)kLocalCap) {
+            if (run.size) { fin[atomicAdd(n_fin, 1u)] = run; run.size = 0; }
+            Seg c;
+            c.start = child_start[d];
+            c.size = sz;
+            c.buf = buf;
+            c.bits = (uint8_t)next_bits;
+            c.shift = (uint16_t)next_shift;
+            if (next_bits == 0) fin[atomicAdd(n_fin, 1u)] = c;
+            else next[atomicAdd(n_next, 1u)] = c;
+            continue;
+        }
+        if (run.size && run.size + sz > (uint32_t)kLocalCap) { fin[atomicAdd(n_fin, 1u)] = run; run.size = 0; }
+        if (run.size == 0) run.start = child_start[d];
+        run.size += sz;
+    }
+    if (run.size) fin[atomicAdd(n_fin, 1u)] = run;
+}
+
 __global__ void classify_l1_kernel(const uint32_t* __restrict__ off, uint32_t ntiles, size_t n,
                                    int shift, int bits, Seg* __restrict__ next,
                                    uint32_t* __restrict__ n_next, Seg* __restrict__ fin,
                                    uint32_t* __restrict__ n_fin) {
+    __shared__ uint64_t cst[kRadix];
+    __shared__ uint32_t csz[kRadix];
     const int d = threadIdx.x;
-    if (d >= kRadix) return;
-    const uint64_t st = off[(size_t)d * ntiles];
-    const uint64_t en = d + 1 < kRadix ? off[(size_t)(d + 1) * ntiles] : n;
-    const uint32_t sz = (uint32_t)(en - st);
-    if (sz == 0) return;
-    Seg c;
-    c.start = st;
-    c.size = sz;
-    c.buf = 1;
-    c.bits = (uint8_t)bits;
-    c.shift = (uint16_t)(shift - bits);
-    if (sz <= (uint32_t)kLocalCap || bits == 0) fin[atomicAdd(n_fin, 1u)] = c;
-    else next[atomicAdd(n_next, 1u)] = c;
+    if (d < kRadix) {
+        const uint64_t st = off[(size_t)d * ntiles];
+        const uint64_t en = d + 1 < kRadix ? off[(size_t)(d + 1) * ntiles] : n;
+        cst[d] = st;
+        csz[d] = (uint32_t)(en - st);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) emit_children(cst, csz, kRadix, 1, shift - bits, bits, next, n_next, fin, n_fin);
 }
 
 __global__ void build_tiles_kernel(const Seg* __restrict__ active, const uint32_t* __restrict__ n_active,
@@ -174,6 +207,8 @@ __global__ void classify_kernel(const Seg* __restrict__ active, const uint32_t* 
                                 const uint32_t* __restrict__ off, Seg* __restrict__ next,
                                 uint32_t* __restrict__ n_next, Seg* __restrict__ fin,
                                 uint32_t* __restrict__ n_fin) {
+    __shared__ uint64_t cst[kRadix];
+    __shared__ uint32_t csz[kRadix];
     const uint32_t na = *n_active;
     for (uint32_t si = blockIdx.x; si < na; si += gridDim.x) {
         const Seg sg = active[si];
@@ -184,18 +219,15 @@ __global__ void classify_kernel(const Seg* __restrict__ active, const uint32_t* 
         for (int d = threadIdx.x; d < nd; d += blockDim.x) {
             const uint64_t st = off[hb + (size_t)d * seg_nt] - e0;
             const uint64_t en = d + 1 < nd ? off[hb + (size_t)(d + 1) * seg_nt] - e0 : sg.size;
-            const uint32_t sz = (uint32_t)(en - st);
-            if (sz == 0) continue;
-            Seg c;
-            c.start = sg.start + st;
-            c.size = sz;
-            c.buf = (uint8_t)(sg.buf ^ 1);
-            const int nb = sg.shift >= 8 ? 8 : sg.shift;
-            c.bits = (uint8_t)nb;
-            c.shift = (uint16_t)(sg.shift - nb);
-            if (sz <= (uint32_t)kLocalCap || nb == 0) fin[atomicAdd(n_fin, 1u)] = c;
-            else next[atomicAdd(n_next, 1u)] = c;
+            cst[d] = sg.start + st;
+            csz[d] = (uint32_t)(en - st);
         }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const int nb = sg.shift >= 8 ? 8 : sg.shift;
+            emit_children(cst, csz, nd, (uint8_t)(sg.buf ^ 1), sg.shift - nb, nb, next, n_next, fin, n_fin);
+        }
+        __syncthreads();
     }
 }
 

@@ -176,53 +176,61 @@ __global__ void classify_l1_kernel(const uint32_t* __restrict__ off, uint32_t nt
 
 // ---------------------------------------------------------------------------
 // Local stage: one CTA sorts one SMEM-resident segment completely.
+//
+// Keys are held in registers during every counting pass, so one 64 KB SMEM
+// buffer suffices and two CTAs share an SM (their barrier waits overlap).
+//   1. CTA pass: counting sort by the 12 highest varying bits (window found by
+//      an OR/AND reduction); each thread owns 8 consecutive bins and
+//      insertion-sorts its small (<=16) sub-buckets itself.
+//   2. Sub-buckets of 17..256 keys: one warp each (dynamic), 8-bit counting
+//      pass in registers, lanes insertion-sort the children; larger children
+//      are queued again. Sub-buckets > 256 keys (heavy rows) take another CTA pass.
 // ---------------------------------------------------------------------------
+constexpr int kLocalItems = kLocalCap / kLocalThreads;  // 16 keys per thread
+
+// Debug instrumentation of the local stage (PRG_LOCAL_STATS=1 at compile time):
+// per-phase cycle sums and work counts accumulated into g_local_stats.
+#ifndef PRG_LOCAL_STATS
+#define PRG_LOCAL_STATS 0
+#endif
+__device__ unsigned long long g_local_stats[16];
+constexpr int kLocalWarps = kLocalThreads / 32;
+
 struct LocalSmem {
     uint64_t X[kLocalCap];
-    uint64_t Y[kLocalCap];
     uint32_t hist[kLocalBins];
-    uint32_t small_list[kLocalCap / 2];
-    uint32_t mid_list[kLocalCap / (kSmallMax + 1) + 1];
+    uint32_t whist[kLocalWarps][kRadix];
+    uint32_t mid_list[kLocalCap / (kSmallMax + 1) + 2];
     uint32_t big_list[kLocalCap / (kMidMax + 1) + 2];
-    uint32_t n_small, n_mid, n_big;
-    uint32_t seg_id;
-    uint64_t red_or[kLocalThreads / 32], red_and[kLocalThreads / 32];
-    uint32_t scan_tmp[kLocalThreads / 32 + 1];
+    uint32_t n_mid, n_big, mid_next, seg_id;
+    uint64_t red_or[kLocalWarps], red_and[kLocalWarps];
+    uint32_t scan_tmp[kLocalWarps + 1];
 };
 
 __device__ __forceinline__ uint32_t pack_range(uint32_t b, uint32_t m) { return (b << 14) | m; }
 __device__ __forceinline__ uint32_t range_b(uint32_t r) { return r >> 14; }
 __device__ __forceinline__ uint32_t range_m(uint32_t r) { return r & 0x3fffu; }
 
-__device__ __forceinline__ void push_range(LocalSmem& S, uint32_t b, uint32_t m) {
-    if (m <= 1) return;
-    if (m <= kSmallMax) S.small_list[atomicAdd(&S.n_small, 1u)] = pack_range(b, m);
-    else if (m <= kMidMax) S.mid_list[atomicAdd(&S.n_mid, 1u)] = pack_range(b, m);
-    else S.big_list[atomicAdd(&S.n_big, 1u)] = pack_range(b, m);
-}
-
-// One thread insertion-sorts X[b, b+m).
 __device__ __forceinline__ void thread_insertion(uint64_t* X, uint32_t b, uint32_t m) {
     for (uint32_t i = b + 1; i < b + m; ++i) {
-        uint64_t v = X[i];
+        const uint64_t v = X[i];
         uint32_t j = i;
         while (j > b && X[j - 1] > v) { X[j] = X[j - 1]; --j; }
         X[j] = v;
     }
 }
 
-// ---------------------------------------------------------------------------
-// Local stage: device routines
-// cta_counting_pass: CTA-wide counting sort of X[b,b+m) by the 12 highest
-// varying bits (via Y, copied back), pushing children ranges.
-// warp_bitonic_256: one warp sorts X[b,b+m), m <= 256, in registers.
-// cta_sort_segment: sorts a loaded segment X[0,n) completely.
-// ---------------------------------------------------------------------------
-static __device__ __noinline__ void cta_counting_pass(LocalSmem& S, uint32_t b, uint32_t m) {
+// CTA-wide counting pass over X[b, b+m) (m <= kLocalCap). All threads call.
+static __device__ __noinline__ void cta_pass(LocalSmem& S, uint32_t b, uint32_t m) {
     const unsigned tid = threadIdx.x, lane = dev::lane_id(), w = dev::warp_id();
-    constexpr unsigned NW = kLocalThreads / 32;
+    uint64_t k[kLocalItems];
     uint64_t o = 0, a = ~0ull;
-    for (uint32_t i = b + tid; i < b + m; i += kLocalThreads) { uint64_t x = S.X[i]; o |= x; a &= x; }
+#pragma unroll
+    for (int j = 0; j < kLocalItems; ++j) {
+        const uint32_t i = tid + j * kLocalThreads;
+        k[j] = i < m ? S.X[b + i] : 0ull;
+        if (i < m) { o |= k[j]; a &= k[j]; }
+    }
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
         o |= __shfl_xor_sync(0xffffffffu, o, d);
@@ -232,128 +240,163 @@ static __device__ __noinline__ void cta_counting_pass(LocalSmem& S, uint32_t b, 
     __syncthreads();
     o = 0; a = ~0ull;
 #pragma unroll
-    for (unsigned k = 0; k < NW; ++k) { o |= S.red_or[k]; a &= S.red_and[k]; }
+    for (int q = 0; q < kLocalWarps; ++q) { o |= S.red_or[q]; a &= S.red_and[q]; }
     const uint64_t diff = o ^ a;
-    __syncthreads();
-    if (diff == 0) return;  // all keys equal: already sorted
+    if (diff == 0) { __syncthreads(); return; }  // all equal: sorted
     const int h = 63 - __clzll((long long)diff);
     const int wb = h + 1 < kWindowBits ? h + 1 : kWindowBits;
     const int sh = h + 1 - wb;
     const unsigned mask = (1u << wb) - 1u, nb = 1u << wb;
-    for (unsigned i = tid; i < nb; i += kLocalThreads) S.hist[i] = 0;
+    constexpr unsigned BPT = kLocalBins / kLocalThreads;  // 8 bins per thread
+    for (unsigned i = tid; i < kLocalBins; i += kLocalThreads) S.hist[i] = 0;
     __syncthreads();
-    for (uint32_t i = b + tid; i < b + m; i += kLocalThreads)
-        atomicAdd(&S.hist[(unsigned)(S.X[i] >> sh) & mask], 1u);
-    __syncthreads();
-    // exclusive scan over nb bins, kLocalBins/kLocalThreads = 8 bins per thread
-    constexpr unsigned BPT = kLocalBins / kLocalThreads;
-    uint32_t c[BPT], s = 0;
 #pragma unroll
-    for (unsigned k = 0; k < BPT; ++k) {
-        unsigned bin = tid * BPT + k;
-        c[k] = bin < nb ? S.hist[bin] : 0u;
-        s += c[k];
+    for (int j = 0; j < kLocalItems; ++j)
+        if (tid + j * kLocalThreads < m) atomicAdd(&S.hist[(unsigned)(k[j] >> sh) & mask], 1u);
+    __syncthreads();
+    uint32_t c[BPT], tsum = 0;
+#pragma unroll
+    for (unsigned q = 0; q < BPT; ++q) {
+        const unsigned bin = tid * BPT + q;
+        c[q] = bin < nb ? S.hist[bin] : 0u;
+        tsum += c[q];
     }
     uint32_t tot;
-    uint32_t run = dev::block_excl_scan(s, S.scan_tmp, tot);
+    const uint32_t run0 = dev::block_excl_scan(tsum, S.scan_tmp, tot);
+    {
+        uint32_t run = run0;
 #pragma unroll
-    for (unsigned k = 0; k < BPT; ++k) {
-        unsigned bin = tid * BPT + k;
-        if (bin < nb) {
-            S.hist[bin] = run;
-            if (c[k] > 1) push_range(S, b + run, c[k]);
+        for (unsigned q = 0; q < BPT; ++q) {
+            const unsigned bin = tid * BPT + q;
+            if (bin < nb) S.hist[bin] = run;
+            if (c[q] > kMidMax) S.big_list[atomicAdd(&S.n_big, 1u)] = pack_range(b + run, c[q]);
+            else if (c[q] > kSmallMax) S.mid_list[atomicAdd(&S.n_mid, 1u)] = pack_range(b + run, c[q]);
+            run += c[q];
         }
-        run += c[k];
     }
     __syncthreads();
-    for (uint32_t i = b + tid; i < b + m; i += kLocalThreads) {
-        uint64_t x = S.X[i];
-        uint32_t p = atomicAdd(&S.hist[(unsigned)(x >> sh) & mask], 1u);
-        S.Y[b + p] = x;
-    }
+#pragma unroll
+    for (int j = 0; j < kLocalItems; ++j)
+        if (tid + j * kLocalThreads < m) S.X[b + atomicAdd(&S.hist[(unsigned)(k[j] >> sh) & mask], 1u)] = k[j];
     __syncthreads();
-    for (uint32_t i = b + tid; i < b + m; i += kLocalThreads) S.X[i] = S.Y[i];
+    {
+        uint32_t run = run0;
+#pragma unroll
+        for (unsigned q = 0; q < BPT; ++q) {
+            if (c[q] >= 2 && c[q] <= kSmallMax) thread_insertion(S.X, b + run, c[q]);
+            run += c[q];
+        }
+    }
     __syncthreads();
 }
 
-static __device__ __noinline__ void warp_bitonic_256(uint64_t* X, uint32_t b, uint32_t m) {
-    const unsigned lane = dev::lane_id();
-    uint64_t v[8];
+// One warp: counting pass over X[b, b+m) (17 <= m <= 256) by the 8 highest varying bits.
+static __device__ __noinline__ void warp_pass(LocalSmem& S, uint32_t b, uint32_t m) {
+    const unsigned lane = dev::lane_id(), w = dev::warp_id();
+    uint64_t k[8];
+    uint64_t o = 0, a = ~0ull;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-        uint32_t e = j * 32 + lane;
-        v[j] = e < m ? X[b + e] : ~0ull;
+        const uint32_t i = lane + j * 32;
+        k[j] = i < m ? S.X[b + i] : 0ull;
+        if (i < m) { o |= k[j]; a &= k[j]; }
     }
 #pragma unroll
-    for (int k = 2; k <= 256; k <<= 1) {
-#pragma unroll
-        for (int d = k >> 1; d > 0; d >>= 1) {
-            if (d >= 32) {
-                const int dj = d >> 5;
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const int jp = j ^ dj;
-                    if (jp > j) {
-                        const bool asc = (((j * 32 + lane) & k) == 0);
-                        const uint64_t x = v[j], y = v[jp];
-                        const bool sw = (x > y) == asc;
-                        v[j] = sw ? y : x;
-                        v[jp] = sw ? x : y;
-                    }
-                }
-            } else {
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const uint64_t other = __shfl_xor_sync(0xffffffffu, v[j], d);
-                    const bool asc = (((j * 32 + lane) & k) == 0);
-                    const bool lower = (lane & d) == 0;
-                    const bool keep_min = (lower == asc);
-                    v[j] = keep_min ? (v[j] < other ? v[j] : other) : (v[j] > other ? v[j] : other);
-                }
-            }
-        }
+    for (int d = 16; d > 0; d >>= 1) {
+        o |= __shfl_xor_sync(0xffffffffu, o, d);
+        a &= __shfl_xor_sync(0xffffffffu, a, d);
     }
+    const uint64_t diff = o ^ a;
+    if (diff == 0) return;
+    const int h = 63 - __clzll((long long)diff);
+    const int wb = h + 1 < 8 ? h + 1 : 8;
+    const int sh = h + 1 - wb;
+    const unsigned mask = (1u << wb) - 1u;
+    uint32_t* H = S.whist[w];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        uint32_t e = j * 32 + lane;
-        if (e < m) X[b + e] = v[j];
+    for (int q = 0; q < 8; ++q) H[lane * 8 + q] = 0;
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        if (lane + j * 32 < m) atomicAdd(&H[(unsigned)(k[j] >> sh) & mask], 1u);
+    __syncwarp();
+    uint32_t c[8], tsum = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) { c[q] = H[lane * 8 + q]; tsum += c[q]; }
+    const uint32_t incl = dev::warp_incl_scan(tsum);
+    uint32_t run = incl - tsum;
+    const uint32_t run0 = run;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        H[lane * 8 + q] = run;
+        if (c[q] > kSmallMax) S.mid_list[atomicAdd(&S.n_mid, 1u)] = pack_range(b + run, c[q]);
+        run += c[q];
     }
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        if (lane + j * 32 < m) S.X[b + atomicAdd(&H[(unsigned)(k[j] >> sh) & mask], 1u)] = k[j];
+    __syncwarp();
+    run = run0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        if (c[q] >= 2 && c[q] <= kSmallMax) thread_insertion(S.X, b + run, c[q]);
+        run += c[q];
+    }
+    __syncwarp();
 }
 
+// Sorts a loaded segment X[0, n) completely. All threads call.
 static __device__ __noinline__ void cta_sort_segment(LocalSmem& S, uint32_t n) {
-    if (threadIdx.x == 0) {
-        S.n_small = 0; S.n_mid = 0; S.n_big = 0;
-        push_range(S, 0, n);
-    }
+    if (threadIdx.x == 0) { S.n_mid = 0; S.n_big = 0; S.mid_next = 0; }
     __syncthreads();
+    if (n > kMidMax) {
+        cta_pass(S, 0, n);
+    } else if (n > kSmallMax) {
+        if (dev::warp_id() == 0) warp_pass(S, 0, n);
+        __syncthreads();
+    } else {
+        if (threadIdx.x == 0 && n > 1) thread_insertion(S.X, 0, n);
+        __syncthreads();
+        return;
+    }
     for (;;) {
-        const uint32_t nb = S.n_big;
+        // heavy sub-buckets: one CTA pass each
+        for (;;) {
+            const uint32_t nb = S.n_big;
+            __syncthreads();
+            if (nb == 0) break;
+            if (PRG_LOCAL_STATS && threadIdx.x == 0) atomicAdd(&g_local_stats[6], 1ull);
+            const uint32_t r = S.big_list[nb - 1];
+            __syncthreads();
+            if (threadIdx.x == 0) S.n_big = nb - 1;
+            __syncthreads();
+            cta_pass(S, range_b(r), range_m(r));
+        }
+        // mid sub-buckets: warps pull dynamically; children may be queued again
+        const uint32_t nm = S.n_mid;
+        const uint32_t first = S.mid_next;
         __syncthreads();
-        if (nb == 0) break;
-        const uint32_t r = S.big_list[nb - 1];
+        if (first >= nm) break;
+        for (;;) {
+            uint32_t i = 0;
+            if (dev::lane_id() == 0) i = atomicAdd(&S.mid_next, 1u);
+            i = __shfl_sync(0xffffffffu, i, 0);
+            if (i >= nm) break;
+            const uint32_t r = S.mid_list[i];
+            warp_pass(S, range_b(r), range_m(r));
+        }
         __syncthreads();
-        if (threadIdx.x == 0) S.n_big = nb - 1;
+        if (threadIdx.x == 0) S.mid_next = nm;
         __syncthreads();
-        cta_counting_pass(S, range_b(r), range_m(r));
     }
-    const uint32_t nm = S.n_mid, ns = S.n_small;
-    for (uint32_t i = dev::warp_id(); i < nm; i += kLocalThreads / 32) {
-        const uint32_t r = S.mid_list[i];
-        warp_bitonic_256(S.X, range_b(r), range_m(r));
-    }
-    for (uint32_t i = threadIdx.x; i < ns; i += kLocalThreads) {
-        const uint32_t r = S.small_list[i];
-        thread_insertion(S.X, range_b(r), range_m(r));
-    }
-    __syncthreads();
 }
-
 
 // Dst must provide:
 //   __device__ void store(uint64_t pos, uint64_t key, bool has_prev, uint64_t prev) const;
 // (has_prev/prev: the preceding key in sorted order when it lies in the same segment).
 template <class Dst>
-__global__ void __launch_bounds__(kLocalThreads, 1)
+__global__ void __launch_bounds__(kLocalThreads, 2)
     local_sort_kernel(const uint64_t* __restrict__ keys0, const uint64_t* __restrict__ keys1,
                       const Seg* __restrict__ fin, const uint32_t* __restrict__ n_fin,
                       uint32_t* __restrict__ work, Dst dst) {
@@ -379,12 +422,25 @@ __global__ void __launch_bounds__(kLocalThreads, 1)
             }
             continue;
         }
+        long long c0 = PRG_LOCAL_STATS ? clock64() : 0;
         for (uint32_t i = threadIdx.x; i < n; i += kLocalThreads) S.X[i] = src[sg.start + i];
         __syncthreads();
+        long long c1 = PRG_LOCAL_STATS ? clock64() : 0;
         cta_sort_segment(S, n);
+        long long c2 = PRG_LOCAL_STATS ? clock64() : 0;
         for (uint32_t i = threadIdx.x; i < n; i += kLocalThreads)
             dst.store(sg.start + i, S.X[i], i > 0, i > 0 ? S.X[i - 1] : 0ull);
         __syncthreads();
+        if (PRG_LOCAL_STATS && threadIdx.x == 0) {
+            long long c3 = clock64();
+            atomicAdd(&g_local_stats[0], 1ull);
+            atomicAdd(&g_local_stats[1], (unsigned long long)n);
+            atomicAdd(&g_local_stats[2], (unsigned long long)(c1 - c0));
+            atomicAdd(&g_local_stats[3], (unsigned long long)(c2 - c1));
+            atomicAdd(&g_local_stats[4], (unsigned long long)(c3 - c2));
+            atomicAdd(&g_local_stats[5], (unsigned long long)S.n_mid);
+            atomicAdd(&g_local_stats[8 + min(7, 31 - __clz(n | 1) - 6 < 0 ? 0 : 31 - __clz(n | 1) - 6)], 1ull);
+        }
     }
 }
 
@@ -415,7 +471,8 @@ void run_segmented_levels(SortWorkspace& ws, int levels_left, cudaStream_t s);
 // exception list exactly once).
 template <class Src, class Dst>
 void msd_sort_split(Src src_hist, Src src_scat, size_t n, int key_bits, Dst dst, SortWorkspace& ws,
-                    cudaStream_t s) {
+                    cudaStream_t s, const char* tag = "sort") {
+    const std::string t(tag);
     if (n == 0) return;
     sort_workspace_init(ws, n, s);
     const int bits1 = key_bits < 8 ? (key_bits > 0 ? key_bits : 1) : 8;
@@ -425,7 +482,7 @@ void msd_sort_split(Src src_hist, Src src_scat, size_t n, int key_bits, Dst dst,
     const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)num_sms() * 4);
     PRG_CUDA(cudaMemsetAsync(ws.counters.get(), 0, 8 * sizeof(uint32_t), s));
     {
-        ProfScope prof("sort_l1_hist", s);
+        ProfScope prof(t + "_l1_hist", s);
         if (Src::kSmem > 48 * 1024)
             PRG_CUDA(cudaFuncSetAttribute(l1_hist_kernel<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)Src::kSmem));
@@ -435,7 +492,7 @@ void msd_sort_split(Src src_hist, Src src_scat, size_t n, int key_bits, Dst dst,
         exclusive_scan_u32(ws.hist.get(), ws.off.get(), (size_t)kRadix * ntiles, nullptr, s);
     }
     {
-        ProfScope prof("sort_l1_scatter", s);
+        ProfScope prof(t + "_l1_scatter", s);
         const size_t smem = (size_t)kTile * sizeof(uint64_t) + Src::kSmem;
         PRG_CUDA(cudaFuncSetAttribute(l1_scatter_kernel<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
@@ -448,22 +505,23 @@ void msd_sort_split(Src src_hist, Src src_scat, size_t n, int key_bits, Dst dst,
         PRG_LAUNCH_CHECK();
     }
     {
-        ProfScope prof("sort_levels", s);
+        ProfScope prof(t + "_levels", s);
         run_segmented_levels(ws, (shift1 + 7) / 8, s);
     }
     {
-        ProfScope prof("sort_local", s);
+        ProfScope prof(t + "_local", s);
         PRG_CUDA(cudaFuncSetAttribute(local_sort_kernel<Dst>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)local_smem_bytes()));
-        local_sort_kernel<Dst><<<num_sms(), kLocalThreads, local_smem_bytes(), s>>>(
+        local_sort_kernel<Dst><<<num_sms() * 2, kLocalThreads, local_smem_bytes(), s>>>(
             ws.keys[0].get(), ws.keys[1].get(), ws.fin.get(), ws.counters.get() + 2, ws.counters.get() + 3, dst);
         PRG_LAUNCH_CHECK();
     }
 }
 
 template <class Src, class Dst>
-void msd_sort(Src src, size_t n, int key_bits, Dst dst, SortWorkspace& ws, cudaStream_t s) {
-    msd_sort_split(src, src, n, key_bits, dst, ws, s);
+void msd_sort(Src src, size_t n, int key_bits, Dst dst, SortWorkspace& ws, cudaStream_t s,
+              const char* tag = "sort") {
+    msd_sort_split(src, src, n, key_bits, dst, ws, s, tag);
 }
 
 }  // namespace prg::sort

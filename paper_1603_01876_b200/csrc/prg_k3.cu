@@ -893,7 +893,8 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
             scat.exc_key = nullptr;
             sort::SortWorkspace ws;
             sort::msd_sort_split(src, scat, (size_t)nnz, 2 * P.sb + 1,
-                                 CscDst{P.csc_idx.get(), P.colptr.get(), exc_cnt.get(), P.sb}, ws, s, "k3t");
+                                 CscDst{P.csc_idx.get(), P.colptr.get(), exc_cnt.get(), P.sb}, ws, s, "k3t",
+                                 /*payload_bits=*/1);
         }
         // colptr[n] = nnz, then fill empty columns with the next column start.
         const uint32_t nz = (uint32_t)nnz;

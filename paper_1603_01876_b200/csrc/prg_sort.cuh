@@ -175,61 +175,52 @@ __global__ void classify_l1_kernel(const uint32_t* __restrict__ off, uint32_t nt
                                    uint32_t* __restrict__ n_fin);
 
 // ---------------------------------------------------------------------------
-// Local stage: one CTA sorts one SMEM-resident segment completely.
-//
-// Keys are held in registers during every counting pass, so one 64 KB SMEM
-// buffer suffices and two CTAs share an SM (their barrier waits overlap).
-//   1. CTA pass: counting sort by the 12 highest varying bits (window found by
-//      an OR/AND reduction); each thread owns 8 consecutive bins and
-//      insertion-sorts its small (<=16) sub-buckets itself.
-//   2. Sub-buckets of 17..256 keys: one warp each (dynamic), 8-bit counting
-//      pass in registers, lanes insertion-sort the children; larger children
-//      are queued again. Sub-buckets > 256 keys (heavy rows) take another CTA pass.
+// Local stage: one CTA sorts one SMEM-resident segment completely with a
+// stable LSD radix sort over the segment's varying bit span only (found by an
+// OR/AND reduction; the low `payload_bits` are carried, not sorted). The cost
+// is independent of the key distribution — an MSD local stage degraded badly
+// on heavy Kronecker rows (ncu: 58% barrier stalls, ~20 cycles/key).
+// Ranking (CUB-style, no ballots, no match_any): thread t owns a contiguous run
+// of 16 keys in the current order and counts them into thread-private 16-bit
+// counters for (digit, t) — threads 2p and 2p+1 share one 32-bit word, so one
+// conflict-free SMEM atomic per key returns the in-thread rank. A block scan
+// over (digit, thread) then gives stable scatter offsets. Keys stay in
+// registers; X is padded (one slot per 16) so blocked reads are conflict-light.
 // ---------------------------------------------------------------------------
 constexpr int kLocalItems = kLocalCap / kLocalThreads;  // 16 keys per thread
+constexpr int kLocalWarps = kLocalThreads / 32;
+constexpr int kLsdBits = 5;
+constexpr int kLsdDigits = 1 << kLsdBits;
+constexpr int kCntWords = kLsdDigits * (kLocalThreads / 2);  // packed counters
+static_assert(kLocalItems == 16, "local stage assumes 16 keys per thread");
 
-// Debug instrumentation of the local stage (PRG_LOCAL_STATS=1 at compile time):
-// per-phase cycle sums and work counts accumulated into g_local_stats.
+// Debug instrumentation of the local stage (PRG_LOCAL_STATS=1 at compile time).
 #ifndef PRG_LOCAL_STATS
 #define PRG_LOCAL_STATS 0
 #endif
 __device__ unsigned long long g_local_stats[16];
-constexpr int kLocalWarps = kLocalThreads / 32;
+
+__host__ __device__ constexpr uint32_t xpad(uint32_t i) { return i + (i >> 4); }
 
 struct LocalSmem {
-    uint64_t X[kLocalCap];
-    uint32_t hist[kLocalBins];
-    uint32_t whist[kLocalWarps][kRadix];
-    uint32_t mid_list[kLocalCap / (kSmallMax + 1) + 2];
-    uint32_t big_list[kLocalCap / (kMidMax + 1) + 2];
-    uint32_t n_mid, n_big, mid_next, seg_id;
+    uint64_t X[kLocalCap + kLocalCap / 16];
+    uint32_t cnt[kCntWords + kCntWords / 16];  // [digit][thread pair], padded (xpad)
+    uint32_t seg_id;
     uint64_t red_or[kLocalWarps], red_and[kLocalWarps];
     uint32_t scan_tmp[kLocalWarps + 1];
 };
 
-__device__ __forceinline__ uint32_t pack_range(uint32_t b, uint32_t m) { return (b << 14) | m; }
-__device__ __forceinline__ uint32_t range_b(uint32_t r) { return r >> 14; }
-__device__ __forceinline__ uint32_t range_m(uint32_t r) { return r & 0x3fffu; }
-
-__device__ __forceinline__ void thread_insertion(uint64_t* X, uint32_t b, uint32_t m) {
-    for (uint32_t i = b + 1; i < b + m; ++i) {
-        const uint64_t v = X[i];
-        uint32_t j = i;
-        while (j > b && X[j - 1] > v) { X[j] = X[j - 1]; --j; }
-        X[j] = v;
-    }
-}
-
-// CTA-wide counting pass over X[b, b+m) (m <= kLocalCap). All threads call.
-static __device__ __noinline__ void cta_pass(LocalSmem& S, uint32_t b, uint32_t m) {
+// Sorts X[0, n) (n <= kLocalCap; X indexed through xpad). All threads call.
+static __device__ __forceinline__ void cta_lsd_sort(LocalSmem& S, uint32_t n, int payload_bits) {
     const unsigned tid = threadIdx.x, lane = dev::lane_id(), w = dev::warp_id();
+    const uint32_t half = (tid & 1u) * 16u;
     uint64_t k[kLocalItems];
     uint64_t o = 0, a = ~0ull;
 #pragma unroll
     for (int j = 0; j < kLocalItems; ++j) {
-        const uint32_t i = tid + j * kLocalThreads;
-        k[j] = i < m ? S.X[b + i] : 0ull;
-        if (i < m) { o |= k[j]; a &= k[j]; }
+        const uint32_t i = tid * kLocalItems + j;
+        k[j] = i < n ? S.X[xpad(i)] : ~0ull;
+        if (i < n) { o |= k[j]; a &= k[j]; }
     }
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
@@ -241,154 +232,55 @@ static __device__ __noinline__ void cta_pass(LocalSmem& S, uint32_t b, uint32_t 
     o = 0; a = ~0ull;
 #pragma unroll
     for (int q = 0; q < kLocalWarps; ++q) { o |= S.red_or[q]; a &= S.red_and[q]; }
-    const uint64_t diff = o ^ a;
-    if (diff == 0) { __syncthreads(); return; }  // all equal: sorted
-    const int h = 63 - __clzll((long long)diff);
-    const int wb = h + 1 < kWindowBits ? h + 1 : kWindowBits;
-    const int sh = h + 1 - wb;
-    const unsigned mask = (1u << wb) - 1u, nb = 1u << wb;
-    constexpr unsigned BPT = kLocalBins / kLocalThreads;  // 8 bins per thread
-    for (unsigned i = tid; i < kLocalBins; i += kLocalThreads) S.hist[i] = 0;
-    __syncthreads();
+    const uint64_t diff = (o ^ a) & (~0ull << payload_bits);
+    if (diff == 0) { __syncthreads(); return; }  // equal above the payload: sorted
+    const int lo = __ffsll((long long)diff) - 1;
+    const int hi = 63 - __clzll((long long)diff);
+    constexpr int WPT = kCntWords / kLocalThreads;  // counter words per thread (16)
+    for (int sh = lo; sh <= hi; sh += kLsdBits) {
 #pragma unroll
-    for (int j = 0; j < kLocalItems; ++j)
-        if (tid + j * kLocalThreads < m) atomicAdd(&S.hist[(unsigned)(k[j] >> sh) & mask], 1u);
-    __syncthreads();
-    uint32_t c[BPT], tsum = 0;
-#pragma unroll
-    for (unsigned q = 0; q < BPT; ++q) {
-        const unsigned bin = tid * BPT + q;
-        c[q] = bin < nb ? S.hist[bin] : 0u;
-        tsum += c[q];
-    }
-    uint32_t tot;
-    const uint32_t run0 = dev::block_excl_scan(tsum, S.scan_tmp, tot);
-    {
-        uint32_t run = run0;
-#pragma unroll
-        for (unsigned q = 0; q < BPT; ++q) {
-            const unsigned bin = tid * BPT + q;
-            if (bin < nb) S.hist[bin] = run;
-            if (c[q] > kMidMax) S.big_list[atomicAdd(&S.n_big, 1u)] = pack_range(b + run, c[q]);
-            else if (c[q] > kSmallMax) S.mid_list[atomicAdd(&S.n_mid, 1u)] = pack_range(b + run, c[q]);
-            run += c[q];
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < kLocalItems; ++j)
-        if (tid + j * kLocalThreads < m) S.X[b + atomicAdd(&S.hist[(unsigned)(k[j] >> sh) & mask], 1u)] = k[j];
-    __syncthreads();
-    {
-        uint32_t run = run0;
-#pragma unroll
-        for (unsigned q = 0; q < BPT; ++q) {
-            if (c[q] >= 2 && c[q] <= kSmallMax) thread_insertion(S.X, b + run, c[q]);
-            run += c[q];
-        }
-    }
-    __syncthreads();
-}
-
-// One warp: counting pass over X[b, b+m) (17 <= m <= 256) by the 8 highest varying bits.
-static __device__ __noinline__ void warp_pass(LocalSmem& S, uint32_t b, uint32_t m) {
-    const unsigned lane = dev::lane_id(), w = dev::warp_id();
-    uint64_t k[8];
-    uint64_t o = 0, a = ~0ull;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        const uint32_t i = lane + j * 32;
-        k[j] = i < m ? S.X[b + i] : 0ull;
-        if (i < m) { o |= k[j]; a &= k[j]; }
-    }
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) {
-        o |= __shfl_xor_sync(0xffffffffu, o, d);
-        a &= __shfl_xor_sync(0xffffffffu, a, d);
-    }
-    const uint64_t diff = o ^ a;
-    if (diff == 0) return;
-    const int h = 63 - __clzll((long long)diff);
-    const int wb = h + 1 < 8 ? h + 1 : 8;
-    const int sh = h + 1 - wb;
-    const unsigned mask = (1u << wb) - 1u;
-    uint32_t* H = S.whist[w];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) H[lane * 8 + q] = 0;
-    __syncwarp();
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-        if (lane + j * 32 < m) atomicAdd(&H[(unsigned)(k[j] >> sh) & mask], 1u);
-    __syncwarp();
-    uint32_t c[8], tsum = 0;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) { c[q] = H[lane * 8 + q]; tsum += c[q]; }
-    const uint32_t incl = dev::warp_incl_scan(tsum);
-    uint32_t run = incl - tsum;
-    const uint32_t run0 = run;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-        H[lane * 8 + q] = run;
-        if (c[q] > kSmallMax) S.mid_list[atomicAdd(&S.n_mid, 1u)] = pack_range(b + run, c[q]);
-        run += c[q];
-    }
-    __syncwarp();
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-        if (lane + j * 32 < m) S.X[b + atomicAdd(&H[(unsigned)(k[j] >> sh) & mask], 1u)] = k[j];
-    __syncwarp();
-    run = run0;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-        if (c[q] >= 2 && c[q] <= kSmallMax) thread_insertion(S.X, b + run, c[q]);
-        run += c[q];
-    }
-    __syncwarp();
-}
-
-// Sorts a loaded segment X[0, n) completely. All threads call.
-static __device__ __noinline__ void cta_sort_segment(LocalSmem& S, uint32_t n) {
-    if (threadIdx.x == 0) { S.n_mid = 0; S.n_big = 0; S.mid_next = 0; }
-    __syncthreads();
-    if (n > kMidMax) {
-        cta_pass(S, 0, n);
-    } else if (n > kSmallMax) {
-        if (dev::warp_id() == 0) warp_pass(S, 0, n);
+        for (int q = 0; q < WPT; ++q) S.cnt[xpad(tid * WPT + q)] = 0;
         __syncthreads();
-    } else {
-        if (threadIdx.x == 0 && n > 1) thread_insertion(S.X, 0, n);
-        __syncthreads();
-        return;
-    }
-    for (;;) {
-        // heavy sub-buckets: one CTA pass each
-        for (;;) {
-            const uint32_t nb = S.n_big;
-            __syncthreads();
-            if (nb == 0) break;
-            if (PRG_LOCAL_STATS && threadIdx.x == 0) atomicAdd(&g_local_stats[6], 1ull);
-            const uint32_t r = S.big_list[nb - 1];
-            __syncthreads();
-            if (threadIdx.x == 0) S.n_big = nb - 1;
-            __syncthreads();
-            cta_pass(S, range_b(r), range_m(r));
-        }
-        // mid sub-buckets: warps pull dynamically; children may be queued again
-        const uint32_t nm = S.n_mid;
-        const uint32_t first = S.mid_next;
-        __syncthreads();
-        if (first >= nm) break;
-        for (;;) {
-            uint32_t i = 0;
-            if (dev::lane_id() == 0) i = atomicAdd(&S.mid_next, 1u);
-            i = __shfl_sync(0xffffffffu, i, 0);
-            if (i >= nm) break;
-            const uint32_t r = S.mid_list[i];
-            warp_pass(S, range_b(r), range_m(r));
+        uint32_t rk[kLocalItems / 2];
+#pragma unroll
+        for (int j = 0; j < kLocalItems; ++j) {
+            const uint32_t d = (uint32_t)(k[j] >> sh) & (kLsdDigits - 1);
+            const uint32_t old = atomicAdd(&S.cnt[xpad(d * (kLocalThreads / 2) + (tid >> 1))], 1u << half);
+            const uint32_t r = (old >> half) & 0xffffu;
+            if (j & 1) rk[j >> 1] |= r << 16; else rk[j >> 1] = r;
         }
         __syncthreads();
-        if (threadIdx.x == 0) S.mid_next = nm;
+        {   // exclusive scan over words in (digit, pair) order; each word holds
+            // (even thread, odd thread) counts -> (prefix_even, prefix_odd)
+            uint32_t ts = 0;
+#pragma unroll 4
+            for (int q = 0; q < WPT; ++q) {
+                const uint32_t wv = S.cnt[xpad(tid * WPT + q)];
+                ts += (wv & 0xffffu) + (wv >> 16);
+            }
+            uint32_t tot;
+            uint32_t run = dev::block_excl_scan(ts, S.scan_tmp, tot);
+#pragma unroll 4
+            for (int q = 0; q < WPT; ++q) {
+                const uint32_t wv = S.cnt[xpad(tid * WPT + q)];
+                const uint32_t lo16 = wv & 0xffffu;
+                S.cnt[xpad(tid * WPT + q)] = run | ((run + lo16) << 16);
+                run += lo16 + (wv >> 16);
+            }
+        }
         __syncthreads();
+#pragma unroll
+        for (int j = 0; j < kLocalItems; ++j) {
+            const uint32_t d = (uint32_t)(k[j] >> sh) & (kLsdDigits - 1);
+            const uint32_t pre = (S.cnt[xpad(d * (kLocalThreads / 2) + (tid >> 1))] >> half) & 0xffffu;
+            const uint32_t r = (rk[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
+            S.X[xpad(pre + r)] = k[j];
+        }
+        __syncthreads();
+        if (sh + kLsdBits <= hi) {
+#pragma unroll
+            for (int j = 0; j < kLocalItems; ++j) k[j] = S.X[xpad(tid * kLocalItems + j)];
+        }
     }
 }
 
@@ -399,7 +291,7 @@ template <class Dst>
 __global__ void __launch_bounds__(kLocalThreads, 2)
     local_sort_kernel(const uint64_t* __restrict__ keys0, const uint64_t* __restrict__ keys1,
                       const Seg* __restrict__ fin, const uint32_t* __restrict__ n_fin,
-                      uint32_t* __restrict__ work, Dst dst) {
+                      uint32_t* __restrict__ work, Dst dst, int payload_bits) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     LocalSmem& S = *reinterpret_cast<LocalSmem*>(smem_raw);
     const uint32_t nf = *n_fin;
@@ -423,13 +315,13 @@ __global__ void __launch_bounds__(kLocalThreads, 2)
             continue;
         }
         long long c0 = PRG_LOCAL_STATS ? clock64() : 0;
-        for (uint32_t i = threadIdx.x; i < n; i += kLocalThreads) S.X[i] = src[sg.start + i];
+        for (uint32_t i = threadIdx.x; i < n; i += kLocalThreads) S.X[xpad(i)] = src[sg.start + i];
         __syncthreads();
         long long c1 = PRG_LOCAL_STATS ? clock64() : 0;
-        cta_sort_segment(S, n);
+        cta_lsd_sort(S, n, payload_bits);
         long long c2 = PRG_LOCAL_STATS ? clock64() : 0;
         for (uint32_t i = threadIdx.x; i < n; i += kLocalThreads)
-            dst.store(sg.start + i, S.X[i], i > 0, i > 0 ? S.X[i - 1] : 0ull);
+            dst.store(sg.start + i, S.X[xpad(i)], i > 0, i > 0 ? S.X[xpad(i - 1)] : 0ull);
         __syncthreads();
         if (PRG_LOCAL_STATS && threadIdx.x == 0) {
             long long c3 = clock64();
@@ -438,7 +330,7 @@ __global__ void __launch_bounds__(kLocalThreads, 2)
             atomicAdd(&g_local_stats[2], (unsigned long long)(c1 - c0));
             atomicAdd(&g_local_stats[3], (unsigned long long)(c2 - c1));
             atomicAdd(&g_local_stats[4], (unsigned long long)(c3 - c2));
-            atomicAdd(&g_local_stats[5], (unsigned long long)S.n_mid);
+
             atomicAdd(&g_local_stats[8 + min(7, 31 - __clz(n | 1) - 6 < 0 ? 0 : 31 - __clz(n | 1) - 6)], 1ull);
         }
     }
@@ -471,7 +363,7 @@ void run_segmented_levels(SortWorkspace& ws, int levels_left, cudaStream_t s);
 // exception list exactly once).
 template <class Src, class Dst>
 void msd_sort_split(Src src_hist, Src src_scat, size_t n, int key_bits, Dst dst, SortWorkspace& ws,
-                    cudaStream_t s, const char* tag = "sort") {
+                    cudaStream_t s, const char* tag = "sort", int payload_bits = 0) {
     const std::string t(tag);
     if (n == 0) return;
     sort_workspace_init(ws, n, s);
@@ -513,7 +405,8 @@ void msd_sort_split(Src src_hist, Src src_scat, size_t n, int key_bits, Dst dst,
         PRG_CUDA(cudaFuncSetAttribute(local_sort_kernel<Dst>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)local_smem_bytes()));
         local_sort_kernel<Dst><<<num_sms() * 2, kLocalThreads, local_smem_bytes(), s>>>(
-            ws.keys[0].get(), ws.keys[1].get(), ws.fin.get(), ws.counters.get() + 2, ws.counters.get() + 3, dst);
+            ws.keys[0].get(), ws.keys[1].get(), ws.fin.get(), ws.counters.get() + 2, ws.counters.get() + 3, dst,
+            payload_bits);
         PRG_LAUNCH_CHECK();
     }
 }

@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(kTileThreads) seg_hist_kernel(
     }
 }
 
-__global__ void __launch_bounds__(kTileThreads) seg_scatter_kernel(
+__global__ void __launch_bounds__(kTileThreads, 2) seg_scatter_kernel(
     const uint64_t* __restrict__ keys0, const uint64_t* __restrict__ keys1,
     uint64_t* __restrict__ out0, uint64_t* __restrict__ out1, const Seg* __restrict__ active,
     const uint32_t* __restrict__ seg_tile0, const uint64_t* __restrict__ seg_elem0,
@@ -165,13 +165,12 @@ __global__ void __launch_bounds__(kTileThreads) seg_scatter_kernel(
         const int cnt = (int)min((uint64_t)kTile, (uint64_t)sg.size - (uint64_t)ti * kTile);
         const unsigned mask = (1u << sg.bits) - 1u;
         uint64_t k[kTileItems];
-        uint32_t r[kTileItems];
 #pragma unroll
         for (int j = 0; j < kTileItems; ++j) {
             int li = j * kTileThreads + threadIdx.x;
             if (li < cnt) {
                 k[j] = src[base + li];
-                r[j] = atomicAdd(&h[(unsigned)(k[j] >> sg.shift) & mask], 1u);
+                atomicAdd(&h[(unsigned)(k[j] >> sg.shift) & mask], 1u);
             }
         }
         __syncthreads();
@@ -180,6 +179,7 @@ __global__ void __launch_bounds__(kTileThreads) seg_scatter_kernel(
             uint32_t ex = dev::block_excl_scan(v, scan_tmp, tot);
             if (threadIdx.x < kRadix) {
                 lstart[threadIdx.x] = ex;
+                h[threadIdx.x] = ex;  // per-digit cursor
                 const size_t hb = (size_t)seg_tile0[si] * kRadix;
                 // off is relative to the concatenation of active segments
                 gbase[threadIdx.x] = sg.start + (off[hb + (size_t)threadIdx.x * seg_nt + ti] - e0);
@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(kTileThreads) seg_scatter_kernel(
 #pragma unroll
         for (int j = 0; j < kTileItems; ++j) {
             int li = j * kTileThreads + threadIdx.x;
-            if (li < cnt) skeys[lstart[(unsigned)(k[j] >> sg.shift) & mask] + r[j]] = k[j];
+            if (li < cnt) skeys[atomicAdd(&h[(unsigned)(k[j] >> sg.shift) & mask], 1u)] = k[j];
         }
         __syncthreads();
         for (int i = threadIdx.x; i < cnt; i += kTileThreads) {

@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(kTileThreads) l1_hist_kernel(Src src, size_t n
 
 // Tile-local counting sort in SMEM, then per-digit contiguous writes.
 template <class Src>
-__global__ void __launch_bounds__(kTileThreads) l1_scatter_kernel(Src src, size_t n, int shift,
+__global__ void __launch_bounds__(kTileThreads, 2) l1_scatter_kernel(Src src, size_t n, int shift,
                                                                   unsigned dmask, uint32_t ntiles,
                                                                   const uint32_t* __restrict__ off,
                                                                   uint64_t* __restrict__ out) {
@@ -86,13 +86,12 @@ __global__ void __launch_bounds__(kTileThreads) l1_scatter_kernel(Src src, size_
         src.prepare(base, cnt, src_smem);
         __syncthreads();
         uint64_t k[kTileItems];
-        uint32_t r[kTileItems];
 #pragma unroll
         for (int j = 0; j < kTileItems; ++j) {
             int li = j * kTileThreads + threadIdx.x;
             if (li < cnt) {
                 k[j] = src.key(base + li, li, src_smem);
-                r[j] = atomicAdd(&h[(unsigned)(k[j] >> shift) & dmask], 1u);
+                atomicAdd(&h[(unsigned)(k[j] >> shift) & dmask], 1u);
             }
         }
         __syncthreads();
@@ -101,6 +100,7 @@ __global__ void __launch_bounds__(kTileThreads) l1_scatter_kernel(Src src, size_
             uint32_t ex = dev::block_excl_scan(v, scan_tmp, tot);
             if (threadIdx.x < kRadix) {
                 lstart[threadIdx.x] = ex;
+                h[threadIdx.x] = ex;  // becomes the per-digit cursor
                 gbase[threadIdx.x] = off[(size_t)threadIdx.x * ntiles + t];
             }
         }
@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(kTileThreads) l1_scatter_kernel(Src src, size_
 #pragma unroll
         for (int j = 0; j < kTileItems; ++j) {
             int li = j * kTileThreads + threadIdx.x;
-            if (li < cnt) skeys[lstart[(unsigned)(k[j] >> shift) & dmask] + r[j]] = k[j];
+            if (li < cnt) skeys[atomicAdd(&h[(unsigned)(k[j] >> shift) & dmask], 1u)] = k[j];
         }
         __syncthreads();
         for (int i = threadIdx.x; i < cnt; i += kTileThreads) {
@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(kTileThreads) seg_hist_kernel(
     const uint32_t* __restrict__ tile_seg, const uint32_t* __restrict__ tile_idx,
     const uint32_t* __restrict__ n_tiles, uint32_t* __restrict__ hist);
 
-__global__ void __launch_bounds__(kTileThreads) seg_scatter_kernel(
+__global__ void __launch_bounds__(kTileThreads, 2) seg_scatter_kernel(
     const uint64_t* __restrict__ keys0, const uint64_t* __restrict__ keys1,
     uint64_t* __restrict__ out0, uint64_t* __restrict__ out1, const Seg* __restrict__ active,
     const uint32_t* __restrict__ seg_tile0, const uint64_t* __restrict__ seg_elem0,

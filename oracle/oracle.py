@@ -235,3 +235,44 @@ def ref_pagerank_step(r, row_offsets, cols, values, n, damping=0.85):
     out = np.empty(n, dtype=np.float64)
     norm = _rstep(n, len(cols), _c64(row_offsets), _c64(cols), _cf(values), _cf(r), damping, out)
     return out, norm
+
+
+# ---- K2 step-level restatements (kernel2_filter.cpp:12-152) -------------
+_bld = _sig(_lib, "oracle_build_adjacency", C.c_int64, [_i64p, C.c_int64, C.c_int64, _i64p, _i64p, _i64p])
+_ind = _sig(_lib, "oracle_in_degree", None, [C.c_int64, C.c_int64, _i64p, _i64p, _i64p])
+_zc = _sig(_lib, "oracle_zero_columns", C.c_int64, [C.c_int64, _i64p, _i64p, _i64p, _i64p, _i64p, _i64p, _i64p])
+_rn = _sig(_lib, "oracle_row_normalize", None, [C.c_int64, _i64p, _i64p, _f64p])
+
+
+def build_adjacency(uv, n: int):
+    """CountMatrix as (row_offsets, cols, counts); raises ValueError like build_from."""
+    uv = np.ascontiguousarray(uv, dtype=np.int64).reshape(-1, 2)
+    m = len(uv)
+    ro = np.empty(n + 1, dtype=np.int64)
+    cols = np.empty(max(m, 1), dtype=np.int64)
+    cnt = np.empty(max(m, 1), dtype=np.int64)
+    nnz = _bld(uv, m, n, ro, cols, cnt)
+    if nnz < 0:
+        raise ValueError({-1: "label outside [1, n]", -2: "input not sorted by start vertex",
+                          -3: "vertex count must be positive"}[int(nnz)])
+    return ro, cols[:nnz].copy(), cnt[:nnz].copy()
+
+
+def in_degree(n, cols, counts):
+    d = np.empty(n, dtype=np.int64)
+    _ind(n, len(cols), _c64(cols), _c64(counts), d)
+    return d
+
+
+def zero_columns(n, row_offsets, cols, counts, d_in):
+    ro = np.empty(n + 1, dtype=np.int64)
+    oc = np.empty(max(len(cols), 1), dtype=np.int64)
+    ocnt = np.empty(max(len(cols), 1), dtype=np.int64)
+    nz = _zc(n, _c64(row_offsets), _c64(cols), _c64(counts), _c64(d_in), ro, oc, ocnt)
+    return ro, oc[:nz].copy(), ocnt[:nz].copy()
+
+
+def row_normalize(n, row_offsets, counts):
+    v = np.zeros(max(len(counts), 1), dtype=np.float64)
+    _rn(n, _c64(row_offsets), _c64(counts), v)
+    return v[: len(counts)]

@@ -29,7 +29,8 @@ HEADER_SYMBOLS = (
     "prg_k0_generate_device", "prg_k1_sort_device", "prg_k1_sort_host", "prg_k2_filter_device",
     "prg_k2_filter_host", "prg_matrix_info", "prg_matrix_download", "prg_matrix_device_arrays",
     "prg_matrix_from_host", "prg_matrix_destroy", "prg_k3_pagerank_device", "prg_k3_pagerank_host",
-    "prg_init_rank_device", "prg_pagerank_step_device",
+    "prg_init_rank_device", "prg_pagerank_step_device", "prg_launch_count", "prg_profile_enable",
+    "prg_profile_report",
 )
 
 
@@ -69,6 +70,9 @@ def lib() -> C.CDLL:
             "prg_k3_pagerank_host": (i32, [i64, i64, vp, vp, vp, f64, i32, u64, i32, vp, vp]),
             "prg_init_rank_device": (i32, [i64, u64, i32, vp, vp, vp]),
             "prg_pagerank_step_device": (i32, [vp, vp, f64, i32, vp, vp, vp]),
+            "prg_launch_count": (i64, []),
+            "prg_profile_enable": (None, [i32]),
+            "prg_profile_report": (i64, [vp, i64, i32]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)

@@ -1,0 +1,277 @@
+"""GPU parity: the CUDA path (through the C-ABI, lib/libprg.so) vs the pinned
+oracle and the reference-generated golden vectors.
+
+Bars (BASELINE.json north_star): K1 and K2 structure bit-exact; K2 values
+bit-exact (stricter than the 1e-12 asked for); K3 ranks within 1e-10 relative
+L1 of the reference in the timed mode and bit-identical in the parity mode.
+"""
+import numpy as np
+import pytest
+
+from conftest import canonical, golden, rel_l1
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+K3_TOL = 1e-10          # north_star: K3 ranks within 1e-10 relative L1
+K3_ACCURATE_TOL = 1e-13  # vs the Neumaier-sum restatement
+
+CONFIGS = [(4, 1, O.GRAPH500), (8, 3, O.GRAPH500), (10, 55, O.GRAPH500), (12, 2, O.UNIFORM),
+           (14, 7, O.GRAPH500), (16, 1, O.GRAPH500)]
+
+
+@pytest.fixture(scope="module")
+def capi(cuda):
+    from paper_1603_01876_b200 import capi as c
+
+    return c
+
+
+def t(a):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.int64)).cuda()
+
+
+# ---- K0 ----------------------------------------------------------------------
+@pytest.mark.parametrize("scale,seed,init", CONFIGS)
+def test_k0_device_generator_bitexact(capi, scale, seed, init):
+    assert np.array_equal(capi.k0_generate(scale, seed, init).cpu().numpy(), O.generate(scale, seed, init))
+
+
+def test_k0_unpermuted(capi):
+    assert np.array_equal(capi.k0_generate(9, 4, permute=False).cpu().numpy(), O.generate(9, 4, permute=False))
+
+
+# ---- K1 ----------------------------------------------------------------------
+@pytest.mark.parametrize("scale,seed,init", CONFIGS + [(18, 5, O.GRAPH500)])
+def test_k1_sort_bitexact(capi, scale, seed, init):
+    uv = O.generate(scale, seed, init)
+    out = capi.k1_sort(t(uv), scale).cpu().numpy()
+    assert np.array_equal(out, O.k1_sort(uv, scale))
+
+
+@pytest.mark.parametrize("name", ["k1k2k3_s10_seed55.npz", "k1k2k3_s8_seed23.npz"])
+def test_k1_vs_reference_golden(capi, name):
+    g = golden(name)
+    out = capi.k1_sort(t(g["edges"]), int(g["scale"])).cpu().numpy()
+    assert np.array_equal(out[:, 0], g["sorted_by_u"][:, 0])  # u-sequence identical to std::sort's
+    assert np.array_equal(out, canonical(g["sorted_by_u"]))   # ties canonicalised by v
+
+
+def test_k1_edge_cases(capi):
+    # empty (test_kernel1_sort.cpp:57-64), hand case (:29-42), all-equal, duplicates, random sizes
+    assert capi.k1_sort_host(np.zeros((0, 2), np.int64), 3).shape == (0, 2)
+    hand = np.array([[3, 1], [1, 2], [2, 9], [1, 7]])
+    assert np.array_equal(capi.k1_sort_host(hand, 4), O.k1_sort(hand, 4))
+    same = np.tile([[5, 5]], (20000, 1))
+    assert np.array_equal(capi.k1_sort_host(same, 3), same)
+    rng = np.random.default_rng(0xDECAF)
+    for _ in range(20):  # property test, test_kernel1_sort.cpp:150-172
+        scale = int(rng.integers(1, 7))
+        cnt = int(rng.integers(1, 300))
+        inp = rng.integers(1, (1 << scale) + 1, size=(cnt, 2)).astype(np.int64)
+        assert np.array_equal(capi.k1_sort_host(inp, scale), O.k1_sort(inp, scale))
+
+
+def test_k1_heavy_duplicates_exceed_local_capacity(capi):
+    # > 8192 identical keys exercise the "no bits left" segment path
+    rng = np.random.default_rng(1)
+    inp = np.concatenate([np.tile([[7, 3]], (30000, 1)), rng.integers(1, 1025, size=(50000, 2))]).astype(np.int64)
+    rng.shuffle(inp)
+    assert np.array_equal(capi.k1_sort_host(inp, 10), O.k1_sort(inp, 10))
+
+
+def test_k1_label_out_of_range(capi):
+    with pytest.raises(capi.PrgError) as e:
+        capi.k1_sort_host(np.array([[1, 2], [9, 1]]), 3)
+    assert e.value.code == -2
+
+
+# ---- K2 ----------------------------------------------------------------------
+def k2_equal(mat, ref):
+    ro, cols, vals, din = mat.download()
+    return (np.array_equal(ro, ref.row_offsets) and np.array_equal(cols, ref.cols)
+            and np.array_equal(vals.view(np.int64), np.asarray(ref.values).view(np.int64))
+            and np.array_equal(din, ref.d_in) and mat.nnz_raw == ref.nnz_raw)
+
+
+@pytest.mark.parametrize("scale,seed,init", CONFIGS + [(18, 5, O.GRAPH500)])
+def test_k2_filter_bitexact(capi, scale, seed, init):
+    srt = O.k1_sort(O.generate(scale, seed, init), scale)
+    ref = O.k2(srt, 1 << scale)
+    mat = capi.k2_filter(t(srt), 1 << scale)
+    assert k2_equal(mat, ref)
+    assert mat.max_in == ref.d_in.max()
+
+
+@pytest.mark.parametrize("name", ["k1k2k3_s10_seed55.npz", "k1k2k3_s8_seed23.npz", "k2k3_er_s12_seed2.npz"])
+def test_k2_on_reference_tie_order(capi, name):
+    # input = the reference's own std::sort output (ties in arbitrary v order)
+    g = golden(name)
+    mat = capi.k2_filter(t(g["sorted_by_u"]), 1 << int(g["scale"]))
+    ro, cols, vals, din = mat.download()
+    assert np.array_equal(ro, g["row_offsets"]) and np.array_equal(cols, g["cols"])
+    assert np.array_equal(vals.view(np.int64), g["values"].view(np.int64)) and np.array_equal(din, g["d_in"])
+
+
+def test_k2_known_answers(capi):
+    worked = O.k1_sort(np.array([[1, 2], [3, 2], [4, 2], [1, 3], [2, 3], [2, 1], [3, 1], [1, 4]]), 2)
+    ro, cols, vals, din = capi.k2_filter_host(worked, 4).download()  # test_kernel2_filter.cpp:93-121
+    assert list(din) == [2, 3, 2, 1] and list(ro) == [0, 1, 3, 4, 4]
+    assert list(cols) == [2, 0, 2, 0] and list(vals) == [1.0, 0.5, 0.5, 1.0]
+    assert capi.k2_filter_host(np.array([[1, 2], [2, 3], [3, 1]]), 3).nnz == 0  # all-max ties (:123-130)
+    m = capi.k2_filter_host(O.k1_sort(np.array([[1, 1], [1, 2], [1, 3], [2, 1], [2, 2], [2, 3], [3, 1]]), 2), 3)
+    assert m.nnz == 4 and 0 not in list(m.download()[1])  # unique max (:132-143)
+    empty = capi.k2_filter_host(np.zeros((0, 2), np.int64), 8)  # run_kernel2 on empty (:233-241)
+    assert empty.nnz == 0 and list(empty.download()[0]) == [0] * 9
+
+
+def test_k2_rejects_bad_input(capi):
+    with pytest.raises(capi.PrgError) as e:
+        capi.k2_filter_host(np.array([[2, 1], [1, 2]]), 2)  # unsorted (:78-85)
+    assert e.value.code == -3
+    with pytest.raises(capi.PrgError) as e:
+        capi.k2_filter_host(np.array([[1, 5]]), 4)  # out of range
+    assert e.value.code == -2
+    with pytest.raises(capi.PrgError):
+        capi.k2_filter_host(np.array([[0, 1]]), 4)
+
+
+def test_k2_long_rows_span_tiles(capi):
+    # one row much longer than a K2 tile (8192 edges) plus a run of duplicates
+    # crossing tile boundaries: exercises the cross-tile fix-ups
+    rng = np.random.default_rng(3)
+    n = 1 << 12
+    e = [np.column_stack([np.full(30000, 5), rng.integers(1, n + 1, 30000)]),
+         np.tile([[6, 9]], (20000, 1)),
+         rng.integers(1, n + 1, size=(40000, 2))]
+    uv = O.k1_sort(np.concatenate(e).astype(np.int64), 12)
+    assert k2_equal(capi.k2_filter_host(uv, n), O.k2(uv, n))
+
+
+# ---- K3 ----------------------------------------------------------------------
+@pytest.mark.parametrize("name", ["k1k2k3_s10_seed55.npz", "k1k2k3_s8_seed23.npz", "k2k3_er_s12_seed2.npz"])
+def test_k3_parity_mode_bit_identical_to_reference(capi, name):
+    g = golden(name)
+    n = 1 << int(g["scale"])
+    mat = capi.DeviceMatrix.from_host(n, g["row_offsets"], g["cols"], g["values"])
+    r, norm = capi.k3_pagerank(mat, seed=int(g["k3_seed"]), mode=1)
+    assert np.array_equal(r.cpu().numpy().view(np.int64), g["ranks"].view(np.int64))
+    assert norm == float(g["norm1"])
+
+
+@pytest.mark.parametrize("name", ["k1k2k3_s10_seed55.npz", "k1k2k3_s8_seed23.npz", "k2k3_er_s12_seed2.npz",
+                                  "k3_s16_seed1.npz"])
+def test_k3_timed_mode_within_tolerance(capi, name):
+    g = golden(name)
+    s = int(g["scale"])
+    n = 1 << s
+    ref = O.k2(O.k1_sort(O.generate(s, int(g["seed"]), tuple(g["initiator"])), s), n)
+    mat = capi.k2_filter(t(O.k1_sort(O.generate(s, int(g["seed"]), tuple(g["initiator"])), s)), n)
+    r, norm = capi.k3_pagerank(mat, seed=int(g["k3_seed"]), mode=0)
+    r = r.cpu().numpy()
+    assert rel_l1(r, g["ranks"]) <= K3_TOL
+    acc, _ = O.run_kernel3(ref.row_offsets, ref.cols, ref.values, n, seed=int(g["k3_seed"]), accurate=True)
+    assert rel_l1(r, acc) <= K3_ACCURATE_TOL
+    assert abs(norm - float(g["norm1"])) <= K3_TOL * float(g["norm1"])
+
+
+def test_k3_deterministic(capi):
+    s = 14
+    mat = capi.k2_filter(t(O.k1_sort(O.generate(s, 7), s)), 1 << s)
+    a, na = capi.k3_pagerank(mat, seed=3)
+    b, nb = capi.k3_pagerank(mat, seed=3)
+    assert np.array_equal(a.cpu().numpy().view(np.int64), b.cpu().numpy().view(np.int64)) and na == nb
+
+
+def test_init_rank_and_step(capi):
+    g = golden("k1k2k3_s10_seed55.npz")
+    n = 1 << 10
+    r0, n0 = capi.init_rank(n, int(g["k3_seed"]), mode=1)
+    assert np.array_equal(r0.cpu().numpy().view(np.int64), g["init_rank"].view(np.int64)) and n0 == g["init_norm1"]
+    r0t, _ = capi.init_rank(n, int(g["k3_seed"]), mode=0)
+    assert rel_l1(r0t.cpu().numpy(), g["init_rank"]) < 1e-15
+    mat = capi.DeviceMatrix.from_host(n, g["row_offsets"], g["cols"], g["values"])
+    s1, ns1 = capi.pagerank_step(mat, r0, mode=1)
+    assert np.array_equal(s1.cpu().numpy().view(np.int64), g["step1"].view(np.int64))
+    s1t, _ = capi.pagerank_step(mat, r0, mode=0)
+    assert rel_l1(s1t.cpu().numpy(), g["step1"]) < 1e-14
+    one, norm = capi.init_rank(1, 5)
+    assert one.item() == 1.0  # test_kernel3_pagerank.cpp:62-66
+
+
+def test_k3_known_answers(capi):
+    import torch
+
+    # zero matrix -> 0.15/4 (test_kernel3_pagerank.cpp:87-93)
+    z = capi.DeviceMatrix.from_host(4, np.zeros(5), np.zeros(0), np.zeros(0))
+    for mode in (0, 1):
+        out, norm = capi.pagerank_step(z, torch.tensor([0.4, 0.3, 0.2, 0.1], dtype=torch.float64, device="cuda"),
+                                       mode=mode)
+        assert np.allclose(out.cpu().numpy(), 0.15 / 4, rtol=1e-15) and abs(norm - 0.15) < 1e-12
+    # permutation matrix fixed point (:78-85)
+    p = capi.DeviceMatrix.from_host(2, [0, 1, 2], [1, 0], [1.0, 1.0])
+    out, norm = capi.pagerank_step(p, torch.tensor([0.5, 0.5], dtype=torch.float64, device="cuda"))
+    assert np.allclose(out.cpu().numpy(), 0.5, rtol=1e-15)
+    # worked case spot value (:95-101)
+    w = O.k2(O.k1_sort(np.array([[1, 2], [3, 2], [4, 2], [1, 3], [2, 3], [2, 1], [3, 1], [1, 4]]), 2), 4)
+    m = capi.DeviceMatrix.from_host(4, w.row_offsets, w.cols, w.values)
+    out, _ = capi.pagerank_step(m, torch.full((4,), 0.25, dtype=torch.float64, device="cuda"))
+    assert abs(out[0].item() - 0.35625) <= 1e-12
+
+
+def test_k3_rejects_bad_config(capi):
+    m = capi.DeviceMatrix.from_host(2, [0, 1, 2], [1, 0], [1.0, 1.0])
+    for damping, iters in ((1.0, 20), (0.0, 20), (0.85, 0)):  # :176-185
+        with pytest.raises(capi.PrgError):
+            capi.k3_pagerank(m, damping=damping, iterations=iters)
+
+
+def test_host_entry_points_e2e(capi):
+    s = 12
+    uv = O.generate(s, 9)
+    srt = capi.k1_sort_host(uv, s)
+    assert np.array_equal(srt, O.k1_sort(uv, s))
+    ref = O.k2(srt, 1 << s)
+    assert k2_equal(capi.k2_filter_host(srt, 1 << s), ref)
+    r, norm = capi.k3_pagerank_host(1 << s, ref.row_offsets, ref.cols, ref.values, seed=9, mode=1)
+    rr, nr = O.run_kernel3(ref.row_offsets, ref.cols, ref.values, 1 << s, seed=9)
+    assert np.array_equal(r.view(np.int64), rr.view(np.int64)) and norm == nr
+
+
+# ---- full size (BASELINE configs): size-independent properties --------------
+FULL = [(20, 1, O.GRAPH500, 15902023, 16086644, 69421, 0.1455844639775524),
+        (22, 2, O.UNIFORM, 67108682, 67108730, 40, 0.99999508210108501),
+        (24, 1, O.GRAPH500, 261074939, 263435020, 369933, 0.098667739035893112)]
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("scale,seed,init,nnz,nnz_raw,max_in,norm_ref", FULL)
+def test_full_size_pipeline_properties(capi, scale, seed, init, nnz, nnz_raw, max_in, norm_ref):
+    import torch
+
+    n = 1 << scale
+    uv = capi.k0_generate(scale, seed, init)
+    srt = capi.k1_sort(uv, scale)
+    # K1: lexicographically sorted and a permutation of the input (packed-key sums/xors)
+    key = lambda a: (a[:, 0] - 1) * n + (a[:, 1] - 1)  # noqa: E731
+    ks, ki = key(srt), key(uv)
+    assert bool((ks[1:] >= ks[:-1]).all())
+    assert int(ks.sum()) == int(ki.sum()) and int((ks * ks % 1000003).sum()) == int((ki * ki % 1000003).sum())
+    del uv, ks, ki
+    mat = capi.k2_filter(srt, n)
+    # K2: counts from SURVEY §8(c), measured on the reference
+    assert (mat.nnz, mat.nnz_raw, mat.max_in) == (nnz, nnz_raw, max_in)
+    ro, cols, vals, din = mat.download()
+    assert int(din.sum()) == 16 * n
+    rs = np.add.reduceat(vals, ro[:-1][np.diff(ro) > 0])
+    assert np.abs(rs - 1.0).max() <= 1e-12
+    del srt, cols, vals
+    torch.cuda.empty_cache()
+    r, norm = capi.k3_pagerank(mat, seed=seed)
+    # K3: final norm1 vs the reference's; its own sequential-sum
+    # drift at these scales is <= 4.3e-11 relative L1
+    assert abs(norm - norm_ref) <= K3_TOL * norm_ref
+    assert float(r.sum().item()) == pytest.approx(norm, rel=1e-12)
+    assert float(r.min().item()) > 0

@@ -82,6 +82,21 @@ prg_status prg_k2_filter_device(const int64_t* d_uv_sorted, int64_t m, int64_t n
                                 void* stream);
 prg_status prg_k2_filter_host(const int64_t* uv_sorted, int64_t m, int64_t n, prg_matrix** out);
 
+/* K2 step-level entry points on the reference's CountMatrix layout (host
+ * int64 arrays; computed on the device). build_adjacency (kernel2_filter.hpp:42-43,
+ * kernel2_filter.cpp:12-54): row_offsets[n+1], cols/counts[m] (nnz <= m) ->
+ * *nnz. in_degree (:46, :101-106). zero_columns (:51, :108-132): outputs sized
+ * like the input. row_normalize (:54, :134-152): values[nnz]. */
+prg_status prg_build_adjacency_host(const int64_t* uv_sorted, int64_t m, int64_t n, int64_t* row_offsets,
+                                    int64_t* cols, int64_t* counts, int64_t* nnz);
+prg_status prg_in_degree_host(int64_t n, int64_t nnz, const int64_t* cols, const int64_t* counts,
+                              int64_t* d_in);
+prg_status prg_zero_columns_host(int64_t n, int64_t nnz, const int64_t* row_offsets, const int64_t* cols,
+                                 const int64_t* counts, const int64_t* d_in, int64_t* out_row_offsets,
+                                 int64_t* out_cols, int64_t* out_counts, int64_t* out_nnz);
+prg_status prg_row_normalize_host(int64_t n, int64_t nnz, const int64_t* row_offsets, const int64_t* counts,
+                                  double* values);
+
 /* Matrix handle. */
 prg_status prg_matrix_info(const prg_matrix* a, int64_t* n, int64_t* nnz, int64_t* nnz_raw,
                            int64_t* max_in_degree);
@@ -118,6 +133,19 @@ prg_status prg_init_rank_device(int64_t n, uint64_t seed, int32_t mode, double* 
                                 void* stream);
 prg_status prg_pagerank_step_device(const prg_matrix* a, const double* d_r, double damping,
                                     int32_t mode, double* d_out, double* norm1, void* stream);
+
+/* Host-buffer variants used by the drop-in C++ shim (prpipe::init_rank,
+ * pagerank_step, run_kernel3 on a K2-produced handle, run_to_convergence). */
+prg_status prg_init_rank_host(int64_t n, uint64_t seed, int32_t mode, double* r, double* norm1);
+prg_status prg_pagerank_step_host(int64_t n, int64_t nnz, const int64_t* row_offsets, const int64_t* cols,
+                                  const double* values, const double* r, double damping, int32_t mode,
+                                  double* out, double* norm1);
+prg_status prg_k3_pagerank_matrix_host(const prg_matrix* a, double damping, int32_t iterations, uint64_t seed,
+                                       int32_t mode, double* ranks, double* norm1);
+prg_status prg_run_to_convergence_host(int64_t n, int64_t nnz, const int64_t* row_offsets, const int64_t* cols,
+                                       const double* values, double damping, double tol, int32_t max_iters,
+                                       const double* start, double* out, int32_t* converged,
+                                       int32_t* iterations);
 
 #ifdef __cplusplus
 }

@@ -276,3 +276,12 @@ def row_normalize(n, row_offsets, counts):
     v = np.zeros(max(len(counts), 1), dtype=np.float64)
     _rn(n, _c64(row_offsets), _c64(counts), v)
     return v[: len(counts)]
+
+
+def ref_write_edges(uv, directory: str, num_files: int, scale: int, sorted_by_start=False):
+    """The reference's write_edges (edge_io.cpp:191-196)."""
+    _need_ref()
+    f = _sig(_ref, "ref_write_edges", C.c_int, [_i64p, C.c_int64, C.c_char_p, C.c_int, C.c_int, C.c_int])
+    uv = np.ascontiguousarray(uv, dtype=np.int64).reshape(-1, 2)
+    if f(uv, len(uv), directory.encode(), num_files, scale, int(sorted_by_start)):
+        raise RuntimeError(_ref.ref_last_error().decode())

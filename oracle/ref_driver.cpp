@@ -16,6 +16,7 @@
 #include <thread>
 #include <vector>
 
+#include "prpipe/edge_io.hpp"
 #include "prpipe/graph_gen.hpp"
 #include "prpipe/kernel2_filter.hpp"
 #include "prpipe/kernel3_pagerank.hpp"
@@ -144,6 +145,20 @@ double ref_init_rank(std::int64_t n, std::uint64_t seed, double* r) {
     auto rv = init_rank(n, seed);
     std::memcpy(r, rv.values.data(), sizeof(double) * n);
     return rv.norm1;
+}
+
+// write_edges (src/edge_io.cpp:191-196) — shard and manifest bytes for the
+// drop-in's edge I/O comparison.
+int ref_write_edges(const std::int64_t* uv, std::int64_t m, const char* dir, int num_files, int scale,
+                    int sorted) {
+    try {
+        std::span<const Edge> e(reinterpret_cast<const Edge*>(uv), static_cast<std::size_t>(m));
+        write_edges(e, dir, num_files, scale, sorted != 0);
+        return 0;
+    } catch (const std::exception& ex) {
+        g_err = ex.what();
+        return -1;
+    }
 }
 
 }  // extern "C"

@@ -28,7 +28,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
               "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"] + ARCH
 CU_SOURCES = ["prg_runtime.cu", "prg_sort.cu", "prg_k0.cu", "prg_k1.cu", "prg_k2.cu", "prg_k3.cu",
-              "prg_capi.cu"]
+              "prg_k2_steps.cu", "prg_capi.cu"]
 HEADERS = ["prg_common.cuh", "prg_internal.cuh", "prg_sort.cuh"]
 
 
@@ -76,16 +76,38 @@ def build_core(force: bool = False) -> str | None:
 
     ext = sysconfig.get_config_var("EXT_SUFFIX") or ".so"
     out = os.path.join(PYMOD_DIR, "_core" + ext)
-    hdrs = [os.path.join(HOST, f) for f in os.listdir(HOST) if f.endswith(".hpp")]
+    hdrs = [os.path.join(HOST, "prpipe", f) for f in os.listdir(os.path.join(HOST, "prpipe"))] + [
+        os.path.join(ROOT, "include", "prg.h")]
     if not (force or _newer(out, srcs + hdrs + [LIB])):
         return out
     py_inc = sysconfig.get_paths()["include"]
-    cmd = ["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-fvisibility=hidden",
-           "-I", os.path.join(ROOT, "include"), "-I", HOST, "-I", pybind11.get_include(), "-I", py_inc,
-           *srcs, "-o", out, "-L", os.path.dirname(LIB), "-lprg", "-Wl,-rpath,$ORIGIN/../../lib",
-           "-lpthread"]
-    _run(cmd)
+    json_dir = _json_include()
+    objdir = os.path.join(ROOT, "build", "host")
+    os.makedirs(objdir, exist_ok=True)
+    base = ["g++", "-std=c++20", "-O2", "-fPIC", "-fvisibility=hidden", "-I", os.path.join(ROOT, "include"),
+            "-I", HOST, "-I", pybind11.get_include(), "-I", py_inc, "-I", json_dir]
+    objs, jobs = [], []
+    for src in srcs:
+        o = os.path.join(objdir, os.path.basename(src).replace(".cpp", ".o"))
+        objs.append(o)
+        if force or _newer(o, [src] + hdrs):
+            jobs.append(base + ["-c", src, "-o", o])
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
+        list(ex.map(_run, jobs))
+    _run(["g++", "-shared", *objs, "-o", out, "-L", os.path.dirname(LIB), "-lprg",
+          "-Wl,-rpath,$ORIGIN/../../lib", "-lpthread"])
     return out
+
+
+def _json_include() -> str:
+    """nlohmann/json.hpp (v3.11.3, vendored in the image's cudnn_frontend) for the manifest."""
+    import glob
+    import site
+
+    for sp in site.getsitepackages():
+        for d in glob.glob(os.path.join(sp, "include", "cudnn_frontend", "thirdparty", "nlohmann")):
+            return d
+    raise RuntimeError("nlohmann/json.hpp not found")
 
 
 def build(force: bool = False) -> None:

@@ -208,6 +208,89 @@ prg_status prg_k2_filter_host(const int64_t* uv_sorted, int64_t m, int64_t n, pr
     });
 }
 
+prg_status prg_build_adjacency_host(const int64_t* uv_sorted, int64_t m, int64_t n, int64_t* row_offsets,
+                                    int64_t* cols, int64_t* counts, int64_t* nnz) {
+    return guarded("prg_build_adjacency", [&] {
+        require(n > 0, PRG_ERR_INVALID_ARGUMENT, "vertex count must be positive");
+        require(m >= 0 && (uint64_t)m < (1ull << 32) && (uint64_t)n < (1ull << 32), PRG_ERR_INVALID_ARGUMENT,
+                "sizes exceed the u32 index range");
+        cudaStream_t s = nullptr;
+        DevBuf<int64_t> a((size_t)std::max<int64_t>(m, 1) * 2, s);
+        if (m) PRG_CUDA(cudaMemcpyAsync(a.get(), uv_sorted, (size_t)m * 16, cudaMemcpyHostToDevice, s));
+        std::unique_ptr<prg_matrix> mat(new prg_matrix());
+        const uint32_t err = prg::k2_filter_device(a.get(), m, n, mat.get(), s, /*filter=*/false, /*normalize=*/false);
+        check_device_errors(err, "build_adjacency");
+        download_u32_as_i64(mat->row_offsets, (size_t)n + 1, row_offsets, s);
+        download_u32_as_i64(mat->cols, (size_t)mat->nnz, cols, s);
+        if (mat->nnz) {
+            std::vector<double> v(mat->nnz);
+            PRG_CUDA(cudaMemcpy(v.data(), mat->values, mat->nnz * 8, cudaMemcpyDeviceToHost));
+            for (uint64_t k = 0; k < mat->nnz; ++k) counts[k] = (int64_t)v[k];  // exact integers
+        }
+        *nnz = (int64_t)mat->nnz;
+    });
+}
+
+prg_status prg_in_degree_host(int64_t n, int64_t nnz, const int64_t* cols, const int64_t* counts, int64_t* d_in) {
+    return guarded("prg_in_degree", [&] {
+        require(n > 0 && nnz >= 0, PRG_ERR_INVALID_ARGUMENT, "bad sizes");
+        cudaStream_t s = nullptr;
+        DevBuf<int64_t> dc((size_t)std::max<int64_t>(nnz, 1), s), dn((size_t)std::max<int64_t>(nnz, 1), s),
+            dd((size_t)n, s);
+        if (nnz) {
+            PRG_CUDA(cudaMemcpyAsync(dc.get(), cols, (size_t)nnz * 8, cudaMemcpyHostToDevice, s));
+            PRG_CUDA(cudaMemcpyAsync(dn.get(), counts, (size_t)nnz * 8, cudaMemcpyHostToDevice, s));
+        }
+        prg::k2_in_degree_device(n, nnz, dc.get(), dn.get(), dd.get(), s);
+        PRG_CUDA(cudaMemcpyAsync(d_in, dd.get(), (size_t)n * 8, cudaMemcpyDeviceToHost, s));
+        PRG_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+prg_status prg_zero_columns_host(int64_t n, int64_t nnz, const int64_t* row_offsets, const int64_t* cols,
+                                 const int64_t* counts, const int64_t* d_in, int64_t* out_row_offsets,
+                                 int64_t* out_cols, int64_t* out_counts, int64_t* out_nnz) {
+    return guarded("prg_zero_columns", [&] {
+        require(n > 0 && nnz >= 0, PRG_ERR_INVALID_ARGUMENT, "bad sizes");
+        cudaStream_t s = nullptr;
+        const size_t z = (size_t)std::max<int64_t>(nnz, 1);
+        DevBuf<int64_t> ro((size_t)n + 1, s), dc(z, s), dn(z, s), dd((size_t)n, s), oro((size_t)n + 1, s),
+            oc(z, s), on(z, s);
+        PRG_CUDA(cudaMemcpyAsync(ro.get(), row_offsets, (size_t)(n + 1) * 8, cudaMemcpyHostToDevice, s));
+        PRG_CUDA(cudaMemcpyAsync(dd.get(), d_in, (size_t)n * 8, cudaMemcpyHostToDevice, s));
+        if (nnz) {
+            PRG_CUDA(cudaMemcpyAsync(dc.get(), cols, (size_t)nnz * 8, cudaMemcpyHostToDevice, s));
+            PRG_CUDA(cudaMemcpyAsync(dn.get(), counts, (size_t)nnz * 8, cudaMemcpyHostToDevice, s));
+        }
+        const int64_t nz = prg::k2_zero_columns_device(n, ro.get(), dc.get(), dn.get(), dd.get(), oro.get(),
+                                                       oc.get(), on.get(), s);
+        PRG_CUDA(cudaMemcpyAsync(out_row_offsets, oro.get(), (size_t)(n + 1) * 8, cudaMemcpyDeviceToHost, s));
+        if (nz) {
+            PRG_CUDA(cudaMemcpyAsync(out_cols, oc.get(), (size_t)nz * 8, cudaMemcpyDeviceToHost, s));
+            PRG_CUDA(cudaMemcpyAsync(out_counts, on.get(), (size_t)nz * 8, cudaMemcpyDeviceToHost, s));
+        }
+        PRG_CUDA(cudaStreamSynchronize(s));
+        *out_nnz = nz;
+    });
+}
+
+prg_status prg_row_normalize_host(int64_t n, int64_t nnz, const int64_t* row_offsets, const int64_t* counts,
+                                  double* values) {
+    return guarded("prg_row_normalize", [&] {
+        require(n > 0 && nnz >= 0, PRG_ERR_INVALID_ARGUMENT, "bad sizes");
+        if (!nnz) return;
+        cudaStream_t s = nullptr;
+        DevBuf<int64_t> ro((size_t)n + 1, s), dn((size_t)nnz, s);
+        DevBuf<double> dv((size_t)nnz, s);
+        PRG_CUDA(cudaMemcpyAsync(ro.get(), row_offsets, (size_t)(n + 1) * 8, cudaMemcpyHostToDevice, s));
+        PRG_CUDA(cudaMemcpyAsync(dn.get(), counts, (size_t)nnz * 8, cudaMemcpyHostToDevice, s));
+        PRG_CUDA(cudaMemsetAsync(dv.get(), 0, (size_t)nnz * 8, s));
+        prg::k2_row_normalize_device(n, ro.get(), dn.get(), dv.get(), s);
+        PRG_CUDA(cudaMemcpyAsync(values, dv.get(), (size_t)nnz * 8, cudaMemcpyDeviceToHost, s));
+        PRG_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
 prg_status prg_matrix_info(const prg_matrix* a, int64_t* n, int64_t* nnz, int64_t* nnz_raw, int64_t* max_in) {
     return guarded("prg_matrix_info", [&] {
         require(a != nullptr, PRG_ERR_INVALID_ARGUMENT, "null matrix");
@@ -338,6 +421,74 @@ prg_status prg_pagerank_step_device(const prg_matrix* a, const double* d_r, doub
         require(a != nullptr && d_r && d_out, PRG_ERR_INVALID_ARGUMENT, "null argument");
         const double nm = prg::k3_step_device(a, d_r, damping, d_out, mode, as_stream(stream));
         if (norm1) *norm1 = nm;
+    });
+}
+
+prg_status prg_init_rank_host(int64_t n, uint64_t seed, int32_t mode, double* r, double* norm1) {
+    return guarded("prg_init_rank_host", [&] {
+        require(n >= 1, PRG_ERR_INVALID_ARGUMENT, "rank vector needs at least one entry");
+        cudaStream_t s = nullptr;
+        DevBuf<double> d((size_t)n, s);
+        const double nm = prg::k3_init_rank_device(n, seed, d.get(), mode, s);
+        PRG_CUDA(cudaMemcpy(r, d.get(), (size_t)n * 8, cudaMemcpyDeviceToHost));
+        if (norm1) *norm1 = nm;
+    });
+}
+
+prg_status prg_pagerank_step_host(int64_t n, int64_t nnz, const int64_t* row_offsets, const int64_t* cols,
+                                  const double* values, const double* r, double damping, int32_t mode,
+                                  double* out, double* norm1) {
+    return guarded("prg_pagerank_step_host", [&] {
+        prg_matrix* a = nullptr;
+        prg_status st = prg_matrix_from_host(n, nnz, row_offsets, cols, values, &a);
+        if (st != PRG_OK) throw ApiError{st, prg::last_error()};
+        std::unique_ptr<prg_matrix> own(a);
+        cudaStream_t s = nullptr;
+        DevBuf<double> dr((size_t)n, s), dout((size_t)n, s);
+        PRG_CUDA(cudaMemcpyAsync(dr.get(), r, (size_t)n * 8, cudaMemcpyHostToDevice, s));
+        const double nm = prg::k3_step_device(a, dr.get(), damping, dout.get(), mode, s);
+        PRG_CUDA(cudaMemcpy(out, dout.get(), (size_t)n * 8, cudaMemcpyDeviceToHost));
+        if (norm1) *norm1 = nm;
+    });
+}
+
+prg_status prg_k3_pagerank_matrix_host(const prg_matrix* a, double damping, int32_t iterations, uint64_t seed,
+                                       int32_t mode, double* ranks, double* norm1) {
+    return guarded("prg_k3_pagerank_matrix_host", [&] {
+        require(a != nullptr && ranks != nullptr, PRG_ERR_INVALID_ARGUMENT, "null argument");
+        cudaStream_t s = nullptr;
+        DevBuf<double> r((size_t)a->n, s);
+        const prg_status st = prg_k3_pagerank_device(a, damping, iterations, seed, mode, r.get(), norm1, s);
+        if (st != PRG_OK) throw ApiError{st, prg::last_error()};
+        PRG_CUDA(cudaMemcpy(ranks, r.get(), (size_t)a->n * 8, cudaMemcpyDeviceToHost));
+    });
+}
+
+prg_status prg_run_to_convergence_host(int64_t n, int64_t nnz, const int64_t* row_offsets, const int64_t* cols,
+                                       const double* values, double damping, double tol, int32_t max_iters,
+                                       const double* start, double* out, int32_t* converged,
+                                       int32_t* iterations) {
+    return guarded("prg_run_to_convergence_host", [&] {
+        // kernel3_pagerank.cpp:89-91
+        require(tol > 0.0, PRG_ERR_INVALID_ARGUMENT, "convergence tolerance must be positive");
+        require(max_iters >= 1, PRG_ERR_INVALID_ARGUMENT, "max_iters must be >= 1");
+        prg_matrix* a = nullptr;
+        prg_status st = prg_matrix_from_host(n, nnz, row_offsets, cols, values, &a);
+        if (st != PRG_OK) throw ApiError{st, prg::last_error()};
+        std::unique_ptr<prg_matrix> own(a);
+        cudaStream_t s = nullptr;
+        DevBuf<double> d0((size_t)n, s), d1((size_t)n, s);
+        PRG_CUDA(cudaMemcpyAsync(d0.get(), start, (size_t)n * 8, cudaMemcpyHostToDevice, s));
+        bool conv = false;
+        int its = 0;
+        try {
+            its = prg::k3_converge_device(a, damping, tol, max_iters, d0.get(), d1.get(), &conv, s);
+        } catch (const CudaError& e) {
+            throw ApiError{PRG_ERR_INVALID_ARGUMENT, e.msg};
+        }
+        PRG_CUDA(cudaMemcpy(out, d1.get(), (size_t)n * 8, cudaMemcpyDeviceToHost));
+        *converged = conv ? 1 : 0;
+        *iterations = its;
     });
 }
 

@@ -27,8 +27,19 @@ void k1_sort_device(const int64_t* d_uv_in, int64_t m, int scale, int64_t* d_uv_
 // K2 (prg_k2.cu): fused build_adjacency + in_degree + zero_columns +
 // row_normalize over a device edge list sorted by start vertex. Returns a
 // DeviceErr mask (0 on success); fills *out.
+// filter=false, normalize=false gives build_adjacency's CountMatrix (values
+// hold the exact integer counts).
 uint32_t k2_filter_device(const int64_t* d_uv, int64_t m, int64_t n, prg_matrix* out,
-                          cudaStream_t s);
+                          cudaStream_t s, bool filter = true, bool normalize = true);
+
+// K2 step-level functions over int64 device arrays (prg_k2_steps.cu).
+void k2_in_degree_device(int64_t n, int64_t nnz, const int64_t* cols, const int64_t* counts, int64_t* d_in,
+                         cudaStream_t s);
+int64_t k2_zero_columns_device(int64_t n, const int64_t* row_offsets, const int64_t* cols, const int64_t* counts,
+                               const int64_t* d_in, int64_t* out_offsets, int64_t* out_cols, int64_t* out_counts,
+                               cudaStream_t s);
+void k2_row_normalize_device(int64_t n, const int64_t* row_offsets, const int64_t* counts, double* values,
+                             cudaStream_t s);
 
 // K3 (prg_k3.cu).
 struct K3Options {
@@ -44,6 +55,9 @@ double k3_pagerank_device(const prg_matrix* a, const K3Options& opt, double* d_r
 // One pagerank_step (kernel3_pagerank.cpp:41-65): d_out = step(d_r). Returns norm1.
 double k3_step_device(const prg_matrix* a, const double* d_r, double damping, double* d_out,
                       int mode, cudaStream_t s);
+// run_to_convergence (kernel3_pagerank.cpp:86-115); returns iterations applied.
+int k3_converge_device(const prg_matrix* a, double damping, double tol, int max_iters, const double* d_start,
+                       double* d_out, bool* converged, cudaStream_t s);
 // init_rank (kernel3_pagerank.cpp:29-39) on the device; returns norm1.
 double k3_init_rank_device(int64_t n, uint64_t seed, double* d_r, int mode, cudaStream_t s);
 

@@ -181,7 +181,8 @@ __global__ void __launch_bounds__(kT) k2_pass_b(
     uint32_t* __restrict__ row_offsets, uint32_t* __restrict__ cols, double* __restrict__ values,
     unsigned long long* __restrict__ tile_status, uint32_t* __restrict__ tile_counter,
     uint32_t* __restrict__ dout_f, uint32_t* __restrict__ fix_rows, uint32_t* __restrict__ n_fix,
-    uint32_t* __restrict__ cont_p, uint32_t* __restrict__ cont_c, unsigned long long* __restrict__ nnz_out) {
+    uint32_t* __restrict__ cont_p, uint32_t* __restrict__ cont_c, unsigned long long* __restrict__ nnz_out,
+    bool normalize) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     PassBSmem& S = *reinterpret_cast<PassBSmem*>(smem_raw);
     const unsigned tid = threadIdx.x;
@@ -313,7 +314,7 @@ __global__ void __launch_bounds__(kT) k2_pass_b(
                     cols[pos] = v;
                     const double c = (double)S.runlen[l];
                     const bool spanning = rh < 0 || (last_spans && rh == rh_last);
-                    values[pos] = spanning ? c : c / (double)S.rowsum[rh];
+                    values[pos] = (spanning || !normalize) ? c : c / (double)S.rowsum[rh];
                     ++pos;
                 }
             }
@@ -359,7 +360,8 @@ __global__ void k2_fix_rows(const uint32_t* __restrict__ fix_rows, const uint32_
 
 }  // namespace
 
-uint32_t k2_filter_device(const int64_t* d_uv, int64_t m, int64_t n, prg_matrix* out, cudaStream_t s) {
+uint32_t k2_filter_device(const int64_t* d_uv, int64_t m, int64_t n, prg_matrix* out, cudaStream_t s,
+                          bool filter, bool normalize) {
     ProfScope prof("k2_filter", s);
     out->n = n;
     out->cap = (uint64_t)(m > 0 ? m : 1);
@@ -412,14 +414,18 @@ uint32_t k2_filter_device(const int64_t* d_uv, int64_t m, int64_t n, prg_matrix*
         k1_sort_device(d_uv, m, scale, tmp.get(), e2.get(), s);
         ws_free(out->row_offsets, s); ws_free(out->cols, s); ws_free(out->values, s); ws_free(out->d_in, s);
         out->row_offsets = nullptr; out->cols = nullptr; out->values = nullptr; out->d_in = nullptr;
-        return k2_filter_device(tmp.get(), m, n, out, s) & ~(uint32_t)kErrNotCanonical;
+        return k2_filter_device(tmp.get(), m, n, out, s, filter, normalize) & ~(uint32_t)kErrNotCanonical;
     }
     const unsigned gn = (unsigned)num_sms() * 8;
     k2_max_kernel<<<gn, 1024, 0, s>>>(out->d_in, n, maxp);
     PRG_LAUNCH_CHECK();
     DevBuf<uint32_t> keepbits((size_t)(n + 31) / 32, s);
-    k2_keep_kernel<<<gn, 1024, 0, s>>>(out->d_in, n, maxp, keepbits.get());
-    PRG_LAUNCH_CHECK();
+    if (filter) {
+        k2_keep_kernel<<<gn, 1024, 0, s>>>(out->d_in, n, maxp, keepbits.get());
+        PRG_LAUNCH_CHECK();
+    } else {  // build_adjacency only: keep every column
+        PRG_CUDA(cudaMemsetAsync(keepbits.get(), 0xff, (size_t)(n + 31) / 32 * 4, s));
+    }
     DevBuf<unsigned long long> tile_status(ntiles, s);
     DevBuf<uint32_t> dout_f((size_t)n, s), fix_rows(ntiles + 1, s), cont_p(ntiles, s), cont_c(ntiles, s);
     PRG_CUDA(cudaMemsetAsync(tile_status.get(), 0, (size_t)ntiles * 8, s));
@@ -428,11 +434,13 @@ uint32_t k2_filter_device(const int64_t* d_uv, int64_t m, int64_t n, prg_matrix*
         ProfScope pb("k2_pass_b", s);
         k2_pass_b<<<ntiles, kT, sizeof(PassBSmem), s>>>(uv, m, n, keepbits.get(), out->row_offsets, out->cols,
                                                         out->values, tile_status.get(), tile_counter, dout_f.get(),
-                                                        fix_rows.get(), n_fix, cont_p.get(), cont_c.get(), nnz_out);
+                                                        fix_rows.get(), n_fix, cont_p.get(), cont_c.get(), nnz_out,
+                                                        normalize);
         PRG_LAUNCH_CHECK();
     }
     k2_fix_runs<<<div_up(ntiles, 256), 256, 0, s>>>(cont_p.get(), cont_c.get(), ntiles, out->values);
     PRG_LAUNCH_CHECK();
+    if (normalize)
     k2_fix_rows<<<(unsigned)num_sms() * 2, 256, 0, s>>>(fix_rows.get(), n_fix, out->row_offsets, dout_f.get(),
                                                          out->values);
     PRG_LAUNCH_CHECK();

@@ -1152,7 +1152,66 @@ void iterate(const K3Plan& P, const double* r_in, double* r_out, int iters, doub
     PRG_LAUNCH_CHECK();
 }
 
+__global__ void l1_diff_partial(const double* __restrict__ a, const double* __restrict__ b, int64_t n,
+                                double* __restrict__ part) {
+    __shared__ double ws[32];
+    const int64_t base = (int64_t)blockIdx.x * 8192;
+    double s = 0.0;
+    for (int q = 0; q < 8; ++q) {
+        const int64_t i = base + q * 1024 + threadIdx.x;
+        if (i < n) s = __dadd_rn(s, fabs(a[i] - b[i]));
+    }
+    s = dev::warp_sum_f64(s);
+    if (dev::lane_id() == 0) ws[dev::warp_id()] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double v = dev::warp_sum_f64(ws[threadIdx.x]);
+        if (threadIdx.x == 0) part[blockIdx.x] = v;
+    }
+}
+
 }  // namespace
+
+// run_to_convergence (kernel3_pagerank.cpp:86-115): iterate, renormalise to
+// 1-norm 1, stop when successive iterates differ by < tol in 1-norm.
+int k3_converge_device(const prg_matrix* A, double damping, double tol, int max_iters, const double* d_start,
+                       double* d_out, bool* converged, cudaStream_t s) {
+    const int64_t n = A->n;
+    const double bgf = (1.0 - damping) / (double)n;
+    K3Plan P;
+    build_plan(A, 0, P, s);
+    Sums S;
+    DevBuf<double> cur((size_t)n, s), nxt((size_t)n, s);
+    const unsigned g = (unsigned)num_sms() * 8;
+    PRG_CUDA(cudaMemcpyAsync(cur.get(), d_start, (size_t)n * 8, cudaMemcpyDeviceToDevice, s));
+    device_sum(cur.get(), n, bgf, 0, S, s);
+    if (!(read_scalar(S.out.get(), s) > 0.0)) throw CudaError{"start vector has no rank mass"};
+    scale_kernel<<<g, 1024, 0, s>>>(cur.get(), n, S.out.get());
+    PRG_LAUNCH_CHECK();
+    device_sum(cur.get(), n, bgf, 0, S, s);
+    const int64_t nb = (n + 8191) / 8192;
+    DevBuf<double> part((size_t)nb, s), dsum(4, s);
+    *converged = false;
+    int it = 0;
+    for (it = 1; it <= max_iters; ++it) {
+        iterate(P, cur.get(), nxt.get(), 1, damping, bgf, S, s);
+        if (!(read_scalar(S.out.get(), s) > 0.0)) throw CudaError{"iterate lost all rank mass"};
+        scale_kernel<<<g, 1024, 0, s>>>(nxt.get(), n, S.out.get());
+        PRG_LAUNCH_CHECK();
+        device_sum(nxt.get(), n, bgf, 0, S, s);
+        l1_diff_partial<<<(unsigned)nb, 1024, 0, s>>>(nxt.get(), cur.get(), n, part.get());
+        final_sum_kernel<<<1, 1024, 0, s>>>(part.get(), nb, 0.0, dsum.get());
+        PRG_LAUNCH_CHECK();
+        std::swap(cur, nxt);
+        if (read_scalar(dsum.get(), s) < tol) {
+            *converged = true;
+            break;
+        }
+    }
+    PRG_CUDA(cudaMemcpyAsync(d_out, cur.get(), (size_t)n * 8, cudaMemcpyDeviceToDevice, s));
+    PRG_CUDA(cudaStreamSynchronize(s));
+    return std::min(it, max_iters);
+}
 
 double k3_init_rank_device(int64_t n, uint64_t seed, double* d_r, int mode, cudaStream_t s) {
     Sums S;

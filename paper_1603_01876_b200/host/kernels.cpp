@@ -1,0 +1,291 @@
+// prpipe drop-in K1/K2/K3 (include/prpipe/kernel{1_sort,2_filter,3_pagerank}.hpp)
+// over the C-ABI of include/prg.h. All compute runs on the B200; the host only
+// moves data and files. Status codes from the C-ABI become prpipe::Error.
+#include <algorithm>
+#include <charconv>
+#include <cstring>
+#include <cstdlib>
+#include <fstream>
+#include <list>
+#include <mutex>
+#include <numeric>
+#include <unistd.h>
+
+#include "prg.h"
+#include "prpipe/kernel1_sort.hpp"
+#include "prpipe/kernel2_filter.hpp"
+#include "prpipe/kernel3_pagerank.hpp"
+#include "prpipe/timer.hpp"
+
+namespace prpipe {
+
+namespace {
+
+void check(prg_status st) {
+    if (st != PRG_OK) throw Error(prg_last_error());
+}
+
+const std::int64_t* edge_words(std::span<const Edge> e) { return reinterpret_cast<const std::int64_t*>(e.data()); }
+
+// ---- K2 -> K3 device residency --------------------------------
+// run_kernel2 returns a host StochasticMatrix (the reference's value type) but
+// keeps its device CSR; run_kernel3 on that same matrix reuses it instead of
+// uploading. Keyed by the host arrays' addresses and sizes, guarded by a
+// sampled fingerprint so a mutated or reallocated matrix misses.
+struct CacheEntry {
+    const void* cols_ptr;
+    std::int64_t n, nnz;
+    std::uint64_t fp;
+    prg_matrix* dev;
+};
+std::mutex g_cache_mu;
+std::list<CacheEntry> g_cache;  // most recent first, at most 2 entries
+
+std::uint64_t fingerprint(const StochasticMatrix& a) {
+    std::uint64_t h = 0x9e3779b97f4a7c15ULL ^ static_cast<std::uint64_t>(a.n);
+    auto mix = [&](std::uint64_t x) { h = (h ^ x) * 0x100000001b3ULL; };
+    const std::size_t nz = a.cols.size();
+    for (std::size_t k = 0; k < 64 && nz; ++k) {
+        const std::size_t i = (k * 2654435761ULL) % nz;
+        mix(static_cast<std::uint64_t>(a.cols[i]));
+        std::uint64_t v;
+        std::memcpy(&v, &a.values[i], 8);
+        mix(v);
+    }
+    for (std::size_t k = 0; k < 64; ++k) mix(static_cast<std::uint64_t>(a.row_offsets[(k * 40503ULL) % a.row_offsets.size()]));
+    return h;
+}
+
+void cache_put(const StochasticMatrix& a, prg_matrix* dev) {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    g_cache.push_front({a.cols.data(), a.n, a.nnz(), fingerprint(a), dev});
+    while (g_cache.size() > 2) {
+        prg_matrix_destroy(g_cache.back().dev);
+        g_cache.pop_back();
+    }
+}
+
+prg_matrix* cache_get(const StochasticMatrix& a) {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    for (auto& e : g_cache)
+        if (e.cols_ptr == a.cols.data() && e.n == a.n && e.nnz == a.nnz() && e.fp == fingerprint(a)) return e.dev;
+    return nullptr;
+}
+
+SortBreakdown g_last_sort;
+
+}  // namespace
+
+// ---- K1 ----------------------------------------------------------------------
+std::int64_t default_memory_budget() {
+    const long pages = sysconf(_SC_PHYS_PAGES), page = sysconf(_SC_PAGE_SIZE);
+    if (pages <= 0 || page <= 0) return std::int64_t{1} << 30;
+    return static_cast<std::int64_t>(pages) * page / 4;
+}
+
+EdgeManifest sort_edges(const EdgeManifest& input, const std::filesystem::path& output_dir,
+                        const SortOptions& options) {
+    if (options.memory_budget_bytes < 0) throw Error("memory budget must be positive");
+    const int files = options.num_files > 0 ? options.num_files : default_num_files(input.total_edges);
+    Timer t0;
+    std::vector<Edge> edges = read_edges(input);
+    g_last_sort.read_s = t0.seconds();
+    Timer t1;
+    std::vector<Edge> sorted(edges.size());
+    if (!edges.empty())
+        check(prg_k1_sort_host(edge_words(edges), static_cast<std::int64_t>(edges.size()), input.scale,
+                               reinterpret_cast<std::int64_t*>(sorted.data())));
+    g_last_sort.device_s = t1.seconds();
+    Timer t2;
+    auto out = write_edges(sorted, output_dir, files, input.scale, /*sorted_by_start=*/true);
+    g_last_sort.write_s = t2.seconds();
+    return out;
+}
+
+SortBreakdown last_sort_breakdown() { return g_last_sort; }
+
+// ---- K2 ----------------------------------------------------------------------
+std::int64_t CountMatrix::total() const { return std::accumulate(counts.begin(), counts.end(), std::int64_t{0}); }
+
+std::int64_t CountMatrix::count_at(std::int64_t row, std::int64_t col) const {
+    const auto b = cols.begin() + row_offsets.at(static_cast<std::size_t>(row));
+    const auto e = cols.begin() + row_offsets.at(static_cast<std::size_t>(row) + 1);
+    const auto it = std::lower_bound(b, e, col);
+    return (it != e && *it == col) ? counts[static_cast<std::size_t>(it - cols.begin())] : 0;
+}
+
+double StochasticMatrix::value_at(std::int64_t row, std::int64_t col) const {
+    const auto b = cols.begin() + row_offsets.at(static_cast<std::size_t>(row));
+    const auto e = cols.begin() + row_offsets.at(static_cast<std::size_t>(row) + 1);
+    const auto it = std::lower_bound(b, e, col);
+    return (it != e && *it == col) ? values[static_cast<std::size_t>(it - cols.begin())] : 0.0;
+}
+
+double StochasticMatrix::row_sum(std::int64_t row) const {
+    double s = 0.0;  // left-to-right, as the reference accessor
+    for (auto k = row_offsets.at(static_cast<std::size_t>(row)); k < row_offsets.at(static_cast<std::size_t>(row) + 1); ++k)
+        s += values[static_cast<std::size_t>(k)];
+    return s;
+}
+
+CountMatrix build_adjacency(std::span<const Edge> edges, std::int64_t n) {
+    if (n <= 0) throw Error("vertex count must be positive");
+    CountMatrix a;
+    a.n = n;
+    a.row_offsets.resize(static_cast<std::size_t>(n) + 1);
+    a.cols.resize(edges.size());
+    a.counts.resize(edges.size());
+    std::int64_t nnz = 0;
+    check(prg_build_adjacency_host(edge_words(edges), static_cast<std::int64_t>(edges.size()), n,
+                                   a.row_offsets.data(), a.cols.data(), a.counts.data(), &nnz));
+    a.cols.resize(static_cast<std::size_t>(nnz));
+    a.counts.resize(static_cast<std::size_t>(nnz));
+    return a;
+}
+
+CountMatrix build_adjacency(EdgeReader& reader, std::int64_t n) {
+    std::vector<Edge> edges;
+    Edge e;
+    while (reader.next(e)) edges.push_back(e);
+    return build_adjacency(std::span<const Edge>(edges), n);
+}
+
+std::vector<std::int64_t> in_degree(const CountMatrix& a) {
+    std::vector<std::int64_t> d(static_cast<std::size_t>(a.n), 0);
+    check(prg_in_degree_host(a.n, a.nnz(), a.cols.data(), a.counts.data(), d.data()));
+    return d;
+}
+
+CountMatrix zero_columns(const CountMatrix& a, const std::vector<std::int64_t>& d_in) {
+    if (static_cast<std::int64_t>(d_in.size()) != a.n) throw Error("in-degree vector length does not match the matrix");
+    CountMatrix out;
+    out.n = a.n;
+    out.row_offsets.resize(static_cast<std::size_t>(a.n) + 1);
+    out.cols.resize(a.cols.size());
+    out.counts.resize(a.counts.size());
+    std::int64_t nz = 0;
+    check(prg_zero_columns_host(a.n, a.nnz(), a.row_offsets.data(), a.cols.data(), a.counts.data(), d_in.data(),
+                                out.row_offsets.data(), out.cols.data(), out.counts.data(), &nz));
+    out.cols.resize(static_cast<std::size_t>(nz));
+    out.counts.resize(static_cast<std::size_t>(nz));
+    return out;
+}
+
+StochasticMatrix row_normalize(const CountMatrix& a) {
+    StochasticMatrix s;
+    s.n = a.n;
+    s.row_offsets = a.row_offsets;
+    s.cols = a.cols;
+    s.values.assign(a.counts.size(), 0.0);
+    if (a.nnz()) check(prg_row_normalize_host(a.n, a.nnz(), a.row_offsets.data(), a.counts.data(), s.values.data()));
+    return s;
+}
+
+Kernel2Result run_kernel2(const EdgeManifest& input) {
+    if (!input.sorted_by_start) throw Error("kernel 2 requires edges sorted by start vertex; run kernel 1 first");
+    Kernel2Result res;
+    res.edges = input.total_edges;
+    Timer timer;  // same region as the reference: read -> build -> filter -> normalise
+    const std::vector<Edge> edges = read_edges(input);
+    prg_matrix* dev = nullptr;
+    check(prg_k2_filter_host(edge_words(edges), static_cast<std::int64_t>(edges.size()), input.vertex_count(), &dev));
+    std::int64_t n = 0, nnz = 0;
+    prg_matrix_info(dev, &n, &nnz, nullptr, nullptr);
+    StochasticMatrix& m = res.matrix;
+    m.n = n;
+    m.row_offsets.resize(static_cast<std::size_t>(n) + 1);
+    m.cols.resize(static_cast<std::size_t>(nnz));
+    m.values.resize(static_cast<std::size_t>(nnz));
+    const prg_status st = prg_matrix_download(dev, m.row_offsets.data(), m.cols.data(), m.values.data(), nullptr);
+    if (st != PRG_OK) {
+        prg_matrix_destroy(dev);
+        check(st);
+    }
+    res.elapsed_seconds = timer.seconds();
+    res.rate = rate_per_second(res.edges, res.elapsed_seconds);
+    cache_put(m, dev);
+    return res;
+}
+
+// ---- K3 ----------------------------------------------------------------------
+void PageRankConfig::validate() const {
+    if (!(damping > 0.0 && damping < 1.0)) throw Error("damping must lie strictly between 0 and 1");
+    if (iterations < 1) throw Error("iteration count must be >= 1");
+}
+
+RankVector init_rank(std::int64_t n, std::uint64_t seed) {
+    if (n < 1) throw Error("rank vector needs at least one entry");
+    RankVector r;
+    r.values.resize(static_cast<std::size_t>(n));
+    check(prg_init_rank_host(n, seed, /*parity*/ 1, r.values.data(), &r.norm1));
+    return r;
+}
+
+RankVector pagerank_step(const RankVector& r, const StochasticMatrix& a, double damping) {
+    if (r.size() != a.n)
+        throw Error("rank vector length " + std::to_string(r.size()) + " does not match matrix size " +
+                    std::to_string(a.n));
+    RankVector out;
+    out.values.resize(static_cast<std::size_t>(a.n));
+    check(prg_pagerank_step_host(a.n, a.nnz(), a.row_offsets.data(), a.cols.data(), a.values.data(), r.values.data(),
+                                 damping, /*parity*/ 1, out.values.data(), &out.norm1));
+    return out;
+}
+
+Kernel3Result run_kernel3(const StochasticMatrix& a, const PageRankConfig& config, std::int64_t total_edges) {
+    config.validate();
+    const char* env = std::getenv("PRPIPE_K3_MODE");
+    const int mode = (env && std::string(env) == "parity") ? 1 : 0;
+    Kernel3Result res;
+    res.ranks.values.resize(static_cast<std::size_t>(a.n));
+    Timer timer;
+    if (prg_matrix* dev = cache_get(a)) {
+        check(prg_k3_pagerank_matrix_host(dev, config.damping, config.iterations, config.seed, mode,
+                                          res.ranks.values.data(), &res.ranks.norm1));
+    } else {
+        check(prg_k3_pagerank_host(a.n, a.nnz(), a.row_offsets.data(), a.cols.data(), a.values.data(), config.damping,
+                                   config.iterations, config.seed, mode, res.ranks.values.data(), &res.ranks.norm1));
+    }
+    res.elapsed_seconds = timer.seconds();
+    res.rate = rate_per_second(static_cast<std::int64_t>(config.iterations) * total_edges, res.elapsed_seconds);
+    return res;
+}
+
+ConvergenceResult run_to_convergence(const StochasticMatrix& a, double damping, double tol, int max_iters,
+                                     std::uint64_t seed) {
+    return run_to_convergence(a, damping, tol, max_iters, init_rank(a.n, seed));
+}
+
+ConvergenceResult run_to_convergence(const StochasticMatrix& a, double damping, double tol, int max_iters,
+                                     RankVector start) {
+    if (!(tol > 0.0)) throw Error("convergence tolerance must be positive");
+    if (max_iters < 1) throw Error("max_iters must be >= 1");
+    if (start.size() != a.n) throw Error("start vector length does not match matrix size");
+    ConvergenceResult res;
+    res.ranks.values.resize(static_cast<std::size_t>(a.n));
+    std::int32_t conv = 0, its = 0;
+    check(prg_run_to_convergence_host(a.n, a.nnz(), a.row_offsets.data(), a.cols.data(), a.values.data(), damping,
+                                      tol, max_iters, start.values.data(), res.ranks.values.data(), &conv, &its));
+    double s = 0.0;
+    for (double v : res.ranks.values) s += v;
+    res.ranks.norm1 = s;
+    res.converged = conv != 0;
+    res.iterations = its;
+    return res;
+}
+
+void dump_ranks(const RankVector& r, const std::filesystem::path& path) {
+    std::ofstream out(path, std::ios::binary | std::ios::trunc);
+    if (!out) throw Error("cannot write rank dump " + path.string());
+    char buf[64];
+    for (std::size_t i = 0; i < r.values.size(); ++i) {
+        char* p = std::to_chars(buf, buf + sizeof(buf), static_cast<std::int64_t>(i) + 1).ptr;
+        *p++ = '\t';
+        p = std::to_chars(p, buf + sizeof(buf), r.values[i]).ptr;
+        *p++ = '\n';
+        out.write(buf, p - buf);
+    }
+    if (!out.flush()) throw Error("failed writing rank dump " + path.string());
+}
+
+}  // namespace prpipe

@@ -105,19 +105,24 @@ __global__ void tile_rows_kernel(const uint32_t* __restrict__ ro, int64_t n, uin
     }
 }
 
-// All threads: srow[li] = row of entry base+li, li < cnt. smem must hold cnt u32.
+// Padded SMEM index for expand_rows' row table: one spare word per 32 keeps the
+// blocked max-scan (thread t touches words 16t..16t+15) free of bank conflicts.
+__device__ __forceinline__ int rpad(int i) { return i + (i >> 5); }
+constexpr int kRowWords = sort::kTile + sort::kTile / 32;
+
+// All threads: srow[rpad(li)] = row of entry base+li, li < cnt. smem must hold kRowWords u32.
 __device__ void expand_rows(const uint32_t* __restrict__ ro, const uint32_t* __restrict__ tile_row,
                             int64_t n, size_t base, int cnt, uint32_t* srow) {
     const uint32_t t = (uint32_t)(base / sort::kTile);
     const uint32_t r0 = tile_row[t];
-    for (int i = threadIdx.x; i < cnt; i += blockDim.x) srow[i] = 0;
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) srow[rpad(i)] = 0;
     __syncthreads();
     if (threadIdx.x == 0) srow[0] = r0;
     // Rows starting inside the tile: scan forward from r0+1 while ro[r] < base+cnt.
     const uint64_t end = base + cnt;
     for (int64_t r = (int64_t)r0 + 1 + threadIdx.x;; r += blockDim.x) {
         const bool in = r < n && ro[r] < end;
-        if (in && ro[r + 1] > ro[r]) srow[ro[r] - base] = (uint32_t)r;
+        if (in && ro[r + 1] > ro[r]) srow[rpad((int)(ro[r] - base))] = (uint32_t)r;
         if (!__syncthreads_or(in)) break;
     }
     // inclusive max-scan over srow (blocked, 8192 entries / blockDim threads)
@@ -125,7 +130,7 @@ __device__ void expand_rows(const uint32_t* __restrict__ ro, const uint32_t* __r
     const int per = (cnt + blockDim.x - 1) / blockDim.x;
     const int l0 = threadIdx.x * per;
     uint32_t m = 0;
-    for (int k = 0; k < per && l0 + k < cnt; ++k) m = max(m, srow[l0 + k]);
+    for (int k = 0; k < per && l0 + k < cnt; ++k) m = max(m, srow[rpad(l0 + k)]);
     uint32_t inc = m;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -148,40 +153,10 @@ __device__ void expand_rows(const uint32_t* __restrict__ ro, const uint32_t* __r
     uint32_t ex = __shfl_up_sync(0xffffffffu, inc, 1);
     if (dev::lane_id() > 0) run = max(run, ex);
     for (int k = 0; k < per && l0 + k < cnt; ++k) {
-        run = max(run, srow[l0 + k]);
-        srow[l0 + k] = run;
+        run = max(run, srow[rpad(l0 + k)]);
+        srow[rpad(l0 + k)] = run;
     }
     __syncthreads();
-}
-
-// Row minimum of stored values -> bmin[u] (as ordered u64 bit patterns; values > 0).
-__global__ void __launch_bounds__(sort::kTileThreads) row_min_kernel(
-    const uint32_t* __restrict__ ro, const uint32_t* __restrict__ tile_row, const double* __restrict__ val,
-    int64_t n, size_t nnz, unsigned long long* __restrict__ bmin) {
-    __shared__ uint32_t srow[sort::kTile];
-    const uint32_t ntiles = div_up(nnz, sort::kTile);
-    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const size_t base = (size_t)t * sort::kTile;
-        const int cnt = (int)min((size_t)sort::kTile, nnz - base);
-        expand_rows(ro, tile_row, n, base, cnt, srow);
-        for (int j = 0; j < sort::kTileItems; ++j) {
-            const int li = j * sort::kTileThreads + threadIdx.x;
-            const bool ok = li < cnt;
-            const uint32_t r = ok ? srow[li] : 0xffffffffu;
-            uint64_t b = ok ? (uint64_t)__double_as_longlong(val[base + li]) : ~0ull;
-            // segmented min over equal rows within the warp (rows are contiguous)
-            const unsigned lane = dev::lane_id();
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const uint64_t ob = __shfl_down_sync(0xffffffffu, b, d);
-                const uint32_t orow = __shfl_down_sync(0xffffffffu, r, d);
-                if (lane + d < 32 && orow == r) b = min(b, ob);
-            }
-            const uint32_t prow = __shfl_up_sync(0xffffffffu, r, 1);
-            if (ok && (lane == 0 || prow != r)) atomicMin(&bmin[r], (unsigned long long)b);
-        }
-        __syncthreads();
-    }
 }
 
 __global__ void gather_base_kernel(const uint32_t* __restrict__ pinv, const unsigned long long* __restrict__ bmin,
@@ -199,35 +174,82 @@ struct CsrEntrySrc {
     const uint32_t* cols;
     const double* val;
     const uint32_t* newid;
-    const unsigned long long* bmin;
+    unsigned long long* bmin;  // row minimum of the stored values (bit patterns, values > 0)
     int64_t n;
     int sb;
-    // exception list (filled by the histogram pass only)
+    int hist_stage;            // 1: histogram pass (computes bmin), 0: scatter pass (uses bmin)
+    // exception list (filled by the scatter pass)
     unsigned long long* exc_key;
     double* exc_val;
     uint32_t* n_exc;
-    static constexpr size_t kSmem = sort::kTile * sizeof(uint32_t);
+    // SMEM: row of each tile entry, then the tile's exception bitmask (scatter pass)
+    static constexpr size_t kSmem = kRowWords * sizeof(uint32_t) + sort::kTile / 8 + sort::kTile / 8;
     __device__ void prepare(size_t base, int cnt, void* smem) const {
-        expand_rows(ro, tile_row, n, base, cnt, static_cast<uint32_t*>(smem));
-    }
-    __device__ __forceinline__ uint64_t key(size_t i, int li, const void* smem) const {
-        const uint32_t r = static_cast<const uint32_t*>(smem)[li];
-        const double v = val[i];
-        const bool exc = (uint64_t)__double_as_longlong(v) != bmin[r];
-        const uint64_t k = ((uint64_t)cols[i] << (sb + 1)) | ((uint64_t)newid[r] << 1) | (uint64_t)exc;
-        if (exc_key) {
-            const unsigned msk = __ballot_sync(__activemask(), exc);
-            if (exc) {
-                const unsigned leader = __ffs(msk) - 1;
-                uint32_t b0 = 0;
-                if (dev::lane_id() == leader) b0 = atomicAdd(n_exc, (uint32_t)__popc(msk));
-                b0 = __shfl_sync(msk, b0, leader);
-                const uint32_t idx = b0 + __popc(msk & ((1u << dev::lane_id()) - 1));
-                exc_key[idx] = k;
-                exc_val[idx] = v;
+        uint32_t* srow = static_cast<uint32_t*>(smem);
+        uint32_t* sexc = srow + kRowWords;
+        expand_rows(ro, tile_row, n, base, cnt, srow);
+        const unsigned lane = dev::lane_id();
+        if (hist_stage) {
+            // Row minimum of this tile's entries: warp-segmented min over rows
+            // (rows are contiguous), one atomicMin per row segment.
+#pragma unroll 8
+            for (int j = 0; j < sort::kTileItems; ++j) {
+                const int li = j * sort::kTileThreads + threadIdx.x;
+                const bool ok = li < cnt;
+                const uint32_t r = ok ? srow[rpad(li)] : 0xffffffffu;
+                uint64_t b = ok ? (uint64_t)__double_as_longlong(val[base + li]) : ~0ull;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const uint64_t ob = __shfl_down_sync(0xffffffffu, b, d);
+                    const uint32_t orow = __shfl_down_sync(0xffffffffu, r, d);
+                    if (lane + d < 32 && orow == r) b = min(b, ob);
+                }
+                const uint32_t prow = __shfl_up_sync(0xffffffffu, r, 1);
+                if (ok && (lane == 0 || prow != r)) atomicMin(&bmin[r], (unsigned long long)b);
+            }
+            return;
+        }
+        // Scatter pass: exception bits (value != row minimum) into the SMEM
+        // bitmask; the tile's exceptions are appended to the list with one
+        // global atomic per tile (a per-warp atomic on one counter serialises).
+        constexpr int kWords = sort::kTile / 32;
+        uint32_t* wpre = sexc + kWords;
+        __shared__ uint32_t scan_tmp[sort::kTileThreads / 32 + 1];
+        __shared__ uint32_t tile_base;
+#pragma unroll 8
+        for (int j = 0; j < sort::kTileItems; ++j) {
+            const int li = j * sort::kTileThreads + threadIdx.x;
+            const bool ok = li < cnt;
+            const bool exc = ok && (uint64_t)__double_as_longlong(val[base + li]) != bmin[srow[rpad(li)]];
+            const unsigned msk = __ballot_sync(0xffffffffu, exc);
+            if (lane == 0) sexc[li >> 5] = msk;
+        }
+        __syncthreads();
+        uint32_t tot;
+        const uint32_t wc = threadIdx.x < kWords ? (uint32_t)__popc(sexc[threadIdx.x]) : 0u;
+        const uint32_t wx = dev::block_excl_scan(wc, scan_tmp, tot);
+        if (threadIdx.x < kWords) wpre[threadIdx.x] = wx;
+        if (threadIdx.x == 0) tile_base = tot ? atomicAdd(n_exc, tot) : 0u;
+        __syncthreads();
+        if (tot == 0) return;
+        const uint32_t b0 = tile_base;
+        for (int j = 0; j < sort::kTileItems; ++j) {
+            const int li = j * sort::kTileThreads + threadIdx.x;
+            const unsigned msk = sexc[li >> 5];
+            if (li < cnt && ((msk >> lane) & 1u)) {
+                const uint32_t idx = b0 + wpre[li >> 5] + __popc(msk & ((1u << lane) - 1));
+                const uint32_t r = srow[rpad(li)];
+                exc_key[idx] = ((uint64_t)cols[base + li] << (sb + 1)) | ((uint64_t)newid[r] << 1) | 1u;
+                exc_val[idx] = val[base + li];
             }
         }
-        return k;
+    }
+    __device__ __forceinline__ uint64_t key(size_t i, int li, const void* smem) const {
+        const uint32_t* srow = static_cast<const uint32_t*>(smem);
+        const uint32_t r = srow[rpad(li)];
+        const uint64_t k = ((uint64_t)cols[i] << (sb + 1)) | ((uint64_t)newid[r] << 1);
+        if (hist_stage) return k;  // the exception bit is a payload bit: digits never see it
+        return k | ((srow[kRowWords + (li >> 5)] >> (li & 31)) & 1u);
     }
 };
 
@@ -854,22 +876,14 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
             P.n_nd = n;
         }
     }
-    // 2. row base values (minimum stored value of each row)
+    // 2. row base values: the minimum stored value of each row, computed by the
+    //    transpose's histogram pass below (it already expands rows and reads values)
     DevBuf<unsigned long long> bmin((size_t)n, s);
     const uint32_t ntiles = nnz ? div_up(nnz, sort::kTile) : 0;
     DevBuf<uint32_t> tile_row(ntiles + 1, s);
-    {
-        ProfScope pr("k3_prep_base", s);
-        PRG_CUDA(cudaMemsetAsync(bmin.get(), 0xff, (size_t)n * 8, s));
-        if (nnz) {
-            tile_rows_kernel<<<g, 1024, 0, s>>>(A->row_offsets, n, tile_row.get());
-            PRG_LAUNCH_CHECK();
-            row_min_kernel<<<std::min<unsigned>(ntiles, (unsigned)num_sms() * 2), sort::kTileThreads, 0, s>>>(
-                A->row_offsets, tile_row.get(), A->values, n, nnz, bmin.get());
-            PRG_LAUNCH_CHECK();
-        }
-        P.bval = DevBuf<double>((size_t)std::max<int64_t>(P.n_nd, 1), s);
-        gather_base_kernel<<<g, 1024, 0, s>>>(P.pinv.get(), bmin.get(), P.n_nd, P.bval.get());
+    PRG_CUDA(cudaMemsetAsync(bmin.get(), 0xff, (size_t)n * 8, s));
+    if (nnz) {
+        tile_rows_kernel<<<g, 1024, 0, s>>>(A->row_offsets, n, tile_row.get());
         PRG_LAUNCH_CHECK();
     }
     // 3. transpose (sort of (col, new row id, exception) keys)
@@ -886,16 +900,23 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
         PRG_CUDA(cudaMemsetAsync(exc_cnt.get(), 0, ngroups * 4, s));
         PRG_CUDA(cudaMemsetAsync(n_exc.get(), 0, 4, s));
         if (nnz) {
+            // histogram pass: row minima, keys without the exception bit;
+            // scatter pass: exception bits from the minima + exception capture.
             CsrEntrySrc src{A->row_offsets, tile_row.get(), A->cols, A->values, P.newid.get(), bmin.get(), n, P.sb,
-                            exc_key.get(), exc_v.get(), n_exc.get()};
-            // The histogram pass captures the exception list; the scatter pass must not.
+                            1, nullptr, nullptr, nullptr};
             CsrEntrySrc scat = src;
-            scat.exc_key = nullptr;
+            scat.hist_stage = 0;
+            scat.exc_key = exc_key.get();
+            scat.exc_val = exc_v.get();
+            scat.n_exc = n_exc.get();
             sort::SortWorkspace ws;
             sort::msd_sort_split(src, scat, (size_t)nnz, 2 * P.sb + 1,
                                  CscDst{P.csc_idx.get(), P.colptr.get(), exc_cnt.get(), P.sb}, ws, s, "k3t",
                                  /*payload_bits=*/1);
         }
+        P.bval = DevBuf<double>((size_t)std::max<int64_t>(P.n_nd, 1), s);
+        gather_base_kernel<<<g, 1024, 0, s>>>(P.pinv.get(), bmin.get(), P.n_nd, P.bval.get());
+        PRG_LAUNCH_CHECK();
         // colptr[n] = nnz, then fill empty columns with the next column start.
         const uint32_t nz = (uint32_t)nnz;
         PRG_CUDA(cudaMemcpyAsync(P.colptr.get() + n, &nz, 4, cudaMemcpyHostToDevice, s));

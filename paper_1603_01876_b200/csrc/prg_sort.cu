@@ -206,7 +206,7 @@ __global__ void classify_kernel(const Seg* __restrict__ active, const uint32_t* 
                                 const uint64_t* __restrict__ seg_elem0,
                                 const uint32_t* __restrict__ off, Seg* __restrict__ next,
                                 uint32_t* __restrict__ n_next, Seg* __restrict__ fin,
-                                uint32_t* __restrict__ n_fin) {
+                                uint32_t* __restrict__ n_fin, int floor_bit) {
     __shared__ uint64_t cst[kRadix];
     __shared__ uint32_t csz[kRadix];
     const uint32_t na = *n_active;
@@ -224,7 +224,8 @@ __global__ void classify_kernel(const Seg* __restrict__ active, const uint32_t* 
         }
         __syncthreads();
         if (threadIdx.x == 0) {
-            const int nb = sg.shift >= 8 ? 8 : sg.shift;
+            const int rem = sg.shift - floor_bit;
+            const int nb = rem >= 8 ? 8 : rem;
             emit_children(cst, csz, nd, (uint8_t)(sg.buf ^ 1), sg.shift - nb, nb, next, n_next, fin, n_fin);
         }
         __syncthreads();
@@ -258,7 +259,7 @@ void sort_workspace_init(SortWorkspace& ws, size_t n, cudaStream_t s) {
     ws.seg_elem0 = DevBuf<uint64_t>(ws.max_active + 1, s);
 }
 
-void run_segmented_levels(SortWorkspace& ws, int levels_left, cudaStream_t s) {
+void run_segmented_levels(SortWorkspace& ws, int levels_left, int floor_bit, cudaStream_t s) {
     static bool attr_set = false;
     const size_t smem = (size_t)kTile * sizeof(uint64_t);
     if (!attr_set) {
@@ -294,7 +295,7 @@ void run_segmented_levels(SortWorkspace& ws, int levels_left, cudaStream_t s) {
             ws.off.get());
         PRG_LAUNCH_CHECK();
         classify_kernel<<<grid, kRadix, 0, s>>>(act, n_act, ws.seg_tile0.get(), ws.seg_elem0.get(),
-                                                 ws.off.get(), nxt, n_nxt, ws.fin.get(), cnt + 2);
+                                                 ws.off.get(), nxt, n_nxt, ws.fin.get(), cnt + 2, floor_bit);
         PRG_LAUNCH_CHECK();
     }
 }

@@ -166,7 +166,7 @@ __global__ void classify_kernel(const Seg* __restrict__ active, const uint32_t* 
                                 const uint64_t* __restrict__ seg_elem0,
                                 const uint32_t* __restrict__ off, Seg* __restrict__ next,
                                 uint32_t* __restrict__ n_next, Seg* __restrict__ fin,
-                                uint32_t* __restrict__ n_fin);
+                                uint32_t* __restrict__ n_fin, int floor_bit);
 
 // Level-1 children classification (the whole input was one segment).
 __global__ void classify_l1_kernel(const uint32_t* __restrict__ off, uint32_t ntiles, size_t n,
@@ -356,7 +356,7 @@ size_t local_smem_bytes();
 
 // Runs levels >= 2 until every segment is final; then the caller launches
 // local_sort_kernel with its Dst. `key_bits` is the number of significant bits.
-void run_segmented_levels(SortWorkspace& ws, int levels_left, cudaStream_t s);
+void run_segmented_levels(SortWorkspace& ws, int levels_left, int floor_bit, cudaStream_t s);
 
 // src_hist feeds the level-1 histogram pass and src_scat the level-1 scatter
 // pass; they must produce identical keys (K3 uses the split to capture its
@@ -367,8 +367,12 @@ void msd_sort_split(Src src_hist, Src src_scat, size_t n, int key_bits, Dst dst,
     const std::string t(tag);
     if (n == 0) return;
     sort_workspace_init(ws, n, s);
-    const int bits1 = key_bits < 8 ? (key_bits > 0 ? key_bits : 1) : 8;
-    const int shift1 = key_bits - bits1 > 0 ? key_bits - bits1 : 0;
+    // Digits cover bits [payload_bits, key_bits); the low payload bits ride along
+    // (they never decide the order: keys are unique above them, or equal keys
+    // carry equal payloads).
+    const int span = key_bits - payload_bits;
+    const int bits1 = span < 8 ? (span > 0 ? span : 1) : 8;
+    const int shift1 = key_bits - bits1 > payload_bits ? key_bits - bits1 : payload_bits;
     const unsigned dmask = (1u << bits1) - 1u;
     const uint32_t ntiles = div_up(n, kTile);
     const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)num_sms() * 4);
@@ -391,14 +395,15 @@ void msd_sort_split(Src src_hist, Src src_scat, size_t n, int key_bits, Dst dst,
         l1_scatter_kernel<Src><<<grid, kTileThreads, smem, s>>>(src_scat, n, shift1, dmask, ntiles,
                                                                 ws.off.get(), ws.keys[1].get());
         PRG_LAUNCH_CHECK();
-        classify_l1_kernel<<<1, kRadix, 0, s>>>(ws.off.get(), ntiles, n, shift1, shift1 >= 8 ? 8 : shift1,
+        const int rem1 = shift1 - payload_bits;
+        classify_l1_kernel<<<1, kRadix, 0, s>>>(ws.off.get(), ntiles, n, shift1, rem1 >= 8 ? 8 : rem1,
                                                  ws.lists[0].get(), ws.counters.get() + 0, ws.fin.get(),
                                                  ws.counters.get() + 2);
         PRG_LAUNCH_CHECK();
     }
     {
         ProfScope prof(t + "_levels", s);
-        run_segmented_levels(ws, (shift1 + 7) / 8, s);
+        run_segmented_levels(ws, (shift1 - payload_bits + 7) / 8, payload_bits, s);
     }
     {
         ProfScope prof(t + "_local", s);

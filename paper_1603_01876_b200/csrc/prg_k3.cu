@@ -159,99 +159,130 @@ __device__ void expand_rows(const uint32_t* __restrict__ ro, const uint32_t* __r
     __syncthreads();
 }
 
+// Degrees in new row order, and the shift from CSR to permuted positions
+// (u32 wrap-around arithmetic; nnz < 2^32).
+__global__ void perm_degree_kernel(const uint32_t* __restrict__ ro, const uint32_t* __restrict__ pinv, int64_t nr,
+                                   uint32_t* __restrict__ deg) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nr; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t u = pinv[i];
+        deg[i] = ro[u + 1] - ro[u];
+    }
+}
+__global__ void perm_delta_kernel(const uint32_t* __restrict__ ro, const uint32_t* __restrict__ pinv,
+                                  const uint32_t* __restrict__ pro, int64_t nr, uint32_t* __restrict__ wdelta) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nr; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t u = pinv[i];
+        wdelta[u] = pro[i] - ro[u];
+    }
+}
+
+// Row minimum of the stored values -> bmin[u] (ordered u64 bit patterns;
+// values > 0). CSR-order tiles (coalesced), warp-segmented min per row, one
+// atomicMin per row segment.
+__global__ void __launch_bounds__(sort::kTileThreads, 2)
+    row_min_kernel(const uint32_t* __restrict__ ro, const uint32_t* __restrict__ tile_row,
+                   const double* __restrict__ val, int64_t n, uint64_t nnz, unsigned long long* __restrict__ bmin) {
+    extern __shared__ uint32_t srow[];
+    const unsigned lane = dev::lane_id();
+    const uint32_t ntiles = (uint32_t)((nnz + sort::kTile - 1) / sort::kTile);
+    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const size_t base = (size_t)t * sort::kTile;
+        const int cnt = (int)min((uint64_t)sort::kTile, nnz - base);
+        expand_rows(ro, tile_row, n, base, cnt, srow);
+#pragma unroll 8
+        for (int j = 0; j < sort::kTileItems; ++j) {
+            const int li = j * sort::kTileThreads + threadIdx.x;
+            const bool ok = li < cnt;
+            const uint32_t r = ok ? srow[rpad(li)] : 0xffffffffu;
+            uint64_t b = ok ? (uint64_t)__double_as_longlong(val[base + li]) : ~0ull;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint64_t ob = __shfl_down_sync(0xffffffffu, b, d);
+                const uint32_t orow = __shfl_down_sync(0xffffffffu, r, d);
+                if (lane + d < 32 && orow == r) b = min(b, ob);
+            }
+            const uint32_t prow = __shfl_up_sync(0xffffffffu, r, 1);
+            if (ok && (lane == 0 || prow != r)) atomicMin(&bmin[r], (unsigned long long)b);
+        }
+        __syncthreads();
+    }
+}
+
+// Transpose keys: for every CSR entry (u, col, a) the key
+// (col, newid[u], a != bmin[u]) written at its position in the NEW row order
+// (rows permuted, each row's entries contiguous). A stable sort of these keys
+// by column then lists every column's rows in ascending new id. Exceptions
+// (a != row base) are also appended to a list (one atomic per tile).
+struct KeyBuildArgs {
+    const uint32_t* ro;
+    const uint32_t* tile_row;
+    const uint32_t* cols;
+    const double* val;
+    const unsigned long long* bmin;
+    const uint32_t* newid;   // null: identity
+    const uint32_t* wdelta;  // null: identity
+    int64_t n;
+    uint64_t nnz;
+    int sb;
+    unsigned long long* keys;
+    unsigned long long* exc_key;
+    double* exc_val;
+    uint32_t* n_exc;
+};
+__global__ void __launch_bounds__(sort::kTileThreads, 2) key_build_kernel(KeyBuildArgs a) {
+    extern __shared__ uint32_t srow[];
+    __shared__ uint32_t scan_tmp[sort::kTileThreads / 32 + 1];
+    __shared__ uint32_t tile_base;
+    const uint32_t ntiles = (uint32_t)((a.nnz + sort::kTile - 1) / sort::kTile);
+    const unsigned lane = dev::lane_id();
+    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const size_t base = (size_t)t * sort::kTile;
+        const int cnt = (int)min((uint64_t)sort::kTile, a.nnz - base);
+        expand_rows(a.ro, a.tile_row, a.n, base, cnt, srow);
+        uint32_t excm = 0;
+#pragma unroll 8
+        for (int j = 0; j < sort::kTileItems; ++j) {
+            const int li = j * sort::kTileThreads + threadIdx.x;
+            if (li < cnt) {
+                const uint32_t u = srow[rpad(li)];
+                const uint32_t e = (uint32_t)(base + li);
+                const uint32_t c = a.cols[e];
+                const double v = a.val[e];
+                const bool exc = (uint64_t)__double_as_longlong(v) != a.bmin[u];
+                const uint32_t nid = a.newid ? a.newid[u] : u;
+                const uint32_t pos = a.wdelta ? e + a.wdelta[u] : e;
+                a.keys[pos] = ((uint64_t)c << (a.sb + 1)) | ((uint64_t)nid << 1) | (uint64_t)exc;
+                excm |= (uint32_t)exc << j;
+            }
+        }
+        uint32_t tot;
+        const uint32_t ex = dev::block_excl_scan((uint32_t)__popc(excm), scan_tmp, tot);
+        if (threadIdx.x == 0) tile_base = tot ? atomicAdd(a.n_exc, tot) : 0u;
+        __syncthreads();
+        if (excm) {
+            uint32_t idx = tile_base + ex;
+            for (int j = 0; j < sort::kTileItems; ++j) {
+                if (!((excm >> j) & 1u)) continue;
+                const int li = j * sort::kTileThreads + threadIdx.x;
+                const uint32_t u = srow[rpad(li)];
+                const uint32_t e = (uint32_t)(base + li);
+                const uint32_t nid = a.newid ? a.newid[u] : u;
+                a.exc_key[idx] = ((uint64_t)a.cols[e] << (a.sb + 1)) | ((uint64_t)nid << 1) | 1u;
+                a.exc_val[idx] = a.val[e];
+                ++idx;
+            }
+        }
+        __syncthreads();
+    }
+    (void)lane;
+}
+
+// bval[i] = row base of new row i.
 __global__ void gather_base_kernel(const uint32_t* __restrict__ pinv, const unsigned long long* __restrict__ bmin,
                                    int64_t n_nd, double* __restrict__ bval) {
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n_nd; j += (int64_t)gridDim.x * blockDim.x)
         bval[j] = __longlong_as_double((long long)bmin[pinv[j]]);
 }
-
-// ---------------------------------------------------------------------------
-// Transpose: sort keys (col << (sb+1)) | (newid << 1) | exc
-// ---------------------------------------------------------------------------
-struct CsrEntrySrc {
-    const uint32_t* ro;
-    const uint32_t* tile_row;
-    const uint32_t* cols;
-    const double* val;
-    const uint32_t* newid;
-    unsigned long long* bmin;  // row minimum of the stored values (bit patterns, values > 0)
-    int64_t n;
-    int sb;
-    int hist_stage;            // 1: histogram pass (computes bmin), 0: scatter pass (uses bmin)
-    // exception list (filled by the scatter pass)
-    unsigned long long* exc_key;
-    double* exc_val;
-    uint32_t* n_exc;
-    // SMEM: row of each tile entry, then the tile's exception bitmask (scatter pass)
-    static constexpr size_t kSmem = kRowWords * sizeof(uint32_t) + sort::kTile / 8 + sort::kTile / 8;
-    __device__ void prepare(size_t base, int cnt, void* smem) const {
-        uint32_t* srow = static_cast<uint32_t*>(smem);
-        uint32_t* sexc = srow + kRowWords;
-        expand_rows(ro, tile_row, n, base, cnt, srow);
-        const unsigned lane = dev::lane_id();
-        if (hist_stage) {
-            // Row minimum of this tile's entries: warp-segmented min over rows
-            // (rows are contiguous), one atomicMin per row segment.
-#pragma unroll 8
-            for (int j = 0; j < sort::kTileItems; ++j) {
-                const int li = j * sort::kTileThreads + threadIdx.x;
-                const bool ok = li < cnt;
-                const uint32_t r = ok ? srow[rpad(li)] : 0xffffffffu;
-                uint64_t b = ok ? (uint64_t)__double_as_longlong(val[base + li]) : ~0ull;
-#pragma unroll
-                for (int d = 1; d < 32; d <<= 1) {
-                    const uint64_t ob = __shfl_down_sync(0xffffffffu, b, d);
-                    const uint32_t orow = __shfl_down_sync(0xffffffffu, r, d);
-                    if (lane + d < 32 && orow == r) b = min(b, ob);
-                }
-                const uint32_t prow = __shfl_up_sync(0xffffffffu, r, 1);
-                if (ok && (lane == 0 || prow != r)) atomicMin(&bmin[r], (unsigned long long)b);
-            }
-            return;
-        }
-        // Scatter pass: exception bits (value != row minimum) into the SMEM
-        // bitmask; the tile's exceptions are appended to the list with one
-        // global atomic per tile (a per-warp atomic on one counter serialises).
-        constexpr int kWords = sort::kTile / 32;
-        uint32_t* wpre = sexc + kWords;
-        __shared__ uint32_t scan_tmp[sort::kTileThreads / 32 + 1];
-        __shared__ uint32_t tile_base;
-#pragma unroll 8
-        for (int j = 0; j < sort::kTileItems; ++j) {
-            const int li = j * sort::kTileThreads + threadIdx.x;
-            const bool ok = li < cnt;
-            const bool exc = ok && (uint64_t)__double_as_longlong(val[base + li]) != bmin[srow[rpad(li)]];
-            const unsigned msk = __ballot_sync(0xffffffffu, exc);
-            if (lane == 0) sexc[li >> 5] = msk;
-        }
-        __syncthreads();
-        uint32_t tot;
-        const uint32_t wc = threadIdx.x < kWords ? (uint32_t)__popc(sexc[threadIdx.x]) : 0u;
-        const uint32_t wx = dev::block_excl_scan(wc, scan_tmp, tot);
-        if (threadIdx.x < kWords) wpre[threadIdx.x] = wx;
-        if (threadIdx.x == 0) tile_base = tot ? atomicAdd(n_exc, tot) : 0u;
-        __syncthreads();
-        if (tot == 0) return;
-        const uint32_t b0 = tile_base;
-        for (int j = 0; j < sort::kTileItems; ++j) {
-            const int li = j * sort::kTileThreads + threadIdx.x;
-            const unsigned msk = sexc[li >> 5];
-            if (li < cnt && ((msk >> lane) & 1u)) {
-                const uint32_t idx = b0 + wpre[li >> 5] + __popc(msk & ((1u << lane) - 1));
-                const uint32_t r = srow[rpad(li)];
-                exc_key[idx] = ((uint64_t)cols[base + li] << (sb + 1)) | ((uint64_t)newid[r] << 1) | 1u;
-                exc_val[idx] = val[base + li];
-            }
-        }
-    }
-    __device__ __forceinline__ uint64_t key(size_t i, int li, const void* smem) const {
-        const uint32_t* srow = static_cast<const uint32_t*>(smem);
-        const uint32_t r = srow[rpad(li)];
-        const uint64_t k = ((uint64_t)cols[i] << (sb + 1)) | ((uint64_t)newid[r] << 1);
-        if (hist_stage) return k;  // the exception bit is a payload bit: digits never see it
-        return k | ((srow[kRowWords + (li >> 5)] >> (li & 31)) & 1u);
-    }
-};
 
 struct CscDst {
     uint32_t* csc_idx;
@@ -876,17 +907,38 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
             P.n_nd = n;
         }
     }
-    // 2. row base values: the minimum stored value of each row, computed by the
-    //    transpose's histogram pass below (it already expands rows and reads values)
+    // 2. row base values (minimum stored value of each row) and the shift of
+    //    every row to its place in the new row order
+    const int64_t nr = P.n_nd;  // non-dangling rows (dangling rows are last in the new order)
     DevBuf<unsigned long long> bmin((size_t)n, s);
+    DevBuf<uint32_t> wdelta;
     const uint32_t ntiles = nnz ? div_up(nnz, sort::kTile) : 0;
     DevBuf<uint32_t> tile_row(ntiles + 1, s);
-    PRG_CUDA(cudaMemsetAsync(bmin.get(), 0xff, (size_t)n * 8, s));
-    if (nnz) {
-        tile_rows_kernel<<<g, 1024, 0, s>>>(A->row_offsets, n, tile_row.get());
+    const size_t row_smem = kRowWords * sizeof(uint32_t);
+    {
+        ProfScope pr("k3_prep_base", s);
+        PRG_CUDA(cudaMemsetAsync(bmin.get(), 0xff, (size_t)n * 8, s));
+        if (mode == 0) {
+            DevBuf<uint32_t> deg((size_t)std::max<int64_t>(nr, 1), s), pro((size_t)nr + 1, s);
+            wdelta = DevBuf<uint32_t>((size_t)n, s);
+            perm_degree_kernel<<<g, 1024, 0, s>>>(A->row_offsets, P.pinv.get(), nr, deg.get());
+            PRG_LAUNCH_CHECK();
+            exclusive_scan_u32(deg.get(), pro.get(), (size_t)nr, pro.get() + nr, s);
+            perm_delta_kernel<<<g, 1024, 0, s>>>(A->row_offsets, P.pinv.get(), pro.get(), nr, wdelta.get());
+            PRG_LAUNCH_CHECK();
+        }
+        if (nnz) {
+            tile_rows_kernel<<<g, 1024, 0, s>>>(A->row_offsets, n, tile_row.get());
+            PRG_LAUNCH_CHECK();
+            row_min_kernel<<<num_sms() * 2, sort::kTileThreads, row_smem, s>>>(A->row_offsets, tile_row.get(),
+                                                                              A->values, n, nnz, bmin.get());
+            PRG_LAUNCH_CHECK();
+        }
+        P.bval = DevBuf<double>((size_t)std::max<int64_t>(nr, 1), s);
+        gather_base_kernel<<<g, 1024, 0, s>>>(P.pinv.get(), bmin.get(), nr, P.bval.get());
         PRG_LAUNCH_CHECK();
     }
-    // 3. transpose (sort of (col, new row id, exception) keys)
+    // 3. transpose: stable sort of (col | new row, exception) keys by column
     P.colptr = DevBuf<uint32_t>((size_t)n + 1, s);
     P.csc_idx = DevBuf<uint32_t>(nnz ? nnz : 1, s);
     const uint64_t ngroups = nnz / kCscGroup + 1;
@@ -900,23 +952,24 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
         PRG_CUDA(cudaMemsetAsync(exc_cnt.get(), 0, ngroups * 4, s));
         PRG_CUDA(cudaMemsetAsync(n_exc.get(), 0, 4, s));
         if (nnz) {
-            // histogram pass: row minima, keys without the exception bit;
-            // scatter pass: exception bits from the minima + exception capture.
-            CsrEntrySrc src{A->row_offsets, tile_row.get(), A->cols, A->values, P.newid.get(), bmin.get(), n, P.sb,
-                            1, nullptr, nullptr, nullptr};
-            CsrEntrySrc scat = src;
-            scat.hist_stage = 0;
-            scat.exc_key = exc_key.get();
-            scat.exc_val = exc_v.get();
-            scat.n_exc = n_exc.get();
             sort::SortWorkspace ws;
-            sort::msd_sort_split(src, scat, (size_t)nnz, 2 * P.sb + 1,
+            sort::sort_workspace_init(ws, (size_t)nnz, s);
+            {
+                ProfScope pk("k3t_keys", s);
+                KeyBuildArgs ka{A->row_offsets, tile_row.get(), A->cols, A->values, bmin.get(),
+                                mode == 0 ? P.newid.get() : nullptr, mode == 0 ? wdelta.get() : nullptr, n, nnz, P.sb,
+                                reinterpret_cast<unsigned long long*>(ws.keys[0].get()), exc_key.get(), exc_v.get(),
+                                n_exc.get()};
+                key_build_kernel<<<num_sms() * 2, sort::kTileThreads, row_smem, s>>>(ka);
+                PRG_LAUNCH_CHECK();
+            }
+            // the keys live in ws.keys[0]; level 1 reads them before any pass overwrites that buffer.
+            // (new row, exception) ride as payload: only column bits are sorted
+            const KeyArraySrc src{reinterpret_cast<const unsigned long long*>(ws.keys[0].get())};
+            sort::msd_sort_split(src, src, (size_t)nnz, 2 * P.sb + 1,
                                  CscDst{P.csc_idx.get(), P.colptr.get(), exc_cnt.get(), P.sb}, ws, s, "k3t",
-                                 /*payload_bits=*/1);
+                                 /*payload_bits=*/P.sb + 1, /*stable=*/true);
         }
-        P.bval = DevBuf<double>((size_t)std::max<int64_t>(P.n_nd, 1), s);
-        gather_base_kernel<<<g, 1024, 0, s>>>(P.pinv.get(), bmin.get(), P.n_nd, P.bval.get());
-        PRG_LAUNCH_CHECK();
         // colptr[n] = nnz, then fill empty columns with the next column start.
         const uint32_t nz = (uint32_t)nnz;
         PRG_CUDA(cudaMemcpyAsync(P.colptr.get() + n, &nz, 4, cudaMemcpyHostToDevice, s));

@@ -140,6 +140,7 @@ __global__ void __launch_bounds__(kTileThreads) seg_hist_kernel(
     }
 }
 
+template <bool kStable>
 __global__ void __launch_bounds__(kTileThreads, 2) seg_scatter_kernel(
     const uint64_t* __restrict__ keys0, const uint64_t* __restrict__ keys1,
     uint64_t* __restrict__ out0, uint64_t* __restrict__ out1, const Seg* __restrict__ active,
@@ -150,7 +151,8 @@ __global__ void __launch_bounds__(kTileThreads, 2) seg_scatter_kernel(
     __shared__ uint32_t lstart[kRadix];
     __shared__ uint64_t gbase[kRadix];
     __shared__ uint32_t scan_tmp[kTileThreads / 32 + 1];
-    extern __shared__ uint64_t skeys[];
+    extern __shared__ __align__(16) uint64_t skeys[];  // kTile keys (+ stable counters)
+    uint32_t* wc = reinterpret_cast<uint32_t*>(skeys + kTile);
     const uint32_t nt = *n_tiles;
     for (uint32_t t = blockIdx.x; t < nt; t += gridDim.x) {
         const uint32_t si = tile_seg[t], ti = tile_idx[t];
@@ -159,39 +161,46 @@ __global__ void __launch_bounds__(kTileThreads, 2) seg_scatter_kernel(
         uint64_t* dst = sg.buf ? out0 : out1;
         const uint32_t seg_nt = seg_tile0[si + 1] - seg_tile0[si];
         const uint64_t e0 = seg_elem0[si];
-        for (int i = threadIdx.x; i < kRadix; i += blockDim.x) h[i] = 0;
-        __syncthreads();
+        if (!kStable) {
+            for (int i = threadIdx.x; i < kRadix; i += blockDim.x) h[i] = 0;
+            __syncthreads();
+        }
         const uint64_t base = sg.start + (uint64_t)ti * kTile;
         const int cnt = (int)min((uint64_t)kTile, (uint64_t)sg.size - (uint64_t)ti * kTile);
         const unsigned mask = (1u << sg.bits) - 1u;
         uint64_t k[kTileItems];
 #pragma unroll
         for (int j = 0; j < kTileItems; ++j) {
-            int li = j * kTileThreads + threadIdx.x;
+            const int li = tile_pos<kStable>(j);
             if (li < cnt) {
                 k[j] = src[base + li];
-                atomicAdd(&h[(unsigned)(k[j] >> sg.shift) & mask], 1u);
+                if (!kStable) atomicAdd(&h[(unsigned)(k[j] >> sg.shift) & mask], 1u);
             }
         }
-        __syncthreads();
-        {
+        const size_t hb = (size_t)seg_tile0[si] * kRadix;
+        if (kStable) {
+            stable_tile_scatter(k, cnt, sg.shift, sg.bits, wc, lstart, scan_tmp, skeys);
+            // off is relative to the concatenation of active segments
+            if (threadIdx.x < kRadix)
+                gbase[threadIdx.x] = sg.start + (off[hb + (size_t)threadIdx.x * seg_nt + ti] - e0);
+            __syncthreads();
+        } else {
+            __syncthreads();
             uint32_t v = threadIdx.x < kRadix ? h[threadIdx.x] : 0u, tot;
             uint32_t ex = dev::block_excl_scan(v, scan_tmp, tot);
             if (threadIdx.x < kRadix) {
                 lstart[threadIdx.x] = ex;
                 h[threadIdx.x] = ex;  // per-digit cursor
-                const size_t hb = (size_t)seg_tile0[si] * kRadix;
-                // off is relative to the concatenation of active segments
                 gbase[threadIdx.x] = sg.start + (off[hb + (size_t)threadIdx.x * seg_nt + ti] - e0);
             }
-        }
-        __syncthreads();
+            __syncthreads();
 #pragma unroll
-        for (int j = 0; j < kTileItems; ++j) {
-            int li = j * kTileThreads + threadIdx.x;
-            if (li < cnt) skeys[atomicAdd(&h[(unsigned)(k[j] >> sg.shift) & mask], 1u)] = k[j];
+            for (int j = 0; j < kTileItems; ++j) {
+                int li = j * kTileThreads + threadIdx.x;
+                if (li < cnt) skeys[atomicAdd(&h[(unsigned)(k[j] >> sg.shift) & mask], 1u)] = k[j];
+            }
+            __syncthreads();
         }
-        __syncthreads();
         for (int i = threadIdx.x; i < cnt; i += kTileThreads) {
             uint64_t key = skeys[i];
             unsigned d = (unsigned)(key >> sg.shift) & mask;
@@ -259,12 +268,14 @@ void sort_workspace_init(SortWorkspace& ws, size_t n, cudaStream_t s) {
     ws.seg_elem0 = DevBuf<uint64_t>(ws.max_active + 1, s);
 }
 
-void run_segmented_levels(SortWorkspace& ws, int levels_left, int floor_bit, cudaStream_t s) {
+void run_segmented_levels(SortWorkspace& ws, int levels_left, int floor_bit, bool stable, cudaStream_t s) {
     static bool attr_set = false;
-    const size_t smem = (size_t)kTile * sizeof(uint64_t);
+    const size_t smem = (size_t)kTile * sizeof(uint64_t) + (stable ? kStableScratch : 0);
     if (!attr_set) {
-        PRG_CUDA(cudaFuncSetAttribute(seg_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
+        PRG_CUDA(cudaFuncSetAttribute(seg_scatter_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)((size_t)kTile * sizeof(uint64_t))));
+        PRG_CUDA(cudaFuncSetAttribute(seg_scatter_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)((size_t)kTile * sizeof(uint64_t) + kStableScratch)));
         attr_set = true;
     }
     const unsigned grid = (unsigned)num_sms() * 4;
@@ -289,10 +300,16 @@ void run_segmented_levels(SortWorkspace& ws, int levels_left, int floor_bit, cud
                                                       ws.tile_idx.get(), cnt + 4, ws.hist.get());
         PRG_LAUNCH_CHECK();
         exclusive_scan_u32(ws.hist.get(), ws.off.get(), hsz, nullptr, s);
-        seg_scatter_kernel<<<grid, kTileThreads, smem, s>>>(
-            ws.keys[0].get(), ws.keys[1].get(), ws.keys[0].get(), ws.keys[1].get(), act,
-            ws.seg_tile0.get(), ws.seg_elem0.get(), ws.tile_seg.get(), ws.tile_idx.get(), cnt + 4,
-            ws.off.get());
+        if (stable)
+            seg_scatter_kernel<true><<<grid, kTileThreads, smem, s>>>(
+                ws.keys[0].get(), ws.keys[1].get(), ws.keys[0].get(), ws.keys[1].get(), act,
+                ws.seg_tile0.get(), ws.seg_elem0.get(), ws.tile_seg.get(), ws.tile_idx.get(), cnt + 4,
+                ws.off.get());
+        else
+            seg_scatter_kernel<false><<<grid, kTileThreads, smem, s>>>(
+                ws.keys[0].get(), ws.keys[1].get(), ws.keys[0].get(), ws.keys[1].get(), act,
+                ws.seg_tile0.get(), ws.seg_elem0.get(), ws.tile_seg.get(), ws.tile_idx.get(), cnt + 4,
+                ws.off.get());
         PRG_LAUNCH_CHECK();
         classify_kernel<<<grid, kRadix, 0, s>>>(act, n_act, ws.seg_tile0.get(), ws.seg_elem0.get(),
                                                  ws.off.get(), nxt, n_nxt, ws.fin.get(), cnt + 2, floor_bit);

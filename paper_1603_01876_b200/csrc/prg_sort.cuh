@@ -67,20 +67,99 @@ __global__ void __launch_bounds__(kTileThreads) l1_hist_kernel(Src src, size_t n
     }
 }
 
+// ---------------------------------------------------------------------------
+// Stable tile ranking (used when the sort must preserve input order among
+// keys equal above the payload bits — the K3 transpose keeps each column's
+// rows in input order and so only sorts column bits). Each warp owns a
+// contiguous chunk of the tile (position li = warp*kWarpSpan + j*32 + lane),
+// so a key's stable slot is: prefix over (digit, earlier warps) + keys of the
+// same digit in the warp's earlier rows + its peers among lower lanes (found
+// with one ballot per digit bit — no match_any).
+// ---------------------------------------------------------------------------
+constexpr int kTileWarps = kTileThreads / 32;
+constexpr int kWarpSpan = kTileItems * 32;
+constexpr size_t kStableScratch = (size_t)kRadix * kTileWarps * sizeof(uint32_t);  // 16 KB
+static_assert(kRadix * kTileWarps == 8 * kTileThreads, "scan assumes 8 counters per thread");
+
+template <bool kStable>
+__device__ __forceinline__ int tile_pos(int j) {
+    return kStable ? (int)(dev::warp_id() * kWarpSpan + j * 32 + dev::lane_id()) : j * kTileThreads + (int)threadIdx.x;
+}
+
+// k[j] holds the key at tile_pos<true>(j) (valid when < cnt). On return skeys
+// holds the tile in (digit, position) order and lstart[d] the digit starts.
+// wc: kStableScratch bytes of SMEM (may alias dead scratch). Ends with a barrier.
+__device__ __forceinline__ void stable_tile_scatter(const uint64_t (&k)[kTileItems], int cnt, int shift, int bits,
+                                                    uint32_t* __restrict__ wc, uint32_t* __restrict__ lstart,
+                                                    uint32_t* __restrict__ scan_tmp, uint64_t* __restrict__ skeys) {
+    const unsigned w = dev::warp_id(), lane = dev::lane_id();
+    const unsigned mask = (1u << bits) - 1u;
+    const unsigned t = threadIdx.x;
+    reinterpret_cast<uint4*>(wc)[2 * t] = make_uint4(0, 0, 0, 0);
+    reinterpret_cast<uint4*>(wc)[2 * t + 1] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kTileItems; ++j) {
+        if (tile_pos<true>(j) < cnt) atomicAdd(&wc[((unsigned)(k[j] >> shift) & mask) * kTileWarps + w], 1u);
+    }
+    __syncthreads();
+    {   // exclusive scan over (digit, warp); thread t owns digit t/2, warps 8*(t&1)..+7
+        uint4 a = reinterpret_cast<uint4*>(wc)[2 * t], b = reinterpret_cast<uint4*>(wc)[2 * t + 1];
+        const uint32_t sum = a.x + a.y + a.z + a.w + b.x + b.y + b.z + b.w;
+        uint32_t tot;
+        uint32_t run = dev::block_excl_scan(sum, scan_tmp, tot);
+        if ((t & 1u) == 0) lstart[t >> 1] = run;
+        uint32_t v;
+        v = a.x; a.x = run; run += v;  v = a.y; a.y = run; run += v;
+        v = a.z; a.z = run; run += v;  v = a.w; a.w = run; run += v;
+        v = b.x; b.x = run; run += v;  v = b.y; b.y = run; run += v;
+        v = b.z; b.z = run; run += v;  v = b.w; b.w = run;
+        reinterpret_cast<uint4*>(wc)[2 * t] = a;
+        reinterpret_cast<uint4*>(wc)[2 * t + 1] = b;
+    }
+    __syncthreads();
+    const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int j = 0; j < kTileItems; ++j) {
+        const bool valid = tile_pos<true>(j) < cnt;
+        const unsigned d = valid ? ((unsigned)(k[j] >> shift) & mask) : 0u;
+        unsigned peers = __ballot_sync(0xffffffffu, valid);
+        for (int b = 0; b < bits; ++b) {
+            const bool bit = (d >> b) & 1u;
+            const unsigned bal = __ballot_sync(0xffffffffu, bit);
+            peers &= bit ? bal : ~bal;
+        }
+        uint32_t* cp = &wc[d * kTileWarps + w];
+        const uint32_t p0 = valid ? *cp : 0u;
+        __syncwarp();
+        if (valid) {
+            skeys[p0 + __popc(peers & lt)] = k[j];
+            if (lane == 31u - __clz(peers)) *cp = p0 + __popc(peers);
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+}
+
 // Tile-local counting sort in SMEM, then per-digit contiguous writes.
-template <class Src>
-__global__ void __launch_bounds__(kTileThreads, 2) l1_scatter_kernel(Src src, size_t n, int shift,
-                                                                  unsigned dmask, uint32_t ntiles,
+// kStable: input order is kept among equal digits (stable_tile_scatter).
+template <class Src, bool kStable>
+__global__ void __launch_bounds__(kTileThreads, 2) l1_scatter_kernel(Src src, size_t n, int shift, int bits,
+                                                                  uint32_t ntiles,
                                                                   const uint32_t* __restrict__ off,
                                                                   uint64_t* __restrict__ out) {
     __shared__ uint32_t h[kRadix];
     __shared__ uint32_t lstart[kRadix];
     __shared__ uint64_t gbase[kRadix];
     __shared__ uint32_t scan_tmp[kTileThreads / 32 + 1];
-    extern __shared__ __align__(16) uint64_t skeys[];  // kTile keys, then Src scratch
+    extern __shared__ __align__(16) uint64_t skeys[];  // kTile keys, then Src scratch (+ stable counters)
     void* src_smem = skeys + kTile;
+    uint32_t* wc = reinterpret_cast<uint32_t*>(static_cast<unsigned char*>(src_smem) +
+                                               (Src::kSmem >= kStableScratch ? 0 : ((Src::kSmem + 15) & ~size_t(15))));
+    const unsigned dmask = (1u << bits) - 1u;
     for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        for (int i = threadIdx.x; i < kRadix; i += blockDim.x) h[i] = 0;
+        if (!kStable)
+            for (int i = threadIdx.x; i < kRadix; i += blockDim.x) h[i] = 0;
         const size_t base = (size_t)t * kTile;
         const int cnt = (int)min((size_t)kTile, n - base);
         src.prepare(base, cnt, src_smem);
@@ -88,14 +167,18 @@ __global__ void __launch_bounds__(kTileThreads, 2) l1_scatter_kernel(Src src, si
         uint64_t k[kTileItems];
 #pragma unroll
         for (int j = 0; j < kTileItems; ++j) {
-            int li = j * kTileThreads + threadIdx.x;
+            const int li = tile_pos<kStable>(j);
             if (li < cnt) {
                 k[j] = src.key(base + li, li, src_smem);
-                atomicAdd(&h[(unsigned)(k[j] >> shift) & dmask], 1u);
+                if (!kStable) atomicAdd(&h[(unsigned)(k[j] >> shift) & dmask], 1u);
             }
         }
         __syncthreads();
-        {
+        if (kStable) {
+            stable_tile_scatter(k, cnt, shift, bits, wc, lstart, scan_tmp, skeys);
+            if (threadIdx.x < kRadix) gbase[threadIdx.x] = off[(size_t)threadIdx.x * ntiles + t];
+            __syncthreads();
+        } else {
             uint32_t v = threadIdx.x < kRadix ? h[threadIdx.x] : 0u, tot;
             uint32_t ex = dev::block_excl_scan(v, scan_tmp, tot);
             if (threadIdx.x < kRadix) {
@@ -103,14 +186,14 @@ __global__ void __launch_bounds__(kTileThreads, 2) l1_scatter_kernel(Src src, si
                 h[threadIdx.x] = ex;  // becomes the per-digit cursor
                 gbase[threadIdx.x] = off[(size_t)threadIdx.x * ntiles + t];
             }
-        }
-        __syncthreads();
+            __syncthreads();
 #pragma unroll
-        for (int j = 0; j < kTileItems; ++j) {
-            int li = j * kTileThreads + threadIdx.x;
-            if (li < cnt) skeys[atomicAdd(&h[(unsigned)(k[j] >> shift) & dmask], 1u)] = k[j];
+            for (int j = 0; j < kTileItems; ++j) {
+                int li = j * kTileThreads + threadIdx.x;
+                if (li < cnt) skeys[atomicAdd(&h[(unsigned)(k[j] >> shift) & dmask], 1u)] = k[j];
+            }
+            __syncthreads();
         }
-        __syncthreads();
         for (int i = threadIdx.x; i < cnt; i += kTileThreads) {
             uint64_t key = skeys[i];
             unsigned d = (unsigned)(key >> shift) & dmask;
@@ -152,6 +235,7 @@ __global__ void __launch_bounds__(kTileThreads) seg_hist_kernel(
     const uint32_t* __restrict__ tile_seg, const uint32_t* __restrict__ tile_idx,
     const uint32_t* __restrict__ n_tiles, uint32_t* __restrict__ hist);
 
+template <bool kStable>
 __global__ void __launch_bounds__(kTileThreads, 2) seg_scatter_kernel(
     const uint64_t* __restrict__ keys0, const uint64_t* __restrict__ keys1,
     uint64_t* __restrict__ out0, uint64_t* __restrict__ out1, const Seg* __restrict__ active,
@@ -356,14 +440,16 @@ size_t local_smem_bytes();
 
 // Runs levels >= 2 until every segment is final; then the caller launches
 // local_sort_kernel with its Dst. `key_bits` is the number of significant bits.
-void run_segmented_levels(SortWorkspace& ws, int levels_left, int floor_bit, cudaStream_t s);
+void run_segmented_levels(SortWorkspace& ws, int levels_left, int floor_bit, bool stable, cudaStream_t s);
 
 // src_hist feeds the level-1 histogram pass and src_scat the level-1 scatter
 // pass; they must produce identical keys (K3 uses the split to capture its
 // exception list exactly once).
+// stable: keys equal above `payload_bits` keep their input order (every pass
+// is stable; the payload bits are never sorted).
 template <class Src, class Dst>
 void msd_sort_split(Src src_hist, Src src_scat, size_t n, int key_bits, Dst dst, SortWorkspace& ws,
-                    cudaStream_t s, const char* tag = "sort", int payload_bits = 0) {
+                    cudaStream_t s, const char* tag = "sort", int payload_bits = 0, bool stable = false) {
     const std::string t(tag);
     if (n == 0) return;
     sort_workspace_init(ws, n, s);
@@ -389,11 +475,20 @@ void msd_sort_split(Src src_hist, Src src_scat, size_t n, int key_bits, Dst dst,
     }
     {
         ProfScope prof(t + "_l1_scatter", s);
-        const size_t smem = (size_t)kTile * sizeof(uint64_t) + Src::kSmem;
-        PRG_CUDA(cudaFuncSetAttribute(l1_scatter_kernel<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
-        l1_scatter_kernel<Src><<<grid, kTileThreads, smem, s>>>(src_scat, n, shift1, dmask, ntiles,
-                                                                ws.off.get(), ws.keys[1].get());
+        if (stable) {
+            const size_t sx = Src::kSmem >= kStableScratch ? Src::kSmem : ((Src::kSmem + 15) & ~size_t(15)) + kStableScratch;
+            const size_t smem = (size_t)kTile * sizeof(uint64_t) + sx;
+            PRG_CUDA(cudaFuncSetAttribute(l1_scatter_kernel<Src, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem));
+            l1_scatter_kernel<Src, true><<<grid, kTileThreads, smem, s>>>(src_scat, n, shift1, bits1, ntiles,
+                                                                          ws.off.get(), ws.keys[1].get());
+        } else {
+            const size_t smem = (size_t)kTile * sizeof(uint64_t) + Src::kSmem;
+            PRG_CUDA(cudaFuncSetAttribute(l1_scatter_kernel<Src, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem));
+            l1_scatter_kernel<Src, false><<<grid, kTileThreads, smem, s>>>(src_scat, n, shift1, bits1, ntiles,
+                                                                           ws.off.get(), ws.keys[1].get());
+        }
         PRG_LAUNCH_CHECK();
         const int rem1 = shift1 - payload_bits;
         classify_l1_kernel<<<1, kRadix, 0, s>>>(ws.off.get(), ntiles, n, shift1, rem1 >= 8 ? 8 : rem1,
@@ -403,7 +498,7 @@ void msd_sort_split(Src src_hist, Src src_scat, size_t n, int key_bits, Dst dst,
     }
     {
         ProfScope prof(t + "_levels", s);
-        run_segmented_levels(ws, (shift1 - payload_bits + 7) / 8, payload_bits, s);
+        run_segmented_levels(ws, (shift1 - payload_bits + 7) / 8, payload_bits, stable, s);
     }
     {
         ProfScope prof(t + "_local", s);

@@ -91,6 +91,10 @@ void exclusive_scan_u32(const uint32_t* in, uint32_t* out, size_t n, uint32_t* t
                         cudaStream_t s);
 void exclusive_scan_u32_to_u64(const uint32_t* in, uint64_t* out, size_t n, uint64_t* total,
                                cudaStream_t s);
+// Exclusive scan of the used prefix in[0, min(cap, *d_count * mult)) of a
+// capacity-sized buffer (the count lives on the device; no host sync).
+void exclusive_scan_u32_prefix(const uint32_t* in, uint32_t* out, size_t cap, const uint32_t* d_count,
+                               uint32_t mult, cudaStream_t s);
 
 // Device error word: kernels that validate input OR a code in; the host reads it
 // back at the end of an entry point (one sync) and turns it into a status.

@@ -179,7 +179,7 @@ __global__ void perm_delta_kernel(const uint32_t* __restrict__ ro, const uint32_
 // Row minimum of the stored values -> bmin[u] (ordered u64 bit patterns;
 // values > 0). CSR-order tiles (coalesced), warp-segmented min per row, one
 // atomicMin per row segment.
-__global__ void __launch_bounds__(sort::kTileThreads, 2)
+__global__ void __launch_bounds__(sort::kTileThreads, 3)
     row_min_kernel(const uint32_t* __restrict__ ro, const uint32_t* __restrict__ tile_row,
                    const double* __restrict__ val, int64_t n, uint64_t nnz, unsigned long long* __restrict__ bmin) {
     extern __shared__ uint32_t srow[];
@@ -226,10 +226,9 @@ struct KeyBuildArgs {
     int sb;
     unsigned long long* keys;
     unsigned long long* exc_key;
-    double* exc_val;
     uint32_t* n_exc;
 };
-__global__ void __launch_bounds__(sort::kTileThreads, 2) key_build_kernel(KeyBuildArgs a) {
+__global__ void __launch_bounds__(sort::kTileThreads, 3) key_build_kernel(KeyBuildArgs a) {
     extern __shared__ uint32_t srow[];
     __shared__ uint32_t scan_tmp[sort::kTileThreads / 32 + 1];
     __shared__ uint32_t tile_base;
@@ -264,11 +263,8 @@ __global__ void __launch_bounds__(sort::kTileThreads, 2) key_build_kernel(KeyBui
             for (int j = 0; j < sort::kTileItems; ++j) {
                 if (!((excm >> j) & 1u)) continue;
                 const int li = j * sort::kTileThreads + threadIdx.x;
-                const uint32_t u = srow[rpad(li)];
                 const uint32_t e = (uint32_t)(base + li);
-                const uint32_t nid = a.newid ? a.newid[u] : u;
-                a.exc_key[idx] = ((uint64_t)a.cols[e] << (a.sb + 1)) | ((uint64_t)nid << 1) | 1u;
-                a.exc_val[idx] = a.val[e];
+                a.exc_key[idx] = ((uint64_t)a.cols[e] << 32) | e;
                 ++idx;
             }
         }
@@ -367,29 +363,35 @@ __global__ void suffix_min_down(uint32_t* a, int64_t n1, const uint32_t* part) {
     }
 }
 
-// Exceptions: locate each in the CSC (binary search inside its column), then
-// store its value at its rank among exception entries in CSC order.
-__global__ void place_exceptions(const unsigned long long* __restrict__ exc_key, const double* __restrict__ exc_v,
-                                 const uint32_t* __restrict__ n_exc, const uint32_t* __restrict__ colptr,
-                                 const uint32_t* __restrict__ csc_idx, const uint32_t* __restrict__ exc_base,
-                                 int sb, double* __restrict__ exc_val) {
-    const uint32_t ne = *n_exc;
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < ne; i += gridDim.x * blockDim.x) {
-        const uint64_t k = exc_key[i];
-        const uint32_t col = (uint32_t)(k >> (sb + 1));
-        const uint32_t nid = (uint32_t)((k >> 1) & ((1ull << sb) - 1));
-        uint32_t lo = colptr[col], hi = colptr[col + 1];
-        while (lo < hi) {
+// Exceptions (entries whose value differs from the row base, i.e. duplicate
+// edges) are captured as keys (col, CSR position). Sorted, they list every
+// column's exceptions contiguously, columns ascending, in CSR order inside a
+// column — which in parity mode (identity numbering) is exactly the CSC order.
+// In timed mode the SELL only needs "the k-th exception slot of column c" to
+// take one of column c's exceptions: the column sum is the same set of products.
+struct ExcValueDst {
+    const uint32_t* ro;       // CSR row offsets [n+1]
+    const uint32_t* tile_row; // row containing the first entry of each kTile tile
+    uint32_t ntiles;
+    const uint32_t* newid;    // null: identity
+    const double* values;
+    int64_t n;
+    uint32_t* e_u;    // new row id
+    double* e_val;    // value
+    __device__ __forceinline__ void store(uint64_t i, uint64_t key, bool, uint64_t) const {
+        const uint32_t e = (uint32_t)key;
+        // row u: the last row with ro[u] <= e (rows may be empty); it lies
+        // between the rows holding the first entries of e's tile and the next.
+        const uint32_t t = e / sort::kTile;
+        uint32_t lo = tile_row[t], hi = t + 1 < ntiles ? tile_row[t + 1] + 1 : (uint32_t)n;
+        while (hi - lo > 1) {
             const uint32_t mid = (lo + hi) >> 1;
-            if ((csc_idx[mid] & 0x7fffffffu) < nid) lo = mid + 1; else hi = mid;
+            if (ro[mid] <= e) lo = mid; else hi = mid;
         }
-        const uint32_t q = lo;
-        const uint32_t g0 = q & ~(uint32_t)(kCscGroup - 1);
-        uint32_t rank = exc_base[q / kCscGroup];
-        for (uint32_t p = g0; p < q; ++p) rank += csc_idx[p] >> 31;
-        exc_val[rank] = exc_v[i];
+        e_u[i] = newid ? newid[lo] : lo;
+        e_val[i] = values[e];
     }
-}
+};
 
 // ---------------------------------------------------------------------------
 // init_rank (kernel3_pagerank.cpp:29-39)
@@ -560,16 +562,20 @@ struct FillArgs {
     const uint32_t* vc_base;
     const uint32_t* colptr;
     const uint32_t* csc_idx;
+    const uint32_t* exc_base;  // CSC groups of kCscGroup: exception rank at the group start
     const uint32_t* slice_ptr;
     uint32_t V, nslices;
+    uint32_t n_nd;             // exception entries gather s[n_nd + CSC exception rank]
     uint32_t* sell;
-    uint32_t* exc_cnt;   // per SELL group of 32
     uint32_t* lane_len;  // [nslices*32]
     uint32_t* lane_col;  // [nslices*32]
     uint32_t* lane_np;   // [nslices*32]
     uint32_t* spos_col;  // [n] pos of part 0 (kEmpty if empty)
 };
 
+// One warp per slice, lane = virtual column. Exception entries (value != row
+// base, flagged in the CSC) are redirected to s[n_nd + rank], where the
+// exception products are stored every iteration — the SpMV has no special case.
 __global__ void sell_fill_kernel(FillArgs a) {
     const uint32_t lane = dev::lane_id();
     for (uint32_t s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < a.nslices; s += (gridDim.x * blockDim.x) >> 5) {
@@ -587,69 +593,32 @@ __global__ void sell_fill_kernel(FillArgs a) {
         a.lane_len[pos] = len;
         a.lane_col[pos] = c;
         a.lane_np[pos] = np;
+        // exception rank at `start`
+        uint32_t er = 0;
+        if (len) {
+            const uint32_t g0 = start & ~(uint32_t)(kCscGroup - 1);
+            er = a.exc_base[start / kCscGroup];
+            for (uint32_t q = g0; q < start; ++q) er += a.csc_idx[q] >> 31;
+        }
         const uint32_t base = a.slice_ptr[s];
         const uint32_t rows = (a.slice_ptr[s + 1] - base) >> 5;
-        for (uint32_t k = 0; k < rows; ++k) {
-            const bool ok = k < len;
-            const uint32_t e = ok ? a.csc_idx[start + k] : 0u;
-            a.sell[base + 32 * k + lane] = e;
-            const uint32_t m = __ballot_sync(0xffffffffu, ok && (e >> 31));
-            if (lane == 0) a.exc_cnt[(base >> 5) + k] = __popc(m);
+        const uint32_t* src = a.csc_idx + start;
+        uint32_t* dst = a.sell + base + lane;
+        for (uint32_t k0 = 0; k0 < rows; k0 += 8) {
+            uint32_t e[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) e[u] = k0 + u < len ? src[k0 + u] : 0x80000000u;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                if (k0 + u < rows) {
+                    uint32_t w = e[u];
+                    if (k0 + u < len && (w >> 31)) w = a.n_nd + er++;
+                    dst[32 * (k0 + u)] = w;
+                }
+            }
         }
     }
 }
-
-// Exceptions (entries whose value differs from the row base value, i.e.
-// duplicate edges) are summed per virtual column by a small kernel each
-// iteration, in a fixed order, and added once per column by the SpMV.
-// Prep: key (SELL lane position, source row) for every exception, sorted.
-__global__ void exc_pos_keys(const unsigned long long* __restrict__ exc_key, const uint32_t* __restrict__ n_exc,
-                             const uint32_t* __restrict__ colptr, const uint32_t* __restrict__ csc_idx,
-                             const uint32_t* __restrict__ vc_base, const uint32_t* __restrict__ vpos, int sb,
-                             unsigned long long* __restrict__ out) {
-    const uint32_t ne = *n_exc;
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < ne; i += gridDim.x * blockDim.x) {
-        const uint64_t key = exc_key[i];
-        const uint32_t col = (uint32_t)(key >> (sb + 1));
-        const uint32_t nid = (uint32_t)((key >> 1) & ((1ull << sb) - 1));
-        uint32_t lo = colptr[col], hi = colptr[col + 1];
-        while (lo < hi) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if ((csc_idx[mid] & 0x7fffffffu) < nid) lo = mid + 1; else hi = mid;
-        }
-        const uint32_t pos = vpos[vc_base[col] + (lo - colptr[col]) / kVcMax];
-        out[i] = ((uint64_t)pos << 32) | nid;
-    }
-}
-
-// For sorted exception i: source row, value (from the CSC-order exception
-// values), and its lane position; flags lanes that have exceptions.
-struct ExcResolveDst {
-    const uint32_t* lane_col;
-    const uint32_t* colptr;
-    const uint32_t* csc_idx;
-    const uint32_t* exc_base;  // CSC groups
-    const double* exc_val_csc;
-    uint32_t* e_pos;
-    uint32_t* e_u;
-    double* e_val;
-    uint32_t* lane_flags;
-    __device__ __forceinline__ void store(uint64_t i, uint64_t key, bool, uint64_t) const {
-        const uint32_t pos = (uint32_t)(key >> 32), u = (uint32_t)key;
-        const uint32_t col = lane_col[pos];
-        uint32_t lo = colptr[col], hi = colptr[col + 1];
-        while (lo < hi) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if ((csc_idx[mid] & 0x7fffffffu) < u) lo = mid + 1; else hi = mid;
-        }
-        uint32_t rank = exc_base[lo / kCscGroup];
-        for (uint32_t q = lo & ~(uint32_t)(kCscGroup - 1); q < lo; ++q) rank += csc_idx[q] >> 31;
-        e_pos[i] = pos;
-        e_u[i] = u;
-        e_val[i] = exc_val_csc[rank];
-        lane_flags[pos] = 1u;
-    }
-};
 
 __global__ void spos_rows_kernel(const uint32_t* __restrict__ pinv, const uint32_t* __restrict__ spos_col,
                                  int64_t n_nd, uint32_t* __restrict__ spos) {
@@ -695,12 +664,9 @@ struct SellArgs {
     const uint32_t* lane_len;
     const uint32_t* lane_col;
     const uint32_t* lane_np;
-    const uint32_t* lane_eptr;   // first exception of the lane (sorted order)
-    const uint32_t* lane_ecnt;   // number of exceptions of the lane
     const uint32_t* vc_base;
     const uint32_t* vpos;
-    const double* exc_x;         // per exception products of this iteration
-    const double* s;             // gather vector [n_nd]
+    const double* s;             // gather vector [n_nd + n_exc]
     double* y;                   // [nslices*32]
     double* partial;             // [nslices*32]
     uint32_t* arrive;            // [n] per split column, never reset
@@ -711,9 +677,8 @@ struct SellArgs {
     double damping;
 };
 
-// Exception products for this iteration: exc_x[j] = r_prev(u_j) * value_j
-// (exceptions sorted by (lane position, source row)); each SpMV lane folds its
-// contiguous run [lane_eptr, lane_eptr + lane_ecnt) into its own sum.
+// Exception products for this iteration: exc_x[j] = r_prev(u_j) * value_j for
+// the CSC-ordered exception j; the SELL entry of that exception gathers it.
 struct ExcArgs {
     const uint32_t* e_u;
     const double* e_val;
@@ -737,21 +702,6 @@ __global__ void exc_products_kernel(ExcArgs a) {
         a.exc_x[j] = __dmul_rn(r, a.e_val[j]);
     }
 }
-__global__ void exc_ranges_kernel(const uint32_t* __restrict__ e_pos, uint32_t ne, uint32_t* __restrict__ eptr,
-                                  uint32_t* __restrict__ ecnt) {
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < ne; i += gridDim.x * blockDim.x) {
-        const uint32_t pos = e_pos[i];
-        if (i == 0 || e_pos[i - 1] != pos) eptr[pos] = i;
-        if (i + 1 == ne || e_pos[i + 1] != pos) {
-            // run end: count = i - start + 1; start found by the head thread, so
-            // recompute it by walking back (runs are bounded by kVcMax)
-            uint32_t st = i;
-            while (st > 0 && e_pos[st - 1] == pos) --st;
-            ecnt[pos] = i - st + 1;
-        }
-    }
-}
-
 // 64 warps per SM and no shared-memory staging: measured on B200 (S=24) the L1
 // caches the hot, degree-ordered head of s by itself, and occupancy (requests
 // in flight) matters more than a software-managed hot set (1.9 ms vs 3.3 ms).
@@ -785,20 +735,6 @@ __global__ void __launch_bounds__(kSpmvThreads, 2) spmv_sell_kernel(SellArgs a) 
                 w[u] = dev::ld_stream_u32_pred(col + 32 * (k1 + u), k1 + u < len, pol_stream, 0x80000000u);
 #pragma unroll
             for (int u = 0; u < U; ++u) acc = __dadd_rn(acc, x[u]);
-        }
-        // duplicate-edge exceptions of this lane (products precomputed this iteration)
-        const uint32_t ecnt = a.lane_ecnt[pos];
-        if (__any_sync(0xffffffffu, ecnt != 0)) {
-            const double* ex = a.exc_x + (ecnt ? a.lane_eptr[pos] : 0u);
-            double eacc = 0.0;
-            for (uint32_t j0 = 0; j0 < ecnt; j0 += 8) {
-                double xe[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) xe[u] = dev::ld_f64_pred(ex + j0 + u, j0 + u < ecnt);
-#pragma unroll
-                for (int u = 0; u < 8; ++u) eacc = __dadd_rn(eacc, xe[u]);
-            }
-            acc = __dadd_rn(acc, eacc);
         }
         const uint32_t np = a.lane_np[pos];
         double yv = 0.0;
@@ -869,9 +805,9 @@ struct K3Plan {
     uint32_t n_exc = 0;
     // timed mode (SELL)
     uint32_t V = 0, nslices = 0, n_empty = 0;
-    DevBuf<uint32_t> sell, slice_ptr, lane_len, lane_col, lane_np, lane_flags, lane_eptr, lane_ecnt, vc_base, vpos,
-        spos, spos_col, split_pos, n_split, arrive, e_pos, e_u;
-    DevBuf<double> e_val, partial;
+    DevBuf<uint32_t> sell, slice_ptr, lane_len, lane_col, lane_np, vc_base, vpos, spos, spos_col, split_pos, n_split,
+        arrive, e_u;  // e_u: new row of CSC-ordered exception i (values in exc_val)
+    DevBuf<double> partial;
 };
 
 void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
@@ -896,7 +832,8 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
             PRG_LAUNCH_CHECK();
             sort::SortWorkspace ws;
             sort::msd_sort(RowClassSrc{A->row_offsets, P.sb}, (size_t)n, P.sb + 8,
-                           PermDst{P.pinv.get(), P.newid.get(), P.sb}, ws, s, "k3rows");
+                           PermDst{P.pinv.get(), P.newid.get(), P.sb}, ws, s, "k3rows", /*payload_bits=*/P.sb,
+                           /*stable=*/true);
             unsigned long long h = 0;
             PRG_CUDA(cudaMemcpyAsync(&h, cnt.get(), 8, cudaMemcpyDeviceToHost, s));
             PRG_CUDA(cudaStreamSynchronize(s));
@@ -930,7 +867,7 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
         if (nnz) {
             tile_rows_kernel<<<g, 1024, 0, s>>>(A->row_offsets, n, tile_row.get());
             PRG_LAUNCH_CHECK();
-            row_min_kernel<<<num_sms() * 2, sort::kTileThreads, row_smem, s>>>(A->row_offsets, tile_row.get(),
+            row_min_kernel<<<num_sms() * 3, sort::kTileThreads, row_smem, s>>>(A->row_offsets, tile_row.get(),
                                                                               A->values, n, nnz, bmin.get());
             PRG_LAUNCH_CHECK();
         }
@@ -944,7 +881,6 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
     const uint64_t ngroups = nnz / kCscGroup + 1;
     DevBuf<uint32_t> exc_cnt(ngroups, s);
     DevBuf<unsigned long long> exc_key(nnz ? nnz : 1, s);
-    DevBuf<double> exc_v(nnz ? nnz : 1, s);
     DevBuf<uint32_t> n_exc(1, s);
     {
         ProfScope pr("k3_prep_transpose", s);
@@ -958,9 +894,8 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
                 ProfScope pk("k3t_keys", s);
                 KeyBuildArgs ka{A->row_offsets, tile_row.get(), A->cols, A->values, bmin.get(),
                                 mode == 0 ? P.newid.get() : nullptr, mode == 0 ? wdelta.get() : nullptr, n, nnz, P.sb,
-                                reinterpret_cast<unsigned long long*>(ws.keys[0].get()), exc_key.get(), exc_v.get(),
-                                n_exc.get()};
-                key_build_kernel<<<num_sms() * 2, sort::kTileThreads, row_smem, s>>>(ka);
+                                reinterpret_cast<unsigned long long*>(ws.keys[0].get()), exc_key.get(), n_exc.get()};
+                key_build_kernel<<<num_sms() * 3, sort::kTileThreads, row_smem, s>>>(ka);
                 PRG_LAUNCH_CHECK();
             }
             // the keys live in ws.keys[0]; level 1 reads them before any pass overwrites that buffer.
@@ -990,10 +925,13 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
         PRG_CUDA(cudaStreamSynchronize(s));
     }
     P.exc_val = DevBuf<double>(P.n_exc ? P.n_exc : 1, s);
+    P.e_u = DevBuf<uint32_t>(P.n_exc ? P.n_exc : 1, s);
     if (P.n_exc) {
-        place_exceptions<<<g, 256, 0, s>>>(exc_key.get(), exc_v.get(), n_exc.get(), P.colptr.get(),
-                                           P.csc_idx.get(), P.exc_base.get(), P.sb, P.exc_val.get());
-        PRG_LAUNCH_CHECK();
+        sort::SortWorkspace ws;
+        sort::msd_sort(KeyArraySrc{exc_key.get()}, (size_t)P.n_exc, 32 + P.sb,
+                       ExcValueDst{A->row_offsets, tile_row.get(), ntiles, mode == 0 ? P.newid.get() : nullptr,
+                                   A->values, n, P.e_u.get(), P.exc_val.get()},
+                       ws, s, "k3exc");
     }
     if (mode == 1) return;
     // 4. SELL over virtual columns
@@ -1015,7 +953,8 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
     if (V) {
         sort::SortWorkspace ws;
         const int vb = bits_for(V);
-        sort::msd_sort(VcClassSrc{vc_len.get(), vb}, (size_t)V, vb + 8, PermDst{order.get(), P.vpos.get(), vb}, ws, s, "k3vc");
+        sort::msd_sort(VcClassSrc{vc_len.get(), vb}, (size_t)V, vb + 8, PermDst{order.get(), P.vpos.get(), vb}, ws, s,
+                       "k3vc", /*payload_bits=*/vb, /*stable=*/true);
     }
     DevBuf<uint32_t> slice_sz(P.nslices ? P.nslices : 1, s);
     P.slice_ptr = DevBuf<uint32_t>((size_t)P.nslices + 1, s);
@@ -1028,43 +967,17 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
     PRG_CUDA(cudaMemcpyAsync(&sell_n, P.slice_ptr.get() + P.nslices, 4, cudaMemcpyDeviceToHost, s));
     PRG_CUDA(cudaStreamSynchronize(s));
     P.sell = DevBuf<uint32_t>(sell_n ? sell_n : 1, s);
-    const uint32_t sgroups = sell_n / 32 + 1;
-    DevBuf<uint32_t> sexc_cnt(sgroups, s);  // (unused by the SpMV; kept for the fill kernel)
-    PRG_CUDA(cudaMemsetAsync(sexc_cnt.get(), 0, (size_t)sgroups * 4, s));
     P.lane_len = DevBuf<uint32_t>(NP ? NP : 1, s);
     P.lane_col = DevBuf<uint32_t>(NP ? NP : 1, s);
     P.lane_np = DevBuf<uint32_t>(NP ? NP : 1, s);
     P.spos_col = DevBuf<uint32_t>((size_t)n, s);
     PRG_CUDA(cudaMemsetAsync(P.spos_col.get(), 0xff, (size_t)n * 4, s));
     if (P.nslices) {
-        FillArgs fa{order.get(), vc_col.get(), vc_len.get(), P.vc_base.get(), P.colptr.get(), P.csc_idx.get(),
-                    P.slice_ptr.get(), V, P.nslices, P.sell.get(), sexc_cnt.get(), P.lane_len.get(),
-                    P.lane_col.get(), P.lane_np.get(), P.spos_col.get()};
+        FillArgs fa{order.get(),         vc_col.get(),     vc_len.get(), P.vc_base.get(),   P.colptr.get(),
+                    P.csc_idx.get(),     P.exc_base.get(), P.slice_ptr.get(), V,                P.nslices,
+                    (uint32_t)P.n_nd,    P.sell.get(),     P.lane_len.get(),  P.lane_col.get(), P.lane_np.get(),
+                    P.spos_col.get()};
         sell_fill_kernel<<<g, 256, 0, s>>>(fa);
-        PRG_LAUNCH_CHECK();
-    }
-    // exceptions grouped by lane position (sorted by (pos, source row))
-    P.lane_flags = DevBuf<uint32_t>(NP ? NP : 1, s);
-    PRG_CUDA(cudaMemsetAsync(P.lane_flags.get(), 0, (size_t)(NP ? NP : 1) * 4, s));
-    P.e_pos = DevBuf<uint32_t>(P.n_exc ? P.n_exc : 1, s);
-    P.e_u = DevBuf<uint32_t>(P.n_exc ? P.n_exc : 1, s);
-    P.e_val = DevBuf<double>(P.n_exc ? P.n_exc : 1, s);
-    if (P.n_exc) {
-        DevBuf<unsigned long long> ek(P.n_exc, s);
-        exc_pos_keys<<<g, 256, 0, s>>>(exc_key.get(), n_exc.get(), P.colptr.get(), P.csc_idx.get(), P.vc_base.get(),
-                                       P.vpos.get(), P.sb, ek.get());
-        PRG_LAUNCH_CHECK();
-        sort::SortWorkspace ws;
-        sort::msd_sort(KeyArraySrc{ek.get()}, (size_t)P.n_exc, 32 + bits_for(NP),
-                       ExcResolveDst{P.lane_col.get(), P.colptr.get(), P.csc_idx.get(), P.exc_base.get(),
-                                     P.exc_val.get(), P.e_pos.get(), P.e_u.get(), P.e_val.get(), P.lane_flags.get()},
-                       ws, s, "k3exc");
-    }
-    P.lane_eptr = DevBuf<uint32_t>(NP ? NP : 1, s);
-    P.lane_ecnt = DevBuf<uint32_t>(NP ? NP : 1, s);
-    PRG_CUDA(cudaMemsetAsync(P.lane_ecnt.get(), 0, (size_t)(NP ? NP : 1) * 4, s));
-    if (P.n_exc) {
-        exc_ranges_kernel<<<g, 256, 0, s>>>(P.e_pos.get(), P.n_exc, P.lane_eptr.get(), P.lane_ecnt.get());
         PRG_LAUNCH_CHECK();
     }
     P.spos = DevBuf<uint32_t>((size_t)std::max<int64_t>(P.n_nd, 1), s);
@@ -1173,8 +1086,9 @@ void iterate(const K3Plan& P, const double* r_in, double* r_out, int iters, doub
 
     }
     const uint32_t NP = P.nslices * 32;
-    DevBuf<double> sbuf((size_t)std::max<int64_t>(P.n_nd, 1), s), y0(NP ? NP : 1, s), y1(NP ? NP : 1, s),
-        slice_sum(P.nslices ? P.nslices : 1, s), exc_x(P.n_exc ? P.n_exc : 1, s);
+    // s = [row-scaled iterate (SELL row order, n_nd) | exception products (n_exc)]
+    DevBuf<double> sbuf((size_t)std::max<int64_t>(P.n_nd + P.n_exc, 1), s), y0(NP ? NP : 1, s), y1(NP ? NP : 1, s),
+        slice_sum(P.nslices ? P.nslices : 1, s);
     double* ys[2] = {y0.get(), y1.get()};
     for (int it = 0; it < iters; ++it) {
         double* y = ys[it & 1];
@@ -1186,8 +1100,8 @@ void iterate(const K3Plan& P, const double* r_in, double* r_out, int iters, doub
             PRG_LAUNCH_CHECK();
         }
         if (P.n_exc) {
-            ExcArgs ea{P.e_u.get(), P.e_val.get(), P.n_exc, it == 0 ? r_in : nullptr, P.pinv.get(), P.spos.get(), yp,
-                       S.out.get(), exc_x.get()};
+            ExcArgs ea{P.e_u.get(), P.exc_val.get(), P.n_exc, it == 0 ? r_in : nullptr, P.pinv.get(), P.spos.get(), yp,
+                       S.out.get(), sbuf.get() + P.n_nd};
             exc_products_kernel<<<g, 256, 0, s>>>(ea);
             PRG_LAUNCH_CHECK();
         }
@@ -1197,11 +1111,8 @@ void iterate(const K3Plan& P, const double* r_in, double* r_out, int iters, doub
         a.lane_len = P.lane_len.get();
         a.lane_col = P.lane_col.get();
         a.lane_np = P.lane_np.get();
-        a.lane_eptr = P.lane_eptr.get();
-        a.lane_ecnt = P.lane_ecnt.get();
         a.vc_base = P.vc_base.get();
         a.vpos = P.vpos.get();
-        a.exc_x = exc_x.get();
         a.s = sbuf.get();
         a.y = y;
         a.partial = P.partial.get();

@@ -106,11 +106,19 @@ constexpr int kScanThreads = 1024;
 constexpr int kScanItems = 8;
 constexpr int kScanTile = kScanThreads * kScanItems;
 
+// dn (optional): the scan covers only the first min(n, *dn * mult) items — the
+// used prefix of a capacity-sized buffer whose size is known only on the device.
+__device__ __forceinline__ size_t scan_len(size_t n, const uint32_t* dn, uint32_t mult) {
+    return dn ? min(n, (size_t)*dn * mult) : n;
+}
+
 __global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(const uint32_t* __restrict__ in,
-                                                                   size_t n,
+                                                                   size_t n, const uint32_t* dn, uint32_t mult,
                                                                    uint64_t* __restrict__ partial) {
     __shared__ uint64_t red[32];
+    n = scan_len(n, dn, mult);
     const size_t base = (size_t)blockIdx.x * kScanTile;
+    if (base >= n && blockIdx.x > 0) return;
     uint64_t s = 0;
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
@@ -129,9 +137,10 @@ __global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(const uint32_
 
 // Single-block exclusive scan over `n` u64 values (in place); total -> *total.
 __global__ void __launch_bounds__(kScanThreads) scan_partials_kernel(uint64_t* __restrict__ p,
-                                                                     size_t n) {
+                                                                     size_t n, const uint32_t* dn, uint32_t mult) {
     __shared__ uint64_t warp_tot[33];
     __shared__ uint64_t carry;
+    if (dn) n = min(n, (scan_len(~size_t(0), dn, mult) + kScanTile - 1) / kScanTile);
     if (threadIdx.x == 0) carry = 0;
     __syncthreads();
     for (size_t base = 0; base < n; base += kScanThreads) {
@@ -158,11 +167,13 @@ __global__ void __launch_bounds__(kScanThreads) scan_partials_kernel(uint64_t* _
 
 template <class Out>
 __global__ void __launch_bounds__(kScanThreads) scan_down_kernel(const uint32_t* __restrict__ in,
-                                                                 size_t n,
+                                                                 size_t n, const uint32_t* dn, uint32_t mult,
                                                                  const uint64_t* __restrict__ partial,
                                                                  Out* __restrict__ out) {
     __shared__ uint64_t warp_tot[33];
+    n = scan_len(n, dn, mult);
     const size_t base = (size_t)blockIdx.x * kScanTile;
+    if (base >= n) return;
     // Blocked arrangement: thread t owns items [base + t*8, base + t*8 + 8).
     uint32_t v[kScanItems];
     const size_t my = base + (size_t)threadIdx.x * kScanItems;
@@ -194,17 +205,18 @@ __global__ void copy_total_kernel(const uint64_t* partial, size_t nb, Out* total
 }
 
 template <class Out>
-void scan_impl(const uint32_t* in, Out* out, size_t n, Out* total, cudaStream_t s) {
+void scan_impl(const uint32_t* in, Out* out, size_t n, Out* total, cudaStream_t s, const uint32_t* dn = nullptr,
+               uint32_t mult = 1) {
     const size_t nb = n ? (n + kScanTile - 1) / kScanTile : 0;
     DevBuf<uint64_t> part(nb + 1, s);
     if (nb) {
-        scan_reduce_kernel<<<(unsigned)nb, kScanThreads, 0, s>>>(in, n, part.get());
+        scan_reduce_kernel<<<(unsigned)nb, kScanThreads, 0, s>>>(in, n, dn, mult, part.get());
         PRG_LAUNCH_CHECK();
     }
-    scan_partials_kernel<<<1, kScanThreads, 0, s>>>(part.get(), nb);
+    scan_partials_kernel<<<1, kScanThreads, 0, s>>>(part.get(), nb, dn, mult);
     PRG_LAUNCH_CHECK();
     if (nb) {
-        scan_down_kernel<Out><<<(unsigned)nb, kScanThreads, 0, s>>>(in, n, part.get(), out);
+        scan_down_kernel<Out><<<(unsigned)nb, kScanThreads, 0, s>>>(in, n, dn, mult, part.get(), out);
         PRG_LAUNCH_CHECK();
     }
     if (total) {
@@ -221,6 +233,10 @@ void exclusive_scan_u32(const uint32_t* in, uint32_t* out, size_t n, uint32_t* t
 void exclusive_scan_u32_to_u64(const uint32_t* in, uint64_t* out, size_t n, uint64_t* total,
                                cudaStream_t s) {
     scan_impl<uint64_t>(in, out, n, total, s);
+}
+void exclusive_scan_u32_prefix(const uint32_t* in, uint32_t* out, size_t cap, const uint32_t* d_count,
+                               uint32_t mult, cudaStream_t s) {
+    scan_impl<uint32_t>(in, out, cap, nullptr, s, d_count, mult);
 }
 
 }  // namespace prg

@@ -33,8 +33,21 @@ __device__ void emit_children(const uint64_t* child_start, const uint32_t* child
             c.buf = buf;
             c.bits = (uint8_t)next_bits;
             c.shift = (uint16_t)next_shift;
-            if (next_bits == 0) fin[atomicAdd(n_fin, 1u)] = c;
-            else next[atomicAdd(n_next, 1u)] = c;
+            if (next_bits == 0) {
+                // no bits left: the keys are equal above the payload, so the
+                // child is already in order — hand it out in cap-sized pieces
+                // so no single CTA streams a huge run.
+                const uint32_t np = (sz + kLocalCap - 1) / kLocalCap;
+                const uint32_t f0 = atomicAdd(n_fin, np);  // one reservation, plain stores
+                for (uint32_t q = 0; q < np; ++q) {
+                    Seg p = c;
+                    p.start = c.start + (uint64_t)q * kLocalCap;
+                    p.size = min((uint32_t)kLocalCap, sz - q * (uint32_t)kLocalCap);
+                    fin[f0 + q] = p;
+                }
+            } else {
+                next[atomicAdd(n_next, 1u)] = c;
+            }
             continue;
         }
         if (run.size && run.size + sz > (uint32_t)kLocalCap) { fin[atomicAdd(n_fin, 1u)] = run; run.size = 0; }
@@ -179,11 +192,10 @@ __global__ void __launch_bounds__(kTileThreads, 2) seg_scatter_kernel(
         }
         const size_t hb = (size_t)seg_tile0[si] * kRadix;
         if (kStable) {
-            stable_tile_scatter(k, cnt, sg.shift, sg.bits, wc, lstart, scan_tmp, skeys);
             // off is relative to the concatenation of active segments
             if (threadIdx.x < kRadix)
                 gbase[threadIdx.x] = sg.start + (off[hb + (size_t)threadIdx.x * seg_nt + ti] - e0);
-            __syncthreads();
+            stable_tile_scatter(k, cnt, sg.shift, sg.bits, wc, lstart, scan_tmp, skeys);
         } else {
             __syncthreads();
             uint32_t v = threadIdx.x < kRadix ? h[threadIdx.x] : 0u, tot;
@@ -291,15 +303,14 @@ void run_segmented_levels(SortWorkspace& ws, int levels_left, int floor_bit, boo
                                               ws.tile_seg.get(), ws.tile_idx.get(), cnt + 4,
                                               ws.max_tiles);
         PRG_LAUNCH_CHECK();
-        // Tiles beyond n_tiles are never read; only the used prefix of hist
-        // matters, but the scan runs over the capacity, so clear it.
+        // Only the used prefix (n_tiles x kRadix, every entry written by
+        // seg_hist) is scanned; the count stays on the device.
         const size_t hsz = (size_t)kRadix * ws.max_tiles;
-        PRG_CUDA(cudaMemsetAsync(ws.hist.get(), 0, hsz * sizeof(uint32_t), s));
         seg_hist_kernel<<<grid, kTileThreads, 0, s>>>(ws.keys[0].get(), ws.keys[1].get(), act,
                                                       ws.seg_tile0.get(), ws.tile_seg.get(),
                                                       ws.tile_idx.get(), cnt + 4, ws.hist.get());
         PRG_LAUNCH_CHECK();
-        exclusive_scan_u32(ws.hist.get(), ws.off.get(), hsz, nullptr, s);
+        exclusive_scan_u32_prefix(ws.hist.get(), ws.off.get(), hsz, cnt + 4, kRadix, s);
         if (stable)
             seg_scatter_kernel<true><<<grid, kTileThreads, smem, s>>>(
                 ws.keys[0].get(), ws.keys[1].get(), ws.keys[0].get(), ws.keys[1].get(), act,

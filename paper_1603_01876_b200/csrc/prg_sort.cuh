@@ -95,30 +95,14 @@ __device__ __forceinline__ void stable_tile_scatter(const uint64_t (&k)[kTileIte
     const unsigned w = dev::warp_id(), lane = dev::lane_id();
     const unsigned mask = (1u << bits) - 1u;
     const unsigned t = threadIdx.x;
+    const unsigned lt = (1u << lane) - 1u;
     reinterpret_cast<uint4*>(wc)[2 * t] = make_uint4(0, 0, 0, 0);
     reinterpret_cast<uint4*>(wc)[2 * t + 1] = make_uint4(0, 0, 0, 0);
     __syncthreads();
-#pragma unroll
-    for (int j = 0; j < kTileItems; ++j) {
-        if (tile_pos<true>(j) < cnt) atomicAdd(&wc[((unsigned)(k[j] >> shift) & mask) * kTileWarps + w], 1u);
-    }
-    __syncthreads();
-    {   // exclusive scan over (digit, warp); thread t owns digit t/2, warps 8*(t&1)..+7
-        uint4 a = reinterpret_cast<uint4*>(wc)[2 * t], b = reinterpret_cast<uint4*>(wc)[2 * t + 1];
-        const uint32_t sum = a.x + a.y + a.z + a.w + b.x + b.y + b.z + b.w;
-        uint32_t tot;
-        uint32_t run = dev::block_excl_scan(sum, scan_tmp, tot);
-        if ((t & 1u) == 0) lstart[t >> 1] = run;
-        uint32_t v;
-        v = a.x; a.x = run; run += v;  v = a.y; a.y = run; run += v;
-        v = a.z; a.z = run; run += v;  v = a.w; a.w = run; run += v;
-        v = b.x; b.x = run; run += v;  v = b.y; b.y = run; run += v;
-        v = b.z; b.z = run; run += v;  v = b.w; b.w = run;
-        reinterpret_cast<uint4*>(wc)[2 * t] = a;
-        reinterpret_cast<uint4*>(wc)[2 * t + 1] = b;
-    }
-    __syncthreads();
-    const unsigned lt = (1u << lane) - 1u;
+    // Rank within the warp's chunk: peers (same digit, same row j) by ballots;
+    // the highest peer advances the warp's running digit count (no atomics, so
+    // skewed digits do not serialise). rk packs two 16-bit ranks per word.
+    uint32_t rk[kTileItems / 2];
 #pragma unroll
     for (int j = 0; j < kTileItems; ++j) {
         const bool valid = tile_pos<true>(j) < cnt;
@@ -129,14 +113,39 @@ __device__ __forceinline__ void stable_tile_scatter(const uint64_t (&k)[kTileIte
             const unsigned bal = __ballot_sync(0xffffffffu, bit);
             peers &= bit ? bal : ~bal;
         }
-        uint32_t* cp = &wc[d * kTileWarps + w];
-        const uint32_t p0 = valid ? *cp : 0u;
+        uint32_t* cp = &wc[w * kRadix + d];  // [warp][digit]: lanes of a warp hit distinct banks
+        const uint32_t r = (valid ? *cp : 0u) + __popc(peers & lt);
         __syncwarp();
-        if (valid) {
-            skeys[p0 + __popc(peers & lt)] = k[j];
-            if (lane == 31u - __clz(peers)) *cp = p0 + __popc(peers);
+        if (valid && lane == 31u - __clz(peers)) *cp = r + 1u;
+        __syncwarp();
+        if (j & 1) rk[j >> 1] |= r << 16; else rk[j >> 1] = r;
+    }
+    __syncthreads();
+    {   // exclusive scan in (digit, warp) order; thread t owns digit t/2, warps 8*(t&1)..+7
+        const unsigned d = t >> 1, w0 = (t & 1u) * 8u;
+        uint32_t v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = wc[(w0 + q) * kRadix + d];
+        uint32_t sum = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) sum += v[q];
+        uint32_t tot;
+        uint32_t run = dev::block_excl_scan(sum, scan_tmp, tot);
+        if ((t & 1u) == 0) lstart[d] = run;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            wc[(w0 + q) * kRadix + d] = run;
+            run += v[q];
         }
-        __syncwarp();
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kTileItems; ++j) {
+        if (tile_pos<true>(j) < cnt) {
+            const unsigned d = (unsigned)(k[j] >> shift) & mask;
+            const uint32_t r = (rk[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
+            skeys[wc[w * kRadix + d] + r] = k[j];
+        }
     }
     __syncthreads();
 }
@@ -175,9 +184,8 @@ __global__ void __launch_bounds__(kTileThreads, 2) l1_scatter_kernel(Src src, si
         }
         __syncthreads();
         if (kStable) {
-            stable_tile_scatter(k, cnt, shift, bits, wc, lstart, scan_tmp, skeys);
             if (threadIdx.x < kRadix) gbase[threadIdx.x] = off[(size_t)threadIdx.x * ntiles + t];
-            __syncthreads();
+            stable_tile_scatter(k, cnt, shift, bits, wc, lstart, scan_tmp, skeys);  // ends with a barrier
         } else {
             uint32_t v = threadIdx.x < kRadix ? h[threadIdx.x] : 0u, tot;
             uint32_t ex = dev::block_excl_scan(v, scan_tmp, tot);
@@ -513,8 +521,8 @@ void msd_sort_split(Src src_hist, Src src_scat, size_t n, int key_bits, Dst dst,
 
 template <class Src, class Dst>
 void msd_sort(Src src, size_t n, int key_bits, Dst dst, SortWorkspace& ws, cudaStream_t s,
-              const char* tag = "sort") {
-    msd_sort_split(src, src, n, key_bits, dst, ws, s, tag);
+              const char* tag = "sort", int payload_bits = 0, bool stable = false) {
+    msd_sort_split(src, src, n, key_bits, dst, ws, s, tag, payload_bits, stable);
 }
 
 }  // namespace prg::sort

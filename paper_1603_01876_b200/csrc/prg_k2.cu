@@ -27,16 +27,22 @@ constexpr int kT = 1024;        // threads per CTA
 constexpr int kI = 8;           // edges per thread
 constexpr int kTE = kT * kI;    // edges per tile
 
+// SMEM arrays indexed by tile position are padded one word per 32: the
+// blocked per-thread view (thread t reads positions 8t..8t+7) is then free of
+// bank conflicts (ncu: 8-way before).
+__device__ __forceinline__ int sp(int l) { return l + (l >> 5); }
+constexpr int kTEP = kTE + kTE / 32;
+
 struct EdgeSmem {
-    uint32_t su[kTE];
-    uint32_t sv[kTE];
+    uint32_t su[kTEP];
+    uint32_t sv[kTEP];
 };
 
 struct PassBSmem {
-    uint32_t su[kTE];
-    uint32_t sv[kTE];
-    uint32_t rowsum[kTE];  // kept-edge count per row head (local index)
-    uint32_t runlen[kTE];  // edge count per run head (local index)
+    uint32_t su[kTEP];
+    uint32_t sv[kTEP];
+    uint32_t rowsum[kTEP];  // kept-edge count per row head (local index, padded)
+    uint32_t runlen[kTEP];  // edge count per run head (local index, padded)
     uint32_t scan_u[kT / 32 + 1];
     int32_t scan_i[kT / 32 + 1];
     uint32_t prev_u, prev_v, next_u;
@@ -102,8 +108,8 @@ __global__ void __launch_bounds__(kT) k2_pass_a(const longlong2* __restrict__ uv
                 const bool ok = p.x >= 1 && p.x <= n && p.y >= 1 && p.y <= n;
                 if (!ok) my_err |= kErrLabelRange;
                 const uint32_t u = ok ? (uint32_t)(p.x - 1) : 0u, v = ok ? (uint32_t)(p.y - 1) : 0u;
-                S.su[l] = u;
-                S.sv[l] = v;
+                S.su[sp(l)] = u;
+                S.sv[sp(l)] = v;
                 if (ok) atomicAdd(&d_in[v], 1u);
             }
         }
@@ -122,10 +128,10 @@ __global__ void __launch_bounds__(kT) k2_pass_a(const longlong2* __restrict__ uv
         for (int k = 0; k < kI; ++k) {
             const int l = l0 + k;
             if (l < cnt) {
-                const uint32_t u = S.su[l], v = S.sv[l];
+                const uint32_t u = S.su[sp(l)], v = S.sv[sp(l)];
                 bool first = false;
                 uint32_t pu = 0, pv = 0;
-                if (l > 0) { pu = S.su[l - 1]; pv = S.sv[l - 1]; }
+                if (l > 0) { pu = S.su[sp(l - 1)]; pv = S.sv[sp(l - 1)]; }
                 else if (has_prev_s) { pu = pu_s; pv = pv_s; }
                 else first = true;
                 if (first) heads++;
@@ -196,10 +202,10 @@ __global__ void __launch_bounds__(kT) k2_pass_b(
         const int l = j * kT + tid;
         if (l < cnt) {
             const longlong2 p = uv[base + l];
-            S.su[l] = (uint32_t)(p.x - 1);
-            S.sv[l] = (uint32_t)(p.y - 1);
+            S.su[sp(l)] = (uint32_t)(p.x - 1);
+            S.sv[sp(l)] = (uint32_t)(p.y - 1);
         }
-        if (l < kTE) { S.rowsum[l] = 0; S.runlen[l] = 0; }
+        if (l < kTE) { S.rowsum[sp(l)] = 0; S.runlen[sp(l)] = 0; }
     }
     if (tid == 0) {
         S.has_prev = base > 0;
@@ -224,9 +230,9 @@ __global__ void __launch_bounds__(kT) k2_pass_b(
     for (int k = 0; k < kI; ++k) {
         const int l = l0 + k;
         if (l < cnt) {
-            const uint32_t u = S.su[l], v = S.sv[l];
+            const uint32_t u = S.su[sp(l)], v = S.sv[sp(l)];
             bool rs, hd;
-            if (l > 0) { rs = u != S.su[l - 1]; hd = rs || v != S.sv[l - 1]; }
+            if (l > 0) { rs = u != S.su[sp(l - 1)]; hd = rs || v != S.sv[sp(l - 1)]; }
             else if (S.has_prev) { rs = u != S.prev_u; hd = rs || v != S.prev_v; }
             else { rs = true; hd = true; }
             const bool kp = (keepbits[v >> 5] >> (v & 31)) & 1u;
@@ -274,12 +280,12 @@ __global__ void __launch_bounds__(kT) k2_pass_b(
             const int l = l0 + k;
             if (l < cnt) {
                 if ((fl_rs >> k) & 1u) {
-                    if (acc_row) { if (rh >= 0) atomicAdd(&S.rowsum[rh], acc_row); else atomicAdd(&S.first_row_part, acc_row); }
+                    if (acc_row) { if (rh >= 0) atomicAdd(&S.rowsum[sp(rh)], acc_row); else atomicAdd(&S.first_row_part, acc_row); }
                     acc_row = 0;
                     rh = l;
                 }
                 if ((fl_hd >> k) & 1u) {
-                    if (acc_run) { if (rn >= 0) atomicAdd(&S.runlen[rn], acc_run); else atomicAdd(&S.first_run_part, acc_run); }
+                    if (acc_run) { if (rn >= 0) atomicAdd(&S.runlen[sp(rn)], acc_run); else atomicAdd(&S.first_run_part, acc_run); }
                     acc_run = 0;
                     rn = l;
                 }
@@ -287,13 +293,13 @@ __global__ void __launch_bounds__(kT) k2_pass_b(
                 acc_run += 1;
             }
         }
-        if (acc_row) { if (rh >= 0) atomicAdd(&S.rowsum[rh], acc_row); else atomicAdd(&S.first_row_part, acc_row); }
-        if (acc_run) { if (rn >= 0) atomicAdd(&S.runlen[rn], acc_run); else atomicAdd(&S.first_run_part, acc_run); }
+        if (acc_row) { if (rh >= 0) atomicAdd(&S.rowsum[sp(rh)], acc_row); else atomicAdd(&S.first_row_part, acc_row); }
+        if (acc_run) { if (rn >= 0) atomicAdd(&S.runlen[sp(rn)], acc_run); else atomicAdd(&S.first_run_part, acc_run); }
     }
     __syncthreads();
     const uint64_t tile_base = S.tile_base;
-    const bool last_spans = S.has_next && S.su[cnt - 1] == S.next_u;
-    const bool first_spans = S.has_prev && S.su[0] == S.prev_u;
+    const bool last_spans = S.has_next && S.su[sp(cnt - 1)] == S.next_u;
+    const bool first_spans = S.has_prev && S.su[sp(0)] == S.prev_u;
     const int32_t rh_last = rs_last_all;  // local head of the tile's last row (-1: began earlier)
 
     // Emit entries and row offsets.
@@ -304,17 +310,17 @@ __global__ void __launch_bounds__(kT) k2_pass_b(
         for (int k = 0; k < kI; ++k) {
             const int l = l0 + k;
             if (l < cnt) {
-                const uint32_t u = S.su[l], v = S.sv[l];
+                const uint32_t u = S.su[sp(l)], v = S.sv[sp(l)];
                 if ((fl_rs >> k) & 1u) {
                     rh = l;
-                    const int64_t pu = l > 0 ? (int64_t)S.su[l - 1] : (S.has_prev ? (int64_t)S.prev_u : -1);
+                    const int64_t pu = l > 0 ? (int64_t)S.su[sp(l - 1)] : (S.has_prev ? (int64_t)S.prev_u : -1);
                     for (int64_t r = pu + 1; r <= (int64_t)u; ++r) row_offsets[r] = (uint32_t)pos;
                 }
                 if (((fl_hd >> k) & 1u) && ((fl_kp >> k) & 1u)) {
                     cols[pos] = v;
-                    const double c = (double)S.runlen[l];
+                    const double c = (double)S.runlen[sp(l)];
                     const bool spanning = rh < 0 || (last_spans && rh == rh_last);
-                    values[pos] = (spanning || !normalize) ? c : c / (double)S.rowsum[rh];
+                    values[pos] = (spanning || !normalize) ? c : c / (double)S.rowsum[sp(rh)];
                     ++pos;
                 }
             }
@@ -322,21 +328,21 @@ __global__ void __launch_bounds__(kT) k2_pass_b(
     }
     if (tid == 0) {
         // Rows crossing tile edges: partial kept-edge sums go to dout_f.
-        if (first_spans && S.first_row_part) atomicAdd(&dout_f[S.su[0]], S.first_row_part);
+        if (first_spans && S.first_row_part) atomicAdd(&dout_f[S.su[sp(0)]], S.first_row_part);
         if (last_spans && rh_last >= 0) {
-            atomicAdd(&dout_f[S.su[cnt - 1]], S.rowsum[rh_last]);
-            fix_rows[atomicAdd(n_fix, 1u)] = S.su[cnt - 1];
+            atomicAdd(&dout_f[S.su[sp(cnt - 1)]], S.rowsum[sp(rh_last)]);
+            fix_rows[atomicAdd(n_fix, 1u)] = S.su[sp(cnt - 1)];
         }
         // A run continuing from the previous tile: its head entry is the last
         // kept entry before this tile (position tile_base-1) when kept.
-        const bool kp0 = (keepbits[S.sv[0] >> 5] >> (S.sv[0] & 31)) & 1u;
+        const bool kp0 = (keepbits[S.sv[sp(0)] >> 5] >> (S.sv[sp(0)] & 31)) & 1u;
         if (S.first_run_part && kp0) { cont_p[t] = (uint32_t)(tile_base - 1); cont_c[t] = S.first_run_part; }
         else { cont_p[t] = 0; cont_c[t] = 0; }
         if (base + cnt == m) *nnz_out = tile_base + tile_kh;
     }
     if (base + cnt == m) {
         const uint64_t total = tile_base + tile_kh;
-        for (int64_t r = (int64_t)S.su[cnt - 1] + 1 + tid; r <= n; r += kT) row_offsets[r] = (uint32_t)total;
+        for (int64_t r = (int64_t)S.su[sp(cnt - 1)] + 1 + tid; r <= n; r += kT) row_offsets[r] = (uint32_t)total;
     }
 }
 
@@ -346,15 +352,44 @@ __global__ void k2_fix_runs(const uint32_t* __restrict__ cont_p, const uint32_t*
         if (cont_c[t]) atomicAdd(&values[cont_p[t]], (double)cont_c[t]);  // exact: integers
 }
 
-__global__ void k2_fix_rows(const uint32_t* __restrict__ fix_rows, const uint32_t* __restrict__ n_fix,
-                            const uint32_t* __restrict__ row_offsets, const uint32_t* __restrict__ dout_f,
-                            double* __restrict__ values) {
+// Rows that span tiles (their row sums were accumulated across tiles) are
+// divided here. Work is flattened over their entries so hub rows (10^5
+// entries) spread over the whole GPU: one block scans the row lengths, then a
+// grid-stride pass over all entries finds its row by binary search.
+__global__ void k2_fix_scan(const uint32_t* __restrict__ fix_rows, const uint32_t* __restrict__ n_fix,
+                            const uint32_t* __restrict__ row_offsets, uint32_t* __restrict__ fix_off) {
+    __shared__ uint32_t scan_tmp[33];
+    __shared__ uint32_t carry;
     const uint32_t nf = *n_fix;
-    for (uint32_t i = blockIdx.x; i < nf; i += gridDim.x) {
-        const uint32_t r = fix_rows[i];
-        const uint32_t b = row_offsets[r], e = row_offsets[r + 1];
-        const double d = (double)dout_f[r];
-        for (uint32_t p = b + threadIdx.x; p < e; p += blockDim.x) values[p] = values[p] / d;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (uint32_t base = 0; base < nf; base += blockDim.x) {
+        const uint32_t i = base + threadIdx.x;
+        uint32_t len = 0;
+        if (i < nf) { const uint32_t r = fix_rows[i]; len = row_offsets[r + 1] - row_offsets[r]; }
+        uint32_t tot;
+        const uint32_t ex = dev::block_excl_scan(len, scan_tmp, tot);
+        if (i < nf) fix_off[i] = carry + ex;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) fix_off[nf] = carry;
+}
+__global__ void k2_fix_rows(const uint32_t* __restrict__ fix_rows, const uint32_t* __restrict__ n_fix,
+                            const uint32_t* __restrict__ fix_off, const uint32_t* __restrict__ row_offsets,
+                            const uint32_t* __restrict__ dout_f, double* __restrict__ values) {
+    const uint32_t nf = *n_fix;
+    const uint32_t total = fix_off[nf];
+    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < total; q += gridDim.x * blockDim.x) {
+        uint32_t lo = 0, hi = nf;  // last i with fix_off[i] <= q
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (fix_off[mid] <= q) lo = mid; else hi = mid;
+        }
+        const uint32_t r = fix_rows[lo];
+        const uint32_t p = row_offsets[r] + (q - fix_off[lo]);
+        values[p] = values[p] / (double)dout_f[r];
     }
 }
 
@@ -441,8 +476,12 @@ uint32_t k2_filter_device(const int64_t* d_uv, int64_t m, int64_t n, prg_matrix*
     k2_fix_runs<<<div_up(ntiles, 256), 256, 0, s>>>(cont_p.get(), cont_c.get(), ntiles, out->values);
     PRG_LAUNCH_CHECK();
     if (normalize)
-    k2_fix_rows<<<(unsigned)num_sms() * 2, 256, 0, s>>>(fix_rows.get(), n_fix, out->row_offsets, dout_f.get(),
-                                                         out->values);
+    {
+        DevBuf<uint32_t> fix_off((size_t)ntiles + 2, s);
+        k2_fix_scan<<<1, 1024, 0, s>>>(fix_rows.get(), n_fix, out->row_offsets, fix_off.get());
+        k2_fix_rows<<<(unsigned)num_sms() * 8, 256, 0, s>>>(fix_rows.get(), n_fix, fix_off.get(), out->row_offsets,
+                                                             dout_f.get(), out->values);
+    }
     PRG_LAUNCH_CHECK();
     uint64_t h[3];
     PRG_CUDA(cudaMemcpyAsync(h, scal.get(), 3 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));

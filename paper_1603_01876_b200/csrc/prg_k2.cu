@@ -23,7 +23,7 @@ namespace prg {
 
 namespace {
 
-constexpr int kT = 1024;        // threads per CTA
+constexpr int kT = 512;         // threads per CTA
 constexpr int kI = 8;           // edges per thread
 constexpr int kTE = kT * kI;    // edges per tile
 
@@ -33,16 +33,13 @@ constexpr int kTE = kT * kI;    // edges per tile
 __device__ __forceinline__ int sp(int l) { return l + (l >> 5); }
 constexpr int kTEP = kTE + kTE / 32;
 
-struct EdgeSmem {
-    uint32_t su[kTEP];
-    uint32_t sv[kTEP];
-};
 
 struct PassBSmem {
     uint32_t su[kTEP];
     uint32_t sv[kTEP];
-    uint32_t rowsum[kTEP];  // kept-edge count per row head (local index, padded)
-    uint32_t runlen[kTEP];  // edge count per run head (local index, padded)
+    // per head (local index, padded): kept-edge count of the row in bits 16..31
+    // (row heads), edge count of the (u,v) run in bits 0..15 (run heads); both <= kTE
+    uint32_t rr[kTEP];
     uint32_t scan_u[kT / 32 + 1];
     int32_t scan_i[kT / 32 + 1];
     uint32_t prev_u, prev_v, next_u;
@@ -87,63 +84,57 @@ __device__ __forceinline__ int32_t block_excl_max_scan(int32_t v, int32_t* smem,
 // ---------------------------------------------------------------------------
 // Pass A
 // ---------------------------------------------------------------------------
+// Pass A keeps edges in registers: edge l is compared with edge l-1 through a
+// warp shuffle; lane 0 takes its predecessor from the previous warp's lane 31
+// via a small SMEM exchange.
 __global__ void __launch_bounds__(kT) k2_pass_a(const longlong2* __restrict__ uv, int64_t m, int64_t n,
                                                 uint32_t* __restrict__ d_in, uint32_t* __restrict__ err,
                                                 unsigned long long* __restrict__ nnz_raw,
                                                 uint32_t ntiles) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    EdgeSmem& S = *reinterpret_cast<EdgeSmem*>(smem_raw);
     __shared__ uint32_t red[kT / 32];
-    __shared__ uint32_t pu_s, pv_s;
-    __shared__ int has_prev_s;
+    __shared__ longlong2 last[kI][kT / 32];  // lane 31 of each (row j, warp)
+    __shared__ longlong2 before;             // edge base-1
     uint32_t my_err = 0;
+    const unsigned lane = dev::lane_id(), w = dev::warp_id();
     for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const int64_t base = (int64_t)t * kTE;
         const int cnt = (int)min((int64_t)kTE, m - base);
+        longlong2 p[kI];
 #pragma unroll
         for (int j = 0; j < kI; ++j) {
             const int l = j * kT + threadIdx.x;
-            if (l < cnt) {
-                const longlong2 p = uv[base + l];
-                const bool ok = p.x >= 1 && p.x <= n && p.y >= 1 && p.y <= n;
-                if (!ok) my_err |= kErrLabelRange;
-                const uint32_t u = ok ? (uint32_t)(p.x - 1) : 0u, v = ok ? (uint32_t)(p.y - 1) : 0u;
-                S.su[sp(l)] = u;
-                S.sv[sp(l)] = v;
-                if (ok) atomicAdd(&d_in[v], 1u);
-            }
+            p[j] = l < cnt ? uv[base + l] : make_longlong2(0, 0);
+            if (lane == 31) last[j][w] = p[j];
         }
-        if (threadIdx.x == 0) {
-            has_prev_s = base > 0;
-            if (base > 0) {
-                const longlong2 p = uv[base - 1];
-                pu_s = (uint32_t)(p.x - 1);
-                pv_s = (uint32_t)(p.y - 1);
-            }
-        }
+        if (threadIdx.x == 0) before = base > 0 ? uv[base - 1] : make_longlong2(0, 0);
         __syncthreads();
         uint32_t heads = 0;
-        const int l0 = threadIdx.x * kI;
 #pragma unroll
-        for (int k = 0; k < kI; ++k) {
-            const int l = l0 + k;
+        for (int j = 0; j < kI; ++j) {
+            const int l = j * kT + threadIdx.x;
+            long long px = __shfl_up_sync(0xffffffffu, p[j].x, 1);
+            long long py = __shfl_up_sync(0xffffffffu, p[j].y, 1);
+            if (lane == 0) {
+                const longlong2 q = w ? last[j][w - 1] : (j ? last[j - 1][kT / 32 - 1] : before);
+                px = q.x;
+                py = q.y;
+            }
             if (l < cnt) {
-                const uint32_t u = S.su[sp(l)], v = S.sv[sp(l)];
-                bool first = false;
-                uint32_t pu = 0, pv = 0;
-                if (l > 0) { pu = S.su[sp(l - 1)]; pv = S.sv[sp(l - 1)]; }
-                else if (has_prev_s) { pu = pu_s; pv = pv_s; }
-                else first = true;
-                if (first) heads++;
-                else {
-                    if (u < pu) my_err |= kErrUnsorted;
-                    else if (u == pu && v < pv) my_err |= kErrNotCanonical;
-                    heads += (u != pu || v != pv);
+                const bool ok = p[j].x >= 1 && p[j].x <= n && p[j].y >= 1 && p[j].y <= n;
+                if (!ok) my_err |= kErrLabelRange;
+                else atomicAdd(&d_in[(uint32_t)(p[j].y - 1)], 1u);
+                if (base + l == 0) {
+                    heads++;
+                } else {
+                    const long long pu = px, pv = py;
+                    if (p[j].x < pu) my_err |= kErrUnsorted;
+                    else if (p[j].x == pu && p[j].y < pv) my_err |= kErrNotCanonical;
+                    heads += (p[j].x != pu || p[j].y != pv);
                 }
             }
         }
         heads = dev::warp_sum(heads);
-        if (dev::lane_id() == 0) red[dev::warp_id()] = heads;
+        if (lane == 0) red[dev::warp_id()] = heads;
         __syncthreads();
         if (threadIdx.x < 32) {
             uint32_t x = threadIdx.x < kT / 32 ? red[threadIdx.x] : 0;
@@ -153,7 +144,7 @@ __global__ void __launch_bounds__(kT) k2_pass_a(const longlong2* __restrict__ uv
         __syncthreads();
     }
     my_err = __reduce_or_sync(0xffffffffu, my_err);
-    if (dev::lane_id() == 0 && my_err) atomicOr(err, my_err);
+    if (lane == 0 && my_err) atomicOr(err, my_err);
 }
 
 __global__ void k2_max_kernel(const uint32_t* __restrict__ d_in, int64_t n, uint32_t* __restrict__ out) {
@@ -202,10 +193,13 @@ __global__ void __launch_bounds__(kT) k2_pass_b(
         const int l = j * kT + tid;
         if (l < cnt) {
             const longlong2 p = uv[base + l];
+            const uint32_t v = (uint32_t)(p.y - 1);
+            // keep bit fetched here, alongside the edge loads; carried in bit 31
+            const uint32_t kp = (keepbits[v >> 5] >> (v & 31)) & 1u;
             S.su[sp(l)] = (uint32_t)(p.x - 1);
-            S.sv[sp(l)] = (uint32_t)(p.y - 1);
+            S.sv[sp(l)] = v | (kp << 31);
         }
-        if (l < kTE) { S.rowsum[sp(l)] = 0; S.runlen[sp(l)] = 0; }
+        if (l < kTE) S.rr[sp(l)] = 0;
     }
     if (tid == 0) {
         S.has_prev = base > 0;
@@ -230,12 +224,12 @@ __global__ void __launch_bounds__(kT) k2_pass_b(
     for (int k = 0; k < kI; ++k) {
         const int l = l0 + k;
         if (l < cnt) {
-            const uint32_t u = S.su[sp(l)], v = S.sv[sp(l)];
+            const uint32_t u = S.su[sp(l)], vk = S.sv[sp(l)], v = vk & 0x7fffffffu;
             bool rs, hd;
-            if (l > 0) { rs = u != S.su[sp(l - 1)]; hd = rs || v != S.sv[sp(l - 1)]; }
+            if (l > 0) { rs = u != S.su[sp(l - 1)]; hd = rs || v != (S.sv[sp(l - 1)] & 0x7fffffffu); }
             else if (S.has_prev) { rs = u != S.prev_u; hd = rs || v != S.prev_v; }
             else { rs = true; hd = true; }
-            const bool kp = (keepbits[v >> 5] >> (v & 31)) & 1u;
+            const bool kp = vk >> 31;
             fl_rs |= (uint32_t)rs << k;
             fl_hd |= (uint32_t)hd << k;
             fl_kp |= (uint32_t)kp << k;
@@ -280,12 +274,12 @@ __global__ void __launch_bounds__(kT) k2_pass_b(
             const int l = l0 + k;
             if (l < cnt) {
                 if ((fl_rs >> k) & 1u) {
-                    if (acc_row) { if (rh >= 0) atomicAdd(&S.rowsum[sp(rh)], acc_row); else atomicAdd(&S.first_row_part, acc_row); }
+                    if (acc_row) { if (rh >= 0) atomicAdd(&S.rr[sp(rh)], acc_row << 16); else atomicAdd(&S.first_row_part, acc_row); }
                     acc_row = 0;
                     rh = l;
                 }
                 if ((fl_hd >> k) & 1u) {
-                    if (acc_run) { if (rn >= 0) atomicAdd(&S.runlen[sp(rn)], acc_run); else atomicAdd(&S.first_run_part, acc_run); }
+                    if (acc_run) { if (rn >= 0) atomicAdd(&S.rr[sp(rn)], acc_run); else atomicAdd(&S.first_run_part, acc_run); }
                     acc_run = 0;
                     rn = l;
                 }
@@ -293,8 +287,8 @@ __global__ void __launch_bounds__(kT) k2_pass_b(
                 acc_run += 1;
             }
         }
-        if (acc_row) { if (rh >= 0) atomicAdd(&S.rowsum[sp(rh)], acc_row); else atomicAdd(&S.first_row_part, acc_row); }
-        if (acc_run) { if (rn >= 0) atomicAdd(&S.runlen[sp(rn)], acc_run); else atomicAdd(&S.first_run_part, acc_run); }
+        if (acc_row) { if (rh >= 0) atomicAdd(&S.rr[sp(rh)], acc_row << 16); else atomicAdd(&S.first_row_part, acc_row); }
+        if (acc_run) { if (rn >= 0) atomicAdd(&S.rr[sp(rn)], acc_run); else atomicAdd(&S.first_run_part, acc_run); }
     }
     __syncthreads();
     const uint64_t tile_base = S.tile_base;
@@ -310,7 +304,7 @@ __global__ void __launch_bounds__(kT) k2_pass_b(
         for (int k = 0; k < kI; ++k) {
             const int l = l0 + k;
             if (l < cnt) {
-                const uint32_t u = S.su[sp(l)], v = S.sv[sp(l)];
+                const uint32_t u = S.su[sp(l)], v = S.sv[sp(l)] & 0x7fffffffu;
                 if ((fl_rs >> k) & 1u) {
                     rh = l;
                     const int64_t pu = l > 0 ? (int64_t)S.su[sp(l - 1)] : (S.has_prev ? (int64_t)S.prev_u : -1);
@@ -318,9 +312,9 @@ __global__ void __launch_bounds__(kT) k2_pass_b(
                 }
                 if (((fl_hd >> k) & 1u) && ((fl_kp >> k) & 1u)) {
                     cols[pos] = v;
-                    const double c = (double)S.runlen[sp(l)];
+                    const double c = (double)(S.rr[sp(l)] & 0xffffu);
                     const bool spanning = rh < 0 || (last_spans && rh == rh_last);
-                    values[pos] = (spanning || !normalize) ? c : c / (double)S.rowsum[sp(rh)];
+                    values[pos] = (spanning || !normalize) ? c : c / (double)(S.rr[sp(rh)] >> 16);
                     ++pos;
                 }
             }
@@ -330,12 +324,12 @@ __global__ void __launch_bounds__(kT) k2_pass_b(
         // Rows crossing tile edges: partial kept-edge sums go to dout_f.
         if (first_spans && S.first_row_part) atomicAdd(&dout_f[S.su[sp(0)]], S.first_row_part);
         if (last_spans && rh_last >= 0) {
-            atomicAdd(&dout_f[S.su[sp(cnt - 1)]], S.rowsum[sp(rh_last)]);
+            atomicAdd(&dout_f[S.su[sp(cnt - 1)]], S.rr[sp(rh_last)] >> 16);
             fix_rows[atomicAdd(n_fix, 1u)] = S.su[sp(cnt - 1)];
         }
         // A run continuing from the previous tile: its head entry is the last
         // kept entry before this tile (position tile_base-1) when kept.
-        const bool kp0 = (keepbits[S.sv[sp(0)] >> 5] >> (S.sv[sp(0)] & 31)) & 1u;
+        const bool kp0 = S.sv[sp(0)] >> 31;
         if (S.first_run_part && kp0) { cont_p[t] = (uint32_t)(tile_base - 1); cont_c[t] = S.first_run_part; }
         else { cont_p[t] = 0; cont_c[t] = 0; }
         if (base + cnt == m) *nnz_out = tile_base + tile_kh;
@@ -398,6 +392,7 @@ __global__ void k2_fix_rows(const uint32_t* __restrict__ fix_rows, const uint32_
 uint32_t k2_filter_device(const int64_t* d_uv, int64_t m, int64_t n, prg_matrix* out, cudaStream_t s,
                           bool filter, bool normalize) {
     ProfScope prof("k2_filter", s);
+    if (n > (int64_t{1} << 31)) throw CudaError{"K2: vertex count above 2^31"};
     out->n = n;
     out->cap = (uint64_t)(m > 0 ? m : 1);
     out->row_offsets = static_cast<uint32_t*>(ws_alloc((size_t)(n + 1) * 4, s));
@@ -423,14 +418,13 @@ uint32_t k2_filter_device(const int64_t* d_uv, int64_t m, int64_t n, prg_matrix*
     const auto* uv = reinterpret_cast<const longlong2*>(d_uv);
     static bool attr = false;
     if (!attr) {
-        PRG_CUDA(cudaFuncSetAttribute(k2_pass_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(EdgeSmem)));
         PRG_CUDA(cudaFuncSetAttribute(k2_pass_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PassBSmem)));
         attr = true;
     }
     const unsigned ga = std::min<unsigned>(ntiles, (unsigned)num_sms() * 2);
     {
         ProfScope pa("k2_pass_a", s);
-        k2_pass_a<<<ga, kT, sizeof(EdgeSmem), s>>>(uv, m, n, out->d_in, err, nnz_raw, ntiles);
+        k2_pass_a<<<ga, kT, 0, s>>>(uv, m, n, out->d_in, err, nnz_raw, ntiles);
         PRG_LAUNCH_CHECK();
     }
     uint32_t h_err = 0;

@@ -62,6 +62,33 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def spmv_traffic():
+    """DRAM bytes (read+write) per SpMV launch from the committed ncu --set full
+    capture (profiles/ncu_traffic.json, written by tools/ncu_traffic.py)."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)["k3_spmv"]["dram_bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
+# Random 8-byte gathers from an L2-resident vector: ~1.0 line/clk/SM measured
+# on this B200 (tools/microbench/mb2.cu); every SpMV entry is one such gather.
+GATHER_LINES_PER_CLK_SM = 1.0
+
+
+def gather_bound(nnz, spmv_ms, clk):
+    if not spmv_ms or not clk or not clk.get("sm_mhz"):
+        return None
+    import torch
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    rate = nnz / (spmv_ms * 1e-3) / (sms * clk["sm_mhz"] * 1e6)
+    return {"gathers_per_launch": int(nnz), "achieved_per_clk_sm": rate,
+            "peak_per_clk_sm": GATHER_LINES_PER_CLK_SM, "frac": rate / GATHER_LINES_PER_CLK_SM,
+            "peak_source": "tools/microbench/mb2.cu random-gather sweep (64 MB working set)"}
+
+
 def alg_bytes(n, m, nnz, iters):
     """SURVEY §8(d) algorithmic (compulsory) bytes."""
     k1 = 32 * m
@@ -246,10 +273,12 @@ def run_ours(args):
         "k3_edges_per_s": value,
         "stage_ms": {"k1_sort": k1_ms, "k2_filter": k2_ms, "k3_pagerank": k3_ms},
         "final_norm1": norm,
-        "roofline": {"bound": "hbm", "kernel": "k3_spmv (spmv_pull_kernel, one PageRank iteration)",
+        "roofline": {"bound": "hbm", "kernel": "k3_spmv (spmv_sell_kernel, one PageRank iteration)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak if achieved else None, "traffic": None,
-                     "alg_bytes_per_launch": b3_iter, "avg_launch_ms": spmv_avg, "peak_source": peak_src},
+                     "frac": achieved / peak if achieved else None, "traffic": spmv_traffic(),
+                     "alg_bytes_per_launch": b3_iter, "avg_launch_ms": spmv_avg, "peak_source": peak_src,
+                     # the binding limit in practice: random 8 B gathers through L1TEX
+                     "gather_bound": gather_bound(nnz, spmv_avg, clk)},
         "stage_roofline": {
             "k1_sort": {"alg_bytes": b1, "achieved_gbs": b1 / (k1_ms * 1e-3) / 1e9,
                         "frac": b1 / (k1_ms * 1e-3) / 1e9 / peak},

@@ -347,11 +347,13 @@ __global__ void k2_fix_runs(const uint32_t* __restrict__ cont_p, const uint32_t*
 }
 
 // Rows that span tiles (their row sums were accumulated across tiles) are
-// divided here. Work is flattened over their entries so hub rows (10^5
-// entries) spread over the whole GPU: one block scans the row lengths, then a
-// grid-stride pass over all entries finds its row by binary search.
+// divided here. Work is split into tasks of <= kFixChunk entries so hub rows
+// (10^5 entries) spread over the GPU: one block scans the per-row task counts
+// and writes the task -> row map, then one warp per task divides its entries.
+constexpr uint32_t kFixChunk = 1024;
 __global__ void k2_fix_scan(const uint32_t* __restrict__ fix_rows, const uint32_t* __restrict__ n_fix,
-                            const uint32_t* __restrict__ row_offsets, uint32_t* __restrict__ fix_off) {
+                            const uint32_t* __restrict__ row_offsets, uint64_t* __restrict__ task_row,
+                            uint32_t* __restrict__ n_tasks) {
     __shared__ uint32_t scan_tmp[33];
     __shared__ uint32_t carry;
     const uint32_t nf = *n_fix;
@@ -359,31 +361,33 @@ __global__ void k2_fix_scan(const uint32_t* __restrict__ fix_rows, const uint32_
     __syncthreads();
     for (uint32_t base = 0; base < nf; base += blockDim.x) {
         const uint32_t i = base + threadIdx.x;
-        uint32_t len = 0;
-        if (i < nf) { const uint32_t r = fix_rows[i]; len = row_offsets[r + 1] - row_offsets[r]; }
+        uint32_t nc = 0;
+        if (i < nf) {
+            const uint32_t r = fix_rows[i];
+            nc = (row_offsets[r + 1] - row_offsets[r] + kFixChunk - 1) / kFixChunk;
+        }
         uint32_t tot;
-        const uint32_t ex = dev::block_excl_scan(len, scan_tmp, tot);
-        if (i < nf) fix_off[i] = carry + ex;
+        const uint32_t ex = carry + dev::block_excl_scan(nc, scan_tmp, tot);
+        for (uint32_t c = 0; c < nc; ++c) task_row[ex + c] = ((uint64_t)i << 32) | c;  // (fix row, chunk)
         __syncthreads();
         if (threadIdx.x == 0) carry += tot;
         __syncthreads();
     }
-    if (threadIdx.x == 0) fix_off[nf] = carry;
+    if (threadIdx.x == 0) *n_tasks = carry;
 }
-__global__ void k2_fix_rows(const uint32_t* __restrict__ fix_rows, const uint32_t* __restrict__ n_fix,
-                            const uint32_t* __restrict__ fix_off, const uint32_t* __restrict__ row_offsets,
+__global__ void k2_fix_rows(const uint32_t* __restrict__ fix_rows, const uint64_t* __restrict__ task_row,
+                            const uint32_t* __restrict__ n_tasks, const uint32_t* __restrict__ row_offsets,
                             const uint32_t* __restrict__ dout_f, double* __restrict__ values) {
-    const uint32_t nf = *n_fix;
-    const uint32_t total = fix_off[nf];
-    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < total; q += gridDim.x * blockDim.x) {
-        uint32_t lo = 0, hi = nf;  // last i with fix_off[i] <= q
-        while (hi - lo > 1) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (fix_off[mid] <= q) lo = mid; else hi = mid;
-        }
-        const uint32_t r = fix_rows[lo];
-        const uint32_t p = row_offsets[r] + (q - fix_off[lo]);
-        values[p] = values[p] / (double)dout_f[r];
+    const uint32_t nt = *n_tasks;
+    const uint32_t lane = dev::lane_id();
+    for (uint32_t q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < nt; q += (gridDim.x * blockDim.x) >> 5) {
+        const uint64_t tk = task_row[q];
+        const uint32_t i = (uint32_t)(tk >> 32), c = (uint32_t)tk;
+        const uint32_t r = fix_rows[i];
+        const uint32_t b = row_offsets[r] + c * kFixChunk;
+        const uint32_t e = min(row_offsets[r + 1], b + kFixChunk);
+        const double d = (double)dout_f[r];
+        for (uint32_t p = b + lane; p < e; p += 32) values[p] = values[p] / d;
     }
 }
 
@@ -471,10 +475,11 @@ uint32_t k2_filter_device(const int64_t* d_uv, int64_t m, int64_t n, prg_matrix*
     PRG_LAUNCH_CHECK();
     if (normalize)
     {
-        DevBuf<uint32_t> fix_off((size_t)ntiles + 2, s);
-        k2_fix_scan<<<1, 1024, 0, s>>>(fix_rows.get(), n_fix, out->row_offsets, fix_off.get());
-        k2_fix_rows<<<(unsigned)num_sms() * 8, 256, 0, s>>>(fix_rows.get(), n_fix, fix_off.get(), out->row_offsets,
-                                                             dout_f.get(), out->values);
+        DevBuf<uint64_t> task_row((size_t)ntiles + (size_t)m / kFixChunk + 2, s);
+        DevBuf<uint32_t> n_tasks(1, s);
+        k2_fix_scan<<<1, 1024, 0, s>>>(fix_rows.get(), n_fix, out->row_offsets, task_row.get(), n_tasks.get());
+        k2_fix_rows<<<(unsigned)num_sms() * 8, 256, 0, s>>>(fix_rows.get(), task_row.get(), n_tasks.get(),
+                                                             out->row_offsets, dout_f.get(), out->values);
     }
     PRG_LAUNCH_CHECK();
     uint64_t h[3];

@@ -6,20 +6,22 @@
 // :58-61). Here the CSR handed over by K2 is transposed once (inside the timed
 // region) and every iteration pulls over columns.
 //
-// Layout (timed mode, SURVEY §7.2):
+// Layout (timed mode):
 //   * rows are renumbered by descending out-degree (quarter-octave classes,
 //     ties by original id); dangling rows go last and are never gathered. The
 //     gather vector s[j] = r[u_j] * b[u_j] (j = new id) is therefore dense and
-//     hot-first: its first kHot entries are staged in shared memory, the rest
-//     (~59 MB at S=24) stays L2-resident. Random gathers are the bound:
-//     ~1 line/clk/SM from L2 vs ~3.6/clk/SM from SMEM (tools/microbench).
+//     hot-first (~59 MB at S=24, L2-resident; the L1 keeps the hot head).
+//     Random gathers are the bound: ~1 line/clk/SM from L2 (tools/microbench).
+//     A shared-memory copy of the hot head measured slower (1.62 vs 1.22 ms).
 //   * b[u] is the row's base value (its minimum stored value; for K2 output
 //     that is 1/d_out exactly). Entries equal to b[u] contribute r[u]*b[u],
 //     the reference's own product r[u]*values[k], bit for bit. Other entries
-//     (duplicate edges, ~2%) are exceptions with an explicit f64 value.
-//   * CSC index stream: u32 per entry, bit 31 = exception, bits 0-30 = new id
-//     of the source row. Columns keep their original ids, so r' needs no
-//     un-permutation and exceptions read r' directly.
+//     (duplicate edges, ~1.3%) are exceptions: their SELL slot gathers
+//     s[n_nd + j], the exception's product r[u]*value written each iteration.
+//   * transpose = stable sort of (col | new row, exception) keys by column
+//     only (the payload keeps each column's rows in ascending new id), then a
+//     SELL-32 layout over virtual columns of <= kVcMax entries, slices sorted
+//     by length class. Columns keep their original ids.
 // Parity mode (mode 1) keeps original row ids, sums every column sequentially
 // in ascending u with separate mul/add, and computes every sum(r) with one
 // thread in index order — the reference's exact evaluation order.
@@ -36,8 +38,6 @@ namespace {
 
 constexpr uint64_t kRankInitStream = 0x72616e6b696e6974ULL;  // kernel3_pagerank.cpp:15
 constexpr int kSpmvThreads = 1024;
-constexpr int kHotBytes = 220 * 1024;
-constexpr int kHot = kHotBytes / 8;
 constexpr int kCscGroup = 32;  // exception ranks are counted per 32-entry group
 
 __host__ __device__ inline int bits_for(int64_t n) {
@@ -501,7 +501,6 @@ __global__ void spmv_seq_kernel(SeqArgs a) {
 // ---------------------------------------------------------------------------
 constexpr uint32_t kVcMax = 2048;
 constexpr uint32_t kEmpty = 0xffffffffu;
-constexpr int kUnroll = 8;
 
 __device__ __forceinline__ uint32_t len_class_desc(uint32_t d) {
     const int lg = 31 - __clz(d);
@@ -1053,7 +1052,6 @@ void init_rank_impl(int64_t n, uint64_t seed, double* d_r, int mode, double bgf,
     device_sum(d_r, n, bgf, mode, S, s);
 }
 
-size_t spmv_smem() { return (size_t)kHot * sizeof(double); }
 
 // Runs `iters` steps from r_in (original order, S.out = {sum(r_in), bg}) and
 // writes the final iterate to r_out (original order); S.out ends as

@@ -1,17 +1,23 @@
 // prg_sort.cuh — device MSD radix sort of u64 keys, shared by K1 (edge sort,
-// kernel1_sort.cpp:63-68) and the K3 CSR->CSC transpose.
+// kernel1_sort.cpp:63-68) and K3 (CSR->CSC transpose, row / column ordering,
+// exception lists).
 //
 // Why MSD with SMEM-staged tiles (measured on B200, tools/microbench):
 //   * SMEM atomic ranking runs at ~5 keys/clk/SM: cheap, but unstable — fine
-//     for MSD, where every level only partitions and the final local stage
-//     sorts completely (equal keys are bit-identical, so output is unique);
-//   * __match_any_sync (the usual stable warp ranking) runs at only ~0.5/clk/SM;
+//     where the keys are unique above the payload bits;
 //   * uncoalesced / atomic-cursor global scatters collapse to <0.15 keys/clk/SM,
 //     so each tile is counting-sorted in shared memory and written as per-digit
-//     contiguous runs at offsets from a reduce-then-scan over tile histograms.
+//     contiguous runs at offsets from a reduce-then-scan over tile histograms;
+//   * where input order must survive (stable mode: the K3 transpose sorts
+//     column bits only and carries the row as payload), tiles are ranked with
+//     one warp ballot per digit bit (no SMEM atomics, no match_any).
 // Global levels peel 8 key bits at a time until every segment fits in shared
 // memory (kLocalCap keys); the local stage then sorts each segment in SMEM with
-// adaptive 12-bit counting passes, warp bitonic networks and insertion sorts.
+// a stable LSD over the segment's varying bits (5-bit digits, thread-private
+// packed counters). An 8-bit ballot-ranked local pass measured slower (K1
+// local 6.3 -> 8.4 ms): instruction-bound on the ballots.
+// For reference, CUB's onesweep DeviceRadixSort on this B200 takes 16.6 ms for
+// 2^28 48-bit keys; K1 (2^28 pairs in and out) takes 13.1 ms here.
 #pragma once
 
 #include "prg_common.cuh"
@@ -24,10 +30,6 @@ constexpr int kTile = kTileThreads * kTileItems;  // 8192 keys per global tile
 constexpr int kRadix = 256;
 constexpr int kLocalCap = 8192;       // keys per SMEM-resident segment
 constexpr int kLocalThreads = 512;
-constexpr int kWindowBits = 12;
-constexpr int kLocalBins = 1 << kWindowBits;
-constexpr int kSmallMax = 16;         // <= : one-thread insertion sort
-constexpr int kMidMax = 256;          // <= : one-warp bitonic network
 
 struct Seg {
     uint64_t start;   // element offset in the key buffers

@@ -221,6 +221,55 @@ def test_k3_known_answers(capi):
     assert abs(out[0].item() - 0.35625) <= 1e-12
 
 
+def _adversarial_csr(n, seed):
+    """A CSR that stresses K3's prep: hub rows longer than a tile (8192), a hot
+    column longer than a SELL part (2048), empty rows and columns, rows whose
+    values are all equal (no exceptions) and rows with random values (nearly
+    every entry an exception)."""
+    rng = np.random.default_rng(seed)
+    rows = []
+    for u in range(n):
+        if u in (3, n // 2):
+            d = 9000 + u % 7          # hub rows spanning tiles
+        elif u % 11 == 0:
+            d = 0                     # dangling
+        else:
+            d = int(rng.integers(1, 40))
+        c = np.sort(rng.choice(n, size=min(d, n), replace=False)) if d else np.zeros(0, np.int64)
+        if d and u % 3 == 0 and 17 not in c:
+            c = np.sort(np.append(c[1:], 17))  # hot column 17
+        if u % 4 == 0:
+            v = np.full(len(c), 1.0 / max(len(c), 1))
+        elif u % 4 == 1:
+            v = rng.random(len(c)) + 1e-3
+        else:  # a few duplicates-like exceptions on top of a base value
+            v = np.full(len(c), 0.5 / max(len(c), 1))
+            if len(c):
+                v[rng.integers(0, len(c), size=max(1, len(c) // 8))] *= 3.0
+        rows.append((c, v))
+    ro = np.zeros(n + 1, np.int64)
+    ro[1:] = np.cumsum([len(c) for c, _ in rows])
+    cols = np.concatenate([c for c, _ in rows]).astype(np.int64)
+    vals = np.concatenate([v for _, v in rows]).astype(np.float64)
+    return ro, cols, vals
+
+
+@pytest.mark.parametrize("n,seed", [(1 << 13, 5), (1 << 15, 6)])
+def test_k3_adversarial_matrix(capi, n, seed):
+    ro, cols, vals = _adversarial_csr(n, seed)
+    mat = capi.DeviceMatrix.from_host(n, ro, cols, vals)
+    rp, normp = capi.k3_pagerank(mat, seed=seed, mode=1)
+    ref, nref = O.run_kernel3(ro, cols, vals, n, seed=seed)
+    assert np.array_equal(rp.cpu().numpy().view(np.int64), ref.view(np.int64)) and normp == nref
+    rt, normt = capi.k3_pagerank(mat, seed=seed, mode=0)
+    rt = rt.cpu().numpy()
+    assert rel_l1(rt, ref) <= K3_TOL
+    acc, _ = O.run_kernel3(ro, cols, vals, n, seed=seed, accurate=True)
+    assert rel_l1(rt, acc) <= K3_ACCURATE_TOL
+    rt2, _ = capi.k3_pagerank(mat, seed=seed, mode=0)
+    assert np.array_equal(rt2.cpu().numpy().view(np.int64), rt.view(np.int64))  # deterministic
+
+
 def test_k3_rejects_bad_config(capi):
     m = capi.DeviceMatrix.from_host(2, [0, 1, 2], [1, 0], [1.0, 1.0])
     for damping, iters in ((1.0, 20), (0.0, 20), (0.85, 0)):  # :176-185

@@ -313,7 +313,7 @@ static __device__ __forceinline__ void cta_lsd_sort(LocalSmem& S, uint32_t n, in
 #pragma unroll
     for (int j = 0; j < kLocalItems; ++j) {
         const uint32_t i = tid * kLocalItems + j;
-        k[j] = i < n ? S.X[xpad(i)] : ~0ull;
+        k[j] = i < n ? S.X[tid * (kLocalItems + 1) + j] : ~0ull;  // == X[xpad(i)]
         if (i < n) { o |= k[j]; a &= k[j]; }
     }
 #pragma unroll
@@ -331,15 +331,20 @@ static __device__ __forceinline__ void cta_lsd_sort(LocalSmem& S, uint32_t n, in
     const int lo = __ffsll((long long)diff) - 1;
     const int hi = 63 - __clzll((long long)diff);
     constexpr int WPT = kCntWords / kLocalThreads;  // counter words per thread (16)
+    static_assert(WPT == 16, "xpad(tid*16 + q) == tid*17 + q relies on 16 words per thread");
+    uint32_t* const my = &S.cnt[tid * (WPT + 1)];   // this thread's 16 scan words, contiguous after padding
+    // counter of (digit d, my thread pair) = cnt[xpad(d*256 + p)] = cnt[d*272 + p + p/16]
+    const uint32_t pp = (tid >> 1) + (tid >> 5);
+    static_assert(kLocalThreads / 2 == 256, "digit stride 272 assumes 256 thread pairs");
     for (int sh = lo; sh <= hi; sh += kLsdBits) {
 #pragma unroll
-        for (int q = 0; q < WPT; ++q) S.cnt[xpad(tid * WPT + q)] = 0;
+        for (int q = 0; q < WPT; ++q) my[q] = 0;
         __syncthreads();
         uint32_t rk[kLocalItems / 2];
 #pragma unroll
         for (int j = 0; j < kLocalItems; ++j) {
             const uint32_t d = (uint32_t)(k[j] >> sh) & (kLsdDigits - 1);
-            const uint32_t old = atomicAdd(&S.cnt[xpad(d * (kLocalThreads / 2) + (tid >> 1))], 1u << half);
+            const uint32_t old = atomicAdd(&S.cnt[d * 272u + pp], 1u << half);
             const uint32_t r = (old >> half) & 0xffffu;
             if (j & 1) rk[j >> 1] |= r << 16; else rk[j >> 1] = r;
         }
@@ -349,16 +354,16 @@ static __device__ __forceinline__ void cta_lsd_sort(LocalSmem& S, uint32_t n, in
             uint32_t ts = 0;
 #pragma unroll 4
             for (int q = 0; q < WPT; ++q) {
-                const uint32_t wv = S.cnt[xpad(tid * WPT + q)];
+                const uint32_t wv = my[q];
                 ts += (wv & 0xffffu) + (wv >> 16);
             }
             uint32_t tot;
             uint32_t run = dev::block_excl_scan(ts, S.scan_tmp, tot);
 #pragma unroll 4
             for (int q = 0; q < WPT; ++q) {
-                const uint32_t wv = S.cnt[xpad(tid * WPT + q)];
+                const uint32_t wv = my[q];
                 const uint32_t lo16 = wv & 0xffffu;
-                S.cnt[xpad(tid * WPT + q)] = run | ((run + lo16) << 16);
+                my[q] = run | ((run + lo16) << 16);
                 run += lo16 + (wv >> 16);
             }
         }
@@ -366,14 +371,14 @@ static __device__ __forceinline__ void cta_lsd_sort(LocalSmem& S, uint32_t n, in
 #pragma unroll
         for (int j = 0; j < kLocalItems; ++j) {
             const uint32_t d = (uint32_t)(k[j] >> sh) & (kLsdDigits - 1);
-            const uint32_t pre = (S.cnt[xpad(d * (kLocalThreads / 2) + (tid >> 1))] >> half) & 0xffffu;
+            const uint32_t pre = (S.cnt[d * 272u + pp] >> half) & 0xffffu;
             const uint32_t r = (rk[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
             S.X[xpad(pre + r)] = k[j];
         }
         __syncthreads();
         if (sh + kLsdBits <= hi) {
 #pragma unroll
-            for (int j = 0; j < kLocalItems; ++j) k[j] = S.X[xpad(tid * kLocalItems + j)];
+            for (int j = 0; j < kLocalItems; ++j) k[j] = S.X[tid * (kLocalItems + 1) + j];  // X[xpad(tid*16+j)]
         }
     }
 }

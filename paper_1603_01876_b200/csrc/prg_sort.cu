@@ -182,13 +182,16 @@ __global__ void __launch_bounds__(kTileThreads, 2) seg_scatter_kernel(
         const int cnt = (int)min((uint64_t)kTile, (uint64_t)sg.size - (uint64_t)ti * kTile);
         const unsigned mask = (1u << sg.bits) - 1u;
         uint64_t k[kTileItems];
+        // all 16 loads first (in flight together), then the counting
 #pragma unroll
         for (int j = 0; j < kTileItems; ++j) {
             const int li = tile_pos<kStable>(j);
-            if (li < cnt) {
-                k[j] = src[base + li];
-                if (!kStable) atomicAdd(&h[(unsigned)(k[j] >> sg.shift) & mask], 1u);
-            }
+            if (li < cnt) k[j] = src[base + li];
+        }
+        if (!kStable) {
+#pragma unroll
+            for (int j = 0; j < kTileItems; ++j)
+                if (tile_pos<kStable>(j) < cnt) atomicAdd(&h[(unsigned)(k[j] >> sg.shift) & mask], 1u);
         }
         const size_t hb = (size_t)seg_tile0[si] * kRadix;
         if (kStable) {

@@ -176,13 +176,16 @@ __global__ void __launch_bounds__(kTileThreads, 2) l1_scatter_kernel(Src src, si
         src.prepare(base, cnt, src_smem);
         __syncthreads();
         uint64_t k[kTileItems];
+        // all 16 loads first (in flight together), then the counting
 #pragma unroll
         for (int j = 0; j < kTileItems; ++j) {
             const int li = tile_pos<kStable>(j);
-            if (li < cnt) {
-                k[j] = src.key(base + li, li, src_smem);
-                if (!kStable) atomicAdd(&h[(unsigned)(k[j] >> shift) & dmask], 1u);
-            }
+            if (li < cnt) k[j] = src.key(base + li, li, src_smem);
+        }
+        if (!kStable) {
+#pragma unroll
+            for (int j = 0; j < kTileItems; ++j)
+                if (tile_pos<kStable>(j) < cnt) atomicAdd(&h[(unsigned)(k[j] >> shift) & dmask], 1u);
         }
         __syncthreads();
         if (kStable) {

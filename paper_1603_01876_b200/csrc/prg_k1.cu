@@ -19,6 +19,7 @@ struct PairKeySrc {
     int scale;
     uint32_t* err;
     static constexpr size_t kSmem = 0;
+    static constexpr int kHistBatch = 4;
     __device__ __forceinline__ void prepare(size_t, int, void*) const {}
     __device__ __forceinline__ uint64_t key(size_t i, int, const void*) const {
         const longlong2 p = uv[i];

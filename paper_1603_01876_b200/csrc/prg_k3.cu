@@ -53,6 +53,7 @@ struct RowClassSrc {
     const uint32_t* ro;
     int sb;
     static constexpr size_t kSmem = 0;
+    static constexpr int kHistBatch = 16;
     __device__ void prepare(size_t, int, void*) const {}
     __device__ __forceinline__ uint64_t key(size_t i, int, const void*) const {
         const uint32_t d = ro[i + 1] - ro[i];
@@ -530,6 +531,7 @@ struct VcClassSrc {
     const uint32_t* vc_len;
     int vb;
     static constexpr size_t kSmem = 0;
+    static constexpr int kHistBatch = 16;
     __device__ void prepare(size_t, int, void*) const {}
     __device__ __forceinline__ uint64_t key(size_t i, int, const void*) const {
         return ((uint64_t)len_class_desc(vc_len[i]) << vb) | i;
@@ -539,6 +541,7 @@ struct VcClassSrc {
 struct KeyArraySrc {
     const unsigned long long* keys;
     static constexpr size_t kSmem = 0;
+    static constexpr int kHistBatch = 16;
     __device__ void prepare(size_t, int, void*) const {}
     __device__ __forceinline__ uint64_t key(size_t i, int, const void*) const { return keys[i]; }
 };

@@ -143,8 +143,15 @@ __global__ void __launch_bounds__(kTileThreads) seg_hist_kernel(
         const uint64_t base = sg.start + (uint64_t)ti * kTile;
         const int cnt = (int)min((uint64_t)kTile, (uint64_t)sg.size - (uint64_t)ti * kTile);
         const unsigned mask = (1u << sg.bits) - 1u;
-        for (int li = threadIdx.x; li < cnt; li += kTileThreads)
-            atomicAdd(&h[(unsigned)(src[base + li] >> sg.shift) & mask], 1u);
+        uint64_t k[kTileItems];
+#pragma unroll
+        for (int j = 0; j < kTileItems; ++j) {
+            const int li = j * kTileThreads + threadIdx.x;
+            if (li < cnt) k[j] = src[base + li];
+        }
+#pragma unroll
+        for (int j = 0; j < kTileItems; ++j)
+            if (j * kTileThreads + (int)threadIdx.x < cnt) atomicAdd(&h[(unsigned)(k[j] >> sg.shift) & mask], 1u);
         __syncthreads();
         // layout: [active seg][digit][tile in seg], packed per segment
         const size_t hb = (size_t)seg_tile0[si] * kRadix;

@@ -43,6 +43,7 @@ struct Seg {
 // Level-1 (whole input) kernels, parameterised by a key source.
 //   Src must provide:
 //     static constexpr size_t kSmem;   // bytes of tile scratch it needs
+//     static constexpr int kHistBatch; // keys loaded ahead in the histogram pass (divides 16)
 //     __device__ void prepare(size_t base, int cnt, void* smem) const;  // all threads; may __syncthreads
 //     __device__ uint64_t key(size_t i, int li, const void* smem) const;  // li = i - base
 // ---------------------------------------------------------------------------
@@ -58,10 +59,20 @@ __global__ void __launch_bounds__(kTileThreads) l1_hist_kernel(Src src, size_t n
         const int cnt = (int)min((size_t)kTile, n - base);
         src.prepare(base, cnt, src_smem);
         __syncthreads();
-#pragma unroll 4
-        for (int j = 0; j < kTileItems; ++j) {
-            const int li = j * kTileThreads + threadIdx.x;
-            if (li < cnt) atomicAdd(&h[(unsigned)(src.key(base + li, li, src_smem) >> shift) & dmask], 1u);
+        // Src::kHistBatch loads in flight, then their counts (measured per source:
+        // 16 for 8-byte key arrays, 4 for the 16-byte edge pairs of K1)
+        constexpr int B = Src::kHistBatch;
+#pragma unroll
+        for (int j0 = 0; j0 < kTileItems; j0 += B) {
+            uint64_t k[B];
+#pragma unroll
+            for (int j = 0; j < B; ++j) {
+                const int li = (j0 + j) * kTileThreads + threadIdx.x;
+                if (li < cnt) k[j] = src.key(base + li, li, src_smem);
+            }
+#pragma unroll
+            for (int j = 0; j < B; ++j)
+                if ((j0 + j) * kTileThreads + (int)threadIdx.x < cnt) atomicAdd(&h[(unsigned)(k[j] >> shift) & dmask], 1u);
         }
         __syncthreads();
         for (int d = threadIdx.x; d < kRadix; d += blockDim.x) hist[(size_t)d * ntiles + t] = h[d];

@@ -227,6 +227,7 @@ struct KeyBuildArgs {
     int sb;
     unsigned long long* keys;
     unsigned long long* exc_key;
+    uint32_t* exc_row;  // [nnz] new row of the exception at CSR position e (only those are written)
     uint32_t* n_exc;
 };
 __global__ void __launch_bounds__(sort::kTileThreads, 3) key_build_kernel(KeyBuildArgs a) {
@@ -265,7 +266,9 @@ __global__ void __launch_bounds__(sort::kTileThreads, 3) key_build_kernel(KeyBui
                 if (!((excm >> j) & 1u)) continue;
                 const int li = j * sort::kTileThreads + threadIdx.x;
                 const uint32_t e = (uint32_t)(base + li);
+                const uint32_t u = srow[rpad(li)];
                 a.exc_key[idx] = ((uint64_t)a.cols[e] << 32) | e;
+                a.exc_row[e] = a.newid ? a.newid[u] : u;
                 ++idx;
             }
         }
@@ -371,25 +374,13 @@ __global__ void suffix_min_down(uint32_t* a, int64_t n1, const uint32_t* part) {
 // In timed mode the SELL only needs "the k-th exception slot of column c" to
 // take one of column c's exceptions: the column sum is the same set of products.
 struct ExcValueDst {
-    const uint32_t* ro;       // CSR row offsets [n+1]
-    const uint32_t* tile_row; // row containing the first entry of each kTile tile
-    uint32_t ntiles;
-    const uint32_t* newid;    // null: identity
+    const uint32_t* exc_row;  // new row of the exception at each CSR position (written by key_build)
     const double* values;
-    int64_t n;
     uint32_t* e_u;    // new row id
     double* e_val;    // value
     __device__ __forceinline__ void store(uint64_t i, uint64_t key, bool, uint64_t) const {
         const uint32_t e = (uint32_t)key;
-        // row u: the last row with ro[u] <= e (rows may be empty); it lies
-        // between the rows holding the first entries of e's tile and the next.
-        const uint32_t t = e / sort::kTile;
-        uint32_t lo = tile_row[t], hi = t + 1 < ntiles ? tile_row[t + 1] + 1 : (uint32_t)n;
-        while (hi - lo > 1) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (ro[mid] <= e) lo = mid; else hi = mid;
-        }
-        e_u[i] = newid ? newid[lo] : lo;
+        e_u[i] = exc_row[e];
         e_val[i] = values[e];
     }
 };
@@ -883,6 +874,7 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
     const uint64_t ngroups = nnz / kCscGroup + 1;
     DevBuf<uint32_t> exc_cnt(ngroups, s);
     DevBuf<unsigned long long> exc_key(nnz ? nnz : 1, s);
+    DevBuf<uint32_t> exc_row(nnz ? nnz : 1, s);  // sparse: written at exception positions only
     DevBuf<uint32_t> n_exc(1, s);
     {
         ProfScope pr("k3_prep_transpose", s);
@@ -896,7 +888,8 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
                 ProfScope pk("k3t_keys", s);
                 KeyBuildArgs ka{A->row_offsets, tile_row.get(), A->cols, A->values, bmin.get(),
                                 mode == 0 ? P.newid.get() : nullptr, mode == 0 ? wdelta.get() : nullptr, n, nnz, P.sb,
-                                reinterpret_cast<unsigned long long*>(ws.keys[0].get()), exc_key.get(), n_exc.get()};
+                                reinterpret_cast<unsigned long long*>(ws.keys[0].get()), exc_key.get(), exc_row.get(),
+                                n_exc.get()};
                 key_build_kernel<<<num_sms() * 3, sort::kTileThreads, row_smem, s>>>(ka);
                 PRG_LAUNCH_CHECK();
             }
@@ -931,8 +924,7 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
     if (P.n_exc) {
         sort::SortWorkspace ws;
         sort::msd_sort(KeyArraySrc{exc_key.get()}, (size_t)P.n_exc, 32 + P.sb,
-                       ExcValueDst{A->row_offsets, tile_row.get(), ntiles, mode == 0 ? P.newid.get() : nullptr,
-                                   A->values, n, P.e_u.get(), P.exc_val.get()},
+                       ExcValueDst{exc_row.get(), A->values, P.e_u.get(), P.exc_val.get()},
                        ws, s, "k3exc");
     }
     if (mode == 1) return;

@@ -244,25 +244,34 @@ __global__ void __launch_bounds__(kT) k2_pass_b(
     uint32_t tile_kh;
     const uint32_t kh_excl = dev::block_excl_scan(nkh, S.scan_u, tile_kh);
 
-    // Decoupled look-back for the tile's global kept-entry base.
-    if (tid == 0) {
+    // Decoupled look-back for the tile's global kept-entry base, by warp 0:
+    // 32 predecessors are inspected at once (sum of aggregates up to the
+    // nearest inclusive prefix).
+    if (tid < 32) {
         uint64_t excl = 0;
         if (t == 0) {
-            atomicExch(&tile_status[0], kFlagInc | tile_kh);
+            if (tid == 0) atomicExch(&tile_status[0], kFlagInc | tile_kh);
         } else {
-            atomicExch(&tile_status[t], kFlagAgg | tile_kh);
-            int64_t k = (int64_t)t - 1;
-            for (;;) {
-                const uint64_t st = *((volatile unsigned long long*)&tile_status[k]);
-                const uint64_t fl = st & ~kValMask;
-                if (fl == 0) continue;
-                excl += st & kValMask;
-                if (fl == kFlagInc) break;
-                --k;
+            if (tid == 0) atomicExch(&tile_status[t], kFlagAgg | tile_kh);
+            for (int64_t k = (int64_t)t - 1;; k -= 32) {
+                const int64_t idx = k - (int64_t)tid;
+                uint64_t st = kFlagInc;  // below tile 0: an empty inclusive prefix
+                if (idx >= 0) {
+                    do {
+                        st = *((volatile unsigned long long*)&tile_status[idx]);
+                    } while ((st & ~kValMask) == 0);
+                }
+                const unsigned incm = __ballot_sync(0xffffffffu, (st & ~kValMask) == kFlagInc);
+                const int first = incm ? __ffs(incm) - 1 : 32;
+                uint64_t v = (int)tid <= first ? (st & kValMask) : 0ull;
+#pragma unroll
+                for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+                excl += v;
+                if (incm) break;
             }
-            atomicExch(&tile_status[t], kFlagInc | (excl + tile_kh));
+            if (tid == 0) atomicExch(&tile_status[t], kFlagInc | (excl + tile_kh));
         }
-        S.tile_base = excl;
+        if (tid == 0) S.tile_base = excl;
     }
 
     // Row sums (kept edges) and run lengths (all edges) into SMEM per head.

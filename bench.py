@@ -322,7 +322,11 @@ def run_ours(args):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_t = float(t.item())
         out["e2e"] = {"value": ws * iters * m / e2e_t, "unit": "edges/s",
+                      # the host CSR the call consumes each step (int64 offsets, int64 cols, f64 values)
                       "h2d_bytes_per_step": 8 * (n + 1) + 16 * nnz, "d2h_bytes_per_step": 8 * n,
+                      # what actually crosses PCIe: the values are reduced on host threads to row
+                      # bases + exceptions while the column indices are in flight
+                      "h2d_wire_bytes_per_step": int(L.prg_last_h2d_bytes()),
                       "api": "prg_k3_pagerank_host (C-ABI, pinned host CSR in, ranks out)",
                       "seconds_per_step": e2e_t}
 

@@ -51,6 +51,12 @@ int32_t prg_device_count(void);
  * regions (k1_sort, k2_filter, k3_spmv, ...) on the stream they ran on;
  * report writes JSON {"name": [count, total_ms]} and returns its length. */
 int64_t prg_launch_count(void);
+
+/* Bytes the last prg_k3_pagerank_host call moved host -> device: its CSR
+ * structure plus, instead of the f64 values, one base value per row and the
+ * entries that differ from it (classified on host threads while the column
+ * indices are in flight). Diagnostics for the bench's e2e record. */
+int64_t prg_last_h2d_bytes(void);
 void prg_profile_enable(int32_t on);
 int64_t prg_profile_report(char* buf, int64_t cap, int32_t reset);
 

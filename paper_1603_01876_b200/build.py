@@ -25,7 +25,8 @@ PYMOD_DIR = os.path.join(PKG, "python", "prpipe")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
+# host code: x86-64-v2 (SSE4.2/POPCNT, every x86 server since ~2009) for the host-side value pass
+NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3", "-Xcompiler", "-march=x86-64-v2",
               "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"] + ARCH
 CU_SOURCES = ["prg_runtime.cu", "prg_sort.cu", "prg_k0.cu", "prg_k1.cu", "prg_k2.cu", "prg_k3.cu",
               "prg_k2_steps.cu", "prg_capi.cu"]

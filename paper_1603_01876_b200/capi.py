@@ -29,7 +29,7 @@ HEADER_SYMBOLS = (
     "prg_k0_generate_device", "prg_k1_sort_device", "prg_k1_sort_host", "prg_k2_filter_device",
     "prg_k2_filter_host", "prg_matrix_info", "prg_matrix_download", "prg_matrix_device_arrays",
     "prg_matrix_from_host", "prg_matrix_destroy", "prg_k3_pagerank_device", "prg_k3_pagerank_host",
-    "prg_init_rank_device", "prg_pagerank_step_device", "prg_launch_count", "prg_profile_enable",
+    "prg_init_rank_device", "prg_pagerank_step_device", "prg_launch_count", "prg_last_h2d_bytes", "prg_profile_enable",
     "prg_profile_report", "prg_build_adjacency_host", "prg_in_degree_host", "prg_zero_columns_host",
     "prg_row_normalize_host", "prg_init_rank_host", "prg_pagerank_step_host", "prg_k3_pagerank_matrix_host",
     "prg_run_to_convergence_host",
@@ -73,6 +73,7 @@ def lib() -> C.CDLL:
             "prg_init_rank_device": (i32, [i64, u64, i32, vp, vp, vp]),
             "prg_pagerank_step_device": (i32, [vp, vp, f64, i32, vp, vp, vp]),
             "prg_launch_count": (i64, []),
+            "prg_last_h2d_bytes": (i64, []),
             "prg_profile_enable": (None, [i32]),
             "prg_profile_report": (i64, [vp, i64, i32]),
             "prg_build_adjacency_host": (i32, [vp, i64, i64, vp, vp, vp, vp]),

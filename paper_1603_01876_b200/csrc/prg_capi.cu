@@ -1,6 +1,15 @@
 // prg_capi.cu — the extern "C" boundary (include/prg.h).
+#include <immintrin.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
+#include <thread>
 #include <type_traits>
 #include <string>
 #include <vector>
@@ -80,6 +89,103 @@ __global__ void narrow_i64(const int64_t* __restrict__ in, int64_t n, int64_t li
     }
 }
 
+// ---------------------------------------------------------------------------
+// Host-buffer K3 (prg_k3_pagerank_host): the CSR crosses PCIe (~55 GB/s) —
+// the bound of the whole call. The f64 values are run-length coded on the
+// host's cores while the column indices are in flight: one bit per entry
+// ("differs, bitwise, from the previous entry") plus the differing values.
+// A stochastic matrix repeats each row's 1/d_out, so at S=24 the 2.1 GB of
+// values cross as 0.14 GB; the device expands them back bit for bit.
+// ---------------------------------------------------------------------------
+int64_t g_last_h2d_bytes = 0;
+
+struct PinnedStage {
+    std::mutex mu;
+    void* p = nullptr;
+    size_t cap = 0;
+    void* get(size_t bytes) {
+        if (bytes > cap) {
+            if (p) cudaFreeHost(p);
+            p = nullptr;
+            cap = 0;
+            PRG_CUDA(cudaMallocHost(&p, bytes));
+            cap = bytes;
+        }
+        return p;
+    }
+};
+PinnedStage& pinned_stage(int which) {
+    static PinnedStage st[2];
+    return st[which];
+}
+
+template <class F>
+void parallel_for(int T, F&& f) {
+    std::vector<std::thread> pool;
+    for (int t = 1; t < T; ++t) pool.emplace_back(f, t);
+    f(0);
+    for (auto& th : pool) th.join();
+}
+
+// Bit i of the result: value k0+i differs (bitwise) from value k0+i-1 (k0 >= 1,
+// 32 entries). AVX2 when the host has it (4 compares per instruction).
+__attribute__((target("avx2"))) uint32_t neq32_avx2(const uint64_t* vb, int64_t k0) {
+    uint32_t eq = 0;
+#pragma GCC unroll 8
+    for (int i = 0; i < 32; i += 4) {
+        const __m256i a = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(vb + k0 + i));
+        const __m256i b = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(vb + k0 + i - 1));
+        eq |= (uint32_t)_mm256_movemask_pd(_mm256_castsi256_pd(_mm256_cmpeq_epi64(a, b))) << i;
+    }
+    return ~eq;
+}
+uint32_t neq32_scalar(const uint64_t* vb, int64_t k0) {
+    uint32_t neq = 0;
+    for (int i = 0; i < 32; ++i) neq |= (uint32_t)(vb[k0 + i] != vb[k0 + i - 1]) << i;
+    return neq;
+}
+const bool g_have_avx2 = __builtin_cpu_supports("avx2");
+
+// Words [w0, w1): bits[w] (bit i: value 32w+i starts a new run; value 0
+// always does) and the run values, in order.
+void rle_values(const double* vals, int64_t nnz, int64_t w0, int64_t w1, uint32_t* bits, std::vector<double>& out) {
+    const uint64_t* vb = reinterpret_cast<const uint64_t*>(vals);
+    for (int64_t w = w0; w < w1; ++w) {
+        const int64_t k0 = w * 32;
+        const int lim = (int)std::min<int64_t>(32, nnz - k0);
+        uint32_t m = 0;
+        if (k0 > 0 && lim == 32) {
+            m = g_have_avx2 ? neq32_avx2(vb, k0) : neq32_scalar(vb, k0);
+        } else {
+            for (int i = 0; i < lim; ++i) m |= (uint32_t)(k0 + i == 0 || vb[k0 + i] != vb[k0 + i - 1]) << i;
+        }
+        bits[w] = m;
+        while (m) {
+            out.push_back(vals[k0 + __builtin_ctz(m)]);
+            m &= m - 1;
+        }
+    }
+}
+
+// values[32w + i] = runs[(set bits at positions <= 32w + i) - 1]; one thread per word.
+__global__ void value_expand_kernel(const uint32_t* __restrict__ bits, const uint32_t* __restrict__ word_base,
+                                    const double* __restrict__ runs, int64_t nnz, double* __restrict__ values) {
+    const int64_t nw = (nnz + 31) / 32;
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nw; w += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t b = bits[w];
+        int64_t cur = (int64_t)word_base[w] - 1;
+        const int lim = (int)min((int64_t)32, nnz - w * 32);
+        for (int i = 0; i < lim; ++i) {
+            cur += (b >> i) & 1u;
+            values[w * 32 + i] = runs[cur];
+        }
+    }
+}
+__global__ void popc_kernel(const uint32_t* __restrict__ bits, int64_t nw, uint32_t* __restrict__ cnt) {
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nw; w += (int64_t)gridDim.x * blockDim.x)
+        cnt[w] = __popc(bits[w]);
+}
+
 void download_u32_as_i64(const uint32_t* d, size_t n, int64_t* h, cudaStream_t s) {
     if (!h || !n) return;
     DevBuf<int64_t> tmp(n, s);
@@ -97,6 +203,7 @@ const char* prg_last_error(void) { return prg::last_error().c_str(); }
 const char* prg_version(void) { return "prg-b200 0.1.0 (sm_100a)"; }
 
 int64_t prg_launch_count(void) { return prg::launch_count(); }
+int64_t prg_last_h2d_bytes(void) { return g_last_h2d_bytes; }
 void prg_profile_enable(int32_t on) { prg::profiling_enable(on != 0); }
 int64_t prg_profile_report(char* buf, int64_t cap, int32_t reset) {
     const std::string s = prg::profile_report(reset != 0);
@@ -394,16 +501,81 @@ prg_status prg_k3_pagerank_host(int64_t n, int64_t nnz, const int64_t* row_offse
                                 const double* values, double damping, int32_t iterations, uint64_t seed,
                                 int32_t mode, double* ranks, double* norm1) {
     return guarded("prg_k3_pagerank_host", [&] {
-        prg_matrix* a = nullptr;
-        prg_status st = prg_matrix_from_host(n, nnz, row_offsets, cols, values, &a);
-        if (st != PRG_OK) throw ApiError{st, prg::last_error()};
-        std::unique_ptr<prg_matrix> own(a);
+        require(ranks != nullptr && row_offsets != nullptr, PRG_ERR_INVALID_ARGUMENT, "null argument");
+        require(n > 0 && nnz >= 0 && (uint64_t)nnz < (1ull << 32) && (uint64_t)n < (1ull << 32),
+                PRG_ERR_INVALID_ARGUMENT, "bad matrix sizes");
+        require(nnz == 0 || (cols != nullptr && values != nullptr), PRG_ERR_INVALID_ARGUMENT, "null argument");
+        require(row_offsets[0] == 0 && row_offsets[n] == nnz, PRG_ERR_INVALID_ARGUMENT,
+                "row_offsets must start at 0 and end at nnz");
         cudaStream_t s = nullptr;
+        const bool dbg = getenv("PRG_E2E_DEBUG") != nullptr;
+        auto now = [] {
+            return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+        };
+        const double t0 = now();
+        auto mat = std::make_unique<prg_matrix>();
+        mat->n = n;
+        mat->nnz = mat->cap = (uint64_t)nnz;
+        mat->row_offsets = dmalloc<uint32_t>((size_t)n + 1);
+        mat->cols = dmalloc<uint32_t>((size_t)nnz);
+        mat->values = dmalloc<double>((size_t)nnz);
+        DevBuf<uint32_t> err(1, s);
+        PRG_CUDA(cudaMemsetAsync(err.get(), 0, 4, s));
+        // 1. structure over PCIe (async when the caller's buffers are pinned) ...
+        DevBuf<int64_t> tro((size_t)n + 1, s), tcol(nnz ? (size_t)nnz : 1, s);
+        PRG_CUDA(cudaMemcpyAsync(tro.get(), row_offsets, (size_t)(n + 1) * 8, cudaMemcpyHostToDevice, s));
+        narrow_i64<<<(unsigned)prg::num_sms() * 4, 1024, 0, s>>>(tro.get(), n + 1, nnz, mat->row_offsets, err.get());
+        PRG_LAUNCH_CHECK();
+        int64_t runs = 0;
+        double t1 = now(), t2 = t1;
+        if (nnz) {
+            PRG_CUDA(cudaMemcpyAsync(tcol.get(), cols, (size_t)nnz * 8, cudaMemcpyHostToDevice, s));
+            narrow_i64<<<(unsigned)prg::num_sms() * 4, 1024, 0, s>>>(tcol.get(), nnz, n - 1, mat->cols, err.get());
+            PRG_LAUNCH_CHECK();
+            // 2. ... while the host run-length codes the values
+            PinnedStage& pb = pinned_stage(0);
+            PinnedStage& pr = pinned_stage(1);
+            std::lock_guard<std::mutex> lock_b(pb.mu), lock_r(pr.mu);
+            const int64_t nw = (nnz + 31) / 32;
+            uint32_t* hbits = static_cast<uint32_t*>(pb.get((size_t)nw * 4));
+            const int T = (int)std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+            std::vector<std::vector<double>> parts((size_t)T);
+            parallel_for(T, [&](int t) { rle_values(values, nnz, nw * t / T, nw * (t + 1) / T, hbits, parts[t]); });
+            std::vector<int64_t> off((size_t)T + 1, 0);
+            for (int t = 0; t < T; ++t) off[t + 1] = off[t] + (int64_t)parts[t].size();
+            runs = off[T];
+            double* hruns = static_cast<double*>(pr.get((size_t)runs * 8));
+            parallel_for(T, [&](int t) { std::memcpy(hruns + off[t], parts[t].data(), parts[t].size() * 8); });
+            t1 = now();
+            DevBuf<uint32_t> dbits((size_t)nw, s), wcnt((size_t)nw, s), wbase((size_t)nw, s);
+            DevBuf<double> druns((size_t)runs, s);
+            PRG_CUDA(cudaMemcpyAsync(dbits.get(), hbits, (size_t)nw * 4, cudaMemcpyHostToDevice, s));
+            PRG_CUDA(cudaMemcpyAsync(druns.get(), hruns, (size_t)runs * 8, cudaMemcpyHostToDevice, s));
+            const unsigned g = (unsigned)prg::num_sms() * 8;
+            popc_kernel<<<g, 1024, 0, s>>>(dbits.get(), nw, wcnt.get());
+            PRG_LAUNCH_CHECK();
+            prg::exclusive_scan_u32(wcnt.get(), wbase.get(), (size_t)nw, nullptr, s);
+            value_expand_kernel<<<g, 256, 0, s>>>(dbits.get(), wbase.get(), druns.get(), nnz, mat->values);
+            PRG_LAUNCH_CHECK();
+            t2 = now();
+            uint32_t h = 0;
+            PRG_CUDA(cudaMemcpyAsync(&h, err.get(), 4, cudaMemcpyDeviceToHost, s));
+            PRG_CUDA(cudaStreamSynchronize(s));  // uploads done: the pinned stages are reused by the next call
+            require(h == 0, PRG_ERR_LABEL_RANGE, "row offsets or column indices out of range");
+        }
+        g_last_h2d_bytes = (n + 1) * 8 + nnz * 8 + (nnz + 31) / 32 * 4 + runs * 8;
+        const double t3 = now();
+        // 3. K3 on the device, ranks back
         DevBuf<double> r((size_t)n, s);
-        st = prg_k3_pagerank_device(a, damping, iterations, seed, mode, r.get(), norm1, s);
+        prg_status st = prg_k3_pagerank_device(mat.get(), damping, iterations, seed, mode, r.get(), norm1, s);
         if (st != PRG_OK) throw ApiError{st, prg::last_error()};
+        const double t4 = now();
         PRG_CUDA(cudaMemcpyAsync(ranks, r.get(), (size_t)n * 8, cudaMemcpyDeviceToHost, s));
         PRG_CUDA(cudaStreamSynchronize(s));
+        if (dbg)
+            fprintf(stderr, "[e2e] host run-length pass %.1f ms | enqueue %.1f | wait uploads %.1f | k3 %.1f | d2h %.1f"
+                    " | total %.1f (runs %lld)\n",
+                    t1 - t0, t2 - t1, now() - t4 > 0 ? t3 - t2 : 0.0, t4 - t3, now() - t4, now() - t0, (long long)runs);
     });
 }
 

@@ -268,6 +268,11 @@ def test_k3_adversarial_matrix(capi, n, seed):
     assert rel_l1(rt, acc) <= K3_ACCURATE_TOL
     rt2, _ = capi.k3_pagerank(mat, seed=seed, mode=0)
     assert np.array_equal(rt2.cpu().numpy().view(np.int64), rt.view(np.int64))  # deterministic
+    # the host-buffer entry point (run-length coded values on the wire) gives the same ranks
+    rh, nh = capi.k3_pagerank_host(n, ro, cols, vals, seed=seed, mode=1)
+    assert np.array_equal(rh.view(np.int64), ref.view(np.int64)) and nh == nref
+    rh0, _ = capi.k3_pagerank_host(n, ro, cols, vals, seed=seed, mode=0)
+    assert np.array_equal(rh0.view(np.int64), rt.view(np.int64))
 
 
 def test_k3_rejects_bad_config(capi):

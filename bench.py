@@ -276,6 +276,7 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "kernel": "k3_spmv (spmv_sell_kernel, one PageRank iteration)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if achieved else None, "traffic": spmv_traffic(),
+                     "traffic_over_alg": (spmv_traffic() / b3_iter) if spmv_traffic() else None,
                      "alg_bytes_per_launch": b3_iter, "avg_launch_ms": spmv_avg, "peak_source": peak_src,
                      # the binding limit in practice: random 8 B gathers through L1TEX
                      "gather_bound": gather_bound(nnz, spmv_avg, clk)},

@@ -521,7 +521,27 @@ prg_status prg_k3_pagerank_host(int64_t n, int64_t nnz, const int64_t* row_offse
         mat->values = dmalloc<double>((size_t)nnz);
         DevBuf<uint32_t> err(1, s);
         PRG_CUDA(cudaMemsetAsync(err.get(), 0, 4, s));
-        // 1. structure over PCIe (async when the caller's buffers are pinned) ...
+        // 1. the host's cores run-length code the values (worker threads) ...
+        PinnedStage& pb = pinned_stage(0);
+        PinnedStage& pr = pinned_stage(1);
+        std::lock_guard<std::mutex> lock_b(pb.mu), lock_r(pr.mu);
+        const int64_t nw = (nnz + 31) / 32;
+        uint32_t* hbits = nnz ? static_cast<uint32_t*>(pb.get((size_t)nw * 4)) : nullptr;
+        const int T = (int)std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+        std::vector<std::vector<double>> parts((size_t)T);
+        std::vector<std::thread> workers;
+        struct Joiner {  // never leave a worker running (an exception would terminate)
+            std::vector<std::thread>& w;
+            ~Joiner() {
+                for (auto& t : w)
+                    if (t.joinable()) t.join();
+            }
+        } joiner{workers};
+        if (nnz)
+            for (int t = 0; t < T; ++t)
+                workers.emplace_back([&, t] { rle_values(values, nnz, nw * t / T, nw * (t + 1) / T, hbits, parts[t]); });
+        // 2. ... while this thread ships the structure over PCIe (async when the
+        // caller's buffers are pinned; staged, but still concurrent, when pageable)
         DevBuf<int64_t> tro((size_t)n + 1, s), tcol(nnz ? (size_t)nnz : 1, s);
         PRG_CUDA(cudaMemcpyAsync(tro.get(), row_offsets, (size_t)(n + 1) * 8, cudaMemcpyHostToDevice, s));
         narrow_i64<<<(unsigned)prg::num_sms() * 4, 1024, 0, s>>>(tro.get(), n + 1, nnz, mat->row_offsets, err.get());
@@ -532,15 +552,7 @@ prg_status prg_k3_pagerank_host(int64_t n, int64_t nnz, const int64_t* row_offse
             PRG_CUDA(cudaMemcpyAsync(tcol.get(), cols, (size_t)nnz * 8, cudaMemcpyHostToDevice, s));
             narrow_i64<<<(unsigned)prg::num_sms() * 4, 1024, 0, s>>>(tcol.get(), nnz, n - 1, mat->cols, err.get());
             PRG_LAUNCH_CHECK();
-            // 2. ... while the host run-length codes the values
-            PinnedStage& pb = pinned_stage(0);
-            PinnedStage& pr = pinned_stage(1);
-            std::lock_guard<std::mutex> lock_b(pb.mu), lock_r(pr.mu);
-            const int64_t nw = (nnz + 31) / 32;
-            uint32_t* hbits = static_cast<uint32_t*>(pb.get((size_t)nw * 4));
-            const int T = (int)std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
-            std::vector<std::vector<double>> parts((size_t)T);
-            parallel_for(T, [&](int t) { rle_values(values, nnz, nw * t / T, nw * (t + 1) / T, hbits, parts[t]); });
+            for (auto& w : workers) w.join();
             std::vector<int64_t> off((size_t)T + 1, 0);
             for (int t = 0; t < T; ++t) off[t + 1] = off[t] + (int64_t)parts[t].size();
             runs = off[T];

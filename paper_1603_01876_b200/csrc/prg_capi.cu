@@ -167,18 +167,16 @@ void rle_values(const double* vals, int64_t nnz, int64_t w0, int64_t w1, uint32_
     }
 }
 
-// values[32w + i] = runs[(set bits at positions <= 32w + i) - 1]; one thread per word.
+// values[k] = runs[(set bits at positions <= k) - 1]: one warp per bit word,
+// one lane per entry (coalesced stores; the word and its base are broadcast).
 __global__ void value_expand_kernel(const uint32_t* __restrict__ bits, const uint32_t* __restrict__ word_base,
                                     const double* __restrict__ runs, int64_t nnz, double* __restrict__ values) {
-    const int64_t nw = (nnz + 31) / 32;
-    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nw; w += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t lane = threadIdx.x & 31u;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t w = k >> 5;
         const uint32_t b = bits[w];
-        int64_t cur = (int64_t)word_base[w] - 1;
-        const int lim = (int)min((int64_t)32, nnz - w * 32);
-        for (int i = 0; i < lim; ++i) {
-            cur += (b >> i) & 1u;
-            values[w * 32 + i] = runs[cur];
-        }
+        const uint32_t upto = b & (0xffffffffu >> (31u - lane));  // bits at positions <= lane
+        values[k] = runs[(int64_t)word_base[w] + __popc(upto) - 1];
     }
 }
 __global__ void popc_kernel(const uint32_t* __restrict__ bits, int64_t nw, uint32_t* __restrict__ cnt) {
@@ -567,7 +565,7 @@ prg_status prg_k3_pagerank_host(int64_t n, int64_t nnz, const int64_t* row_offse
             popc_kernel<<<g, 1024, 0, s>>>(dbits.get(), nw, wcnt.get());
             PRG_LAUNCH_CHECK();
             prg::exclusive_scan_u32(wcnt.get(), wbase.get(), (size_t)nw, nullptr, s);
-            value_expand_kernel<<<g, 256, 0, s>>>(dbits.get(), wbase.get(), druns.get(), nnz, mat->values);
+            value_expand_kernel<<<g, 1024, 0, s>>>(dbits.get(), wbase.get(), druns.get(), nnz, mat->values);
             PRG_LAUNCH_CHECK();
             t2 = now();
             uint32_t h = 0;

@@ -52,6 +52,12 @@ __host__ __device__ inline int bits_for(int64_t n) {
 struct RowClassSrc {
     const uint32_t* ro;
     int sb;
+    // Within a degree class, rows are ordered by the top fb bits of their first
+    // (smallest) column: rows feeding the same columns get nearby new ids, so a
+    // column's gathers reuse L1 lines (SpMV 1.22 -> 1.16 ms at S=24; the class
+    // alone, or 8 bits of the column, gave nothing).
+    const uint32_t* cols;  // null: class only
+    int fb;
     static constexpr size_t kSmem = 0;
     static constexpr int kHistBatch = 16;
     __device__ void prepare(size_t, int, void*) const {}
@@ -63,6 +69,10 @@ struct RowClassSrc {
             const int lg = 31 - __clz(d);
             const uint32_t q = lg >= 2 ? (d >> (lg - 2)) & 3u : (lg == 1 ? (d & 1u) << 1 : 0u);
             cls = 127u - (uint32_t)(lg * 4) - q;
+        }
+        if (cols) {
+            const uint32_t fc = d ? (sb > fb ? cols[ro[i]] >> (sb - fb) : cols[ro[i]]) : 0u;
+            return ((uint64_t)cls << (sb + fb)) | ((uint64_t)fc << sb) | i;
         }
         return ((uint64_t)cls << sb) | i;
     }
@@ -824,7 +834,12 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
             count_nondangling<<<g, 1024, 0, s>>>(A->row_offsets, n, cnt.get());
             PRG_LAUNCH_CHECK();
             sort::SortWorkspace ws;
-            sort::msd_sort(RowClassSrc{A->row_offsets, P.sb}, (size_t)n, P.sb + 8,
+            static int ro_bits = -1;  // PRG_ROW_ORDER_BITS: column bits of the row order (default 16, 0 = off)
+            if (ro_bits < 0) { const char* e = getenv("PRG_ROW_ORDER_BITS"); ro_bits = e ? atoi(e) : 16; }
+            const int ro_exp = ro_bits > 0;
+            const int fb = ro_exp ? std::min(P.sb, std::min(ro_bits, 24)) : 0;
+            sort::msd_sort(RowClassSrc{A->row_offsets, P.sb, ro_exp ? A->cols : nullptr, fb}, (size_t)n,
+                           P.sb + 8 + fb,
                            PermDst{P.pinv.get(), P.newid.get(), P.sb}, ws, s, "k3rows", /*payload_bits=*/P.sb,
                            /*stable=*/true);
             unsigned long long h = 0;

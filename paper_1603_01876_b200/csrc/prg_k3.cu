@@ -642,15 +642,76 @@ __global__ void permute_orig_kernel(const double* __restrict__ r, const uint32_t
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n_nd; j += (int64_t)gridDim.x * blockDim.x)
         s[j] = __dmul_rn(r[pinv[j]], bval[j]);
 }
-__global__ void permute_sell_kernel(const double* __restrict__ y, const uint32_t* __restrict__ spos,
-                                    const double* __restrict__ bgp, const double* __restrict__ bval, int64_t n_nd,
-                                    double* __restrict__ s) {
-    const double bg = bgp[2];
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n_nd; j += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t p = spos[j];
-        s[j] = __dmul_rn(p == kEmpty ? bg : y[p], bval[j]);
+// s for one iteration, in one launch: s[j] = r(j) * b[j] for rows j < n_nd and
+// s[n_nd + e] = r(u_e) * value_e for exception e, where r(x) is the previous
+// iterate of new row x (first step: r0 in the original order; then y in SELL
+// order, or bg for an empty column).
+struct GatherArgs {
+    const double* r0;      // first step (original order) or null
+    const uint32_t* pinv;
+    const double* y;       // previous iterate, SELL order
+    const uint32_t* spos;  // new row -> SELL position of its column (kEmpty: empty)
+    const double* bgp;     // [2] = bg of the previous iterate
+    const double* bval;
+    const uint32_t* e_u;
+    const double* e_val;
+    int64_t n_nd;
+    uint32_t n_exc;
+    double* s;
+};
+__global__ void gather_s_kernel(GatherArgs a) {
+    const double bg = a.bgp[2];
+    const int64_t tot = a.n_nd + a.n_exc;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < tot; j += (int64_t)gridDim.x * blockDim.x) {
+        const bool row = j < a.n_nd;
+        const uint32_t x = row ? (uint32_t)j : a.e_u[j - a.n_nd];
+        double r;
+        if (a.r0) r = a.r0[a.pinv[x]];
+        else {
+            const uint32_t p = a.spos[x];
+            r = p == kEmpty ? bg : a.y[p];
+        }
+        a.s[j] = __dmul_rn(r, row ? a.bval[j] : a.e_val[j - a.n_nd]);
     }
 }
+
+// Σ of the iterate, deterministic two-level tree: block b sums slice sums
+// [b*chunk, (b+1)*chunk) and split-column values likewise; one warp adds the
+// block partials (sell_sum_final).
+constexpr int kSumBlocks = 64;
+__global__ void sell_sum_part(const double* __restrict__ slice_sum, uint32_t nslices, const double* __restrict__ y,
+                              const uint32_t* __restrict__ split_pos, const uint32_t* __restrict__ n_split,
+                              double* __restrict__ part) {
+    __shared__ double ws[32];
+    const uint32_t ns = *n_split;
+    const uint32_t c1 = (nslices + gridDim.x - 1) / gridDim.x, c2 = (ns + gridDim.x - 1) / gridDim.x;
+    double a = 0.0;
+    for (uint32_t i = blockIdx.x * c1 + threadIdx.x; i < min(nslices, (blockIdx.x + 1) * c1); i += blockDim.x)
+        a = __dadd_rn(a, slice_sum[i]);
+    for (uint32_t i = blockIdx.x * c2 + threadIdx.x; i < min(ns, (blockIdx.x + 1) * c2); i += blockDim.x)
+        a = __dadd_rn(a, y[split_pos[i]]);
+    a = dev::warp_sum_f64(a);
+    if (dev::lane_id() == 0) ws[dev::warp_id()] = a;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const double v = dev::warp_sum_f64(threadIdx.x < blockDim.x / 32 ? ws[threadIdx.x] : 0.0);
+        if (threadIdx.x == 0) part[blockIdx.x] = v;
+    }
+}
+__global__ void sell_sum_final(const double* __restrict__ part, int np, double n_empty, double bgf,
+                               double* __restrict__ out) {
+    double v = 0.0;
+    for (int i = threadIdx.x; i < np; i += 32) v = __dadd_rn(v, part[i]);
+    v = dev::warp_sum_f64(v);
+    if (threadIdx.x == 0) {
+        const double bg_cur = out[1];
+        const double tot = __dadd_rn(v, __dmul_rn(n_empty, bg_cur));
+        out[0] = tot;
+        out[2] = bg_cur;
+        out[1] = __dmul_rn(bgf, tot);
+    }
+}
+
 // Final un-permutation: ranks[c] = y[spos_col[c]] or bg.
 __global__ void unpermute_kernel(const double* __restrict__ y, const uint32_t* __restrict__ spos_col,
                                  const double* __restrict__ bgp, int64_t n, double* __restrict__ out) {
@@ -680,31 +741,6 @@ struct SellArgs {
     double damping;
 };
 
-// Exception products for this iteration: exc_x[j] = r_prev(u_j) * value_j for
-// the CSC-ordered exception j; the SELL entry of that exception gathers it.
-struct ExcArgs {
-    const uint32_t* e_u;
-    const double* e_val;
-    uint32_t ne;
-    const double* r0;       // previous iterate in original order (first step) or null
-    const uint32_t* pinv;
-    const uint32_t* spos;
-    const double* y_prev;
-    const double* bgp;      // [2] = bg of the previous iterate
-    double* exc_x;
-};
-__global__ void exc_products_kernel(ExcArgs a) {
-    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < a.ne; j += gridDim.x * blockDim.x) {
-        const uint32_t u = a.e_u[j];
-        double r;
-        if (a.r0) r = a.r0[a.pinv[u]];
-        else {
-            const uint32_t p = a.spos[u];
-            r = p == kEmpty ? a.bgp[2] : a.y_prev[p];
-        }
-        a.exc_x[j] = __dmul_rn(r, a.e_val[j]);
-    }
-}
 // 64 warps per SM and no shared-memory staging: measured on B200 (S=24) the L1
 // caches the hot, degree-ordered head of s by itself, and occupancy (requests
 // in flight) matters more than a software-managed hot set (1.9 ms vs 3.3 ms).
@@ -762,30 +798,6 @@ __global__ void __launch_bounds__(kSpmvThreads, 2) spmv_sell_kernel(SellArgs a) 
     }
 }
 
-// Sum of the iterate: tree(slice sums) + tree(split-column values) + n_empty*bg.
-__global__ void sell_sum_kernel(const double* __restrict__ slice_sum, uint32_t nslices, const double* __restrict__ y,
-                                const uint32_t* __restrict__ split_pos, const uint32_t* __restrict__ n_split,
-                                double n_empty, double bgf, double* __restrict__ out) {
-    __shared__ double ws[32];
-    const uint32_t ns = *n_split;
-    double a = 0.0, b = 0.0;
-    for (uint32_t i = threadIdx.x; i < nslices; i += 1024) a = __dadd_rn(a, slice_sum[i]);
-    for (uint32_t i = threadIdx.x; i < ns; i += 1024) b = __dadd_rn(b, y[split_pos[i]]);
-    a = dev::warp_sum_f64(a);
-    b = dev::warp_sum_f64(b);
-    if (dev::lane_id() == 0) ws[dev::warp_id()] = __dadd_rn(a, b);
-    __syncthreads();
-    if (threadIdx.x < 32) {
-        double v = dev::warp_sum_f64(ws[threadIdx.x]);
-        if (threadIdx.x == 0) {
-            const double bg_cur = out[1];
-            const double tot = __dadd_rn(v, __dmul_rn(n_empty, bg_cur));
-            out[0] = tot;
-            out[2] = bg_cur;
-            out[1] = __dmul_rn(bgf, tot);
-        }
-    }
-}
 
 __global__ void count_set_kernel(const uint32_t* __restrict__ a, int64_t n, uint32_t* __restrict__ out) {
     uint32_t c = 0;
@@ -1096,21 +1108,16 @@ void iterate(const K3Plan& P, const double* r_in, double* r_out, int iters, doub
     const uint32_t NP = P.nslices * 32;
     // s = [row-scaled iterate (SELL row order, n_nd) | exception products (n_exc)]
     DevBuf<double> sbuf((size_t)std::max<int64_t>(P.n_nd + P.n_exc, 1), s), y0(NP ? NP : 1, s), y1(NP ? NP : 1, s),
-        slice_sum(P.nslices ? P.nslices : 1, s);
+        slice_sum(P.nslices ? P.nslices : 1, s), sum_part(kSumBlocks, s);
     double* ys[2] = {y0.get(), y1.get()};
     for (int it = 0; it < iters; ++it) {
         double* y = ys[it & 1];
         const double* yp = ys[(it & 1) ^ 1];
-        if (P.n_nd) {
+        {
             ProfScope pp("k3_permute", s);
-            if (it == 0) permute_orig_kernel<<<g, 1024, 0, s>>>(r_in, P.pinv.get(), P.bval.get(), P.n_nd, sbuf.get());
-            else permute_sell_kernel<<<g, 1024, 0, s>>>(yp, P.spos.get(), S.out.get(), P.bval.get(), P.n_nd, sbuf.get());
-            PRG_LAUNCH_CHECK();
-        }
-        if (P.n_exc) {
-            ExcArgs ea{P.e_u.get(), P.exc_val.get(), P.n_exc, it == 0 ? r_in : nullptr, P.pinv.get(), P.spos.get(), yp,
-                       S.out.get(), sbuf.get() + P.n_nd};
-            exc_products_kernel<<<g, 256, 0, s>>>(ea);
+            GatherArgs ga{it == 0 ? r_in : nullptr, P.pinv.get(), yp, P.spos.get(), S.out.get(), P.bval.get(),
+                          P.e_u.get(), P.exc_val.get(), P.n_nd, P.n_exc, sbuf.get()};
+            if (P.n_nd + P.n_exc) gather_s_kernel<<<g, 1024, 0, s>>>(ga);
             PRG_LAUNCH_CHECK();
         }
         SellArgs a;
@@ -1137,8 +1144,9 @@ void iterate(const K3Plan& P, const double* r_in, double* r_out, int iters, doub
             else spmv_sell_kernel<4><<<num_sms() * 2, kSpmvThreads, 0, s>>>(a);
             PRG_LAUNCH_CHECK();
         }
-        sell_sum_kernel<<<1, 1024, 0, s>>>(slice_sum.get(), P.nslices, y, P.split_pos.get(), P.n_split.get(),
-                                           (double)P.n_empty, bgf, S.out.get());
+        sell_sum_part<<<kSumBlocks, 1024, 0, s>>>(slice_sum.get(), P.nslices, y, P.split_pos.get(), P.n_split.get(),
+                                                  sum_part.get());
+        sell_sum_final<<<1, 32, 0, s>>>(sum_part.get(), kSumBlocks, (double)P.n_empty, bgf, S.out.get());
         PRG_LAUNCH_CHECK();
     }
     unpermute_kernel<<<g, 1024, 0, s>>>(ys[(iters - 1) & 1], P.spos_col.get(), S.out.get(), n, r_out);

@@ -78,6 +78,28 @@ struct RowClassSrc {
     }
 };
 
+__global__ void nondangling_flag_kernel(const uint32_t* __restrict__ ro, int64_t n, uint32_t* __restrict__ flag) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        flag[i] = ro[i + 1] > ro[i];
+}
+// Non-dangling row i -> its sort key at its rank pos[i]; dangling row i -> new
+// id n_nd + (its rank among the dangling rows), written directly.
+template <class Src>
+__global__ void row_keys_kernel(Src src, int64_t n, const uint32_t* __restrict__ pos,
+                                unsigned long long* __restrict__ keys, uint32_t* __restrict__ pinv,
+                                uint32_t* __restrict__ newid, uint32_t n_nd) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t p = pos[i];
+        if (pos[i + 1] > p) {
+            keys[p] = src.key((size_t)i, 0, nullptr);
+        } else {
+            const uint32_t id = n_nd + (uint32_t)i - p;
+            pinv[id] = (uint32_t)i;
+            newid[i] = id;
+        }
+    }
+}
+
 struct PermDst {
     uint32_t* pinv;   // new id -> original row
     uint32_t* newid;  // original row -> new id
@@ -96,13 +118,6 @@ __global__ void iota_kernel(uint32_t* a, uint32_t* b, int64_t n) {
     }
 }
 
-__global__ void count_nondangling(const uint32_t* __restrict__ ro, int64_t n, unsigned long long* out) {
-    uint32_t c = 0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        c += ro[i + 1] > ro[i];
-    c = __reduce_add_sync(0xffffffffu, c);
-    if (dev::lane_id() == 0 && c) atomicAdd(out, (unsigned long long)c);
-}
 
 // ---------------------------------------------------------------------------
 // CSR tile expansion: row id of every entry of a tile of nnz.
@@ -841,23 +856,31 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
     {
         ProfScope pr("k3_prep_rows", s);
         if (mode == 0) {
-            DevBuf<unsigned long long> cnt(1, s);
-            PRG_CUDA(cudaMemsetAsync(cnt.get(), 0, 8, s));
-            count_nondangling<<<g, 1024, 0, s>>>(A->row_offsets, n, cnt.get());
+            // Dangling rows keep their relative order after all others (they are
+            // never gathered); only the non-dangling rows are sorted.
+            DevBuf<uint32_t> flag((size_t)n, s), pos((size_t)n + 1, s);
+            nondangling_flag_kernel<<<g, 1024, 0, s>>>(A->row_offsets, n, flag.get());
             PRG_LAUNCH_CHECK();
-            sort::SortWorkspace ws;
+            exclusive_scan_u32(flag.get(), pos.get(), (size_t)n, pos.get() + n, s);
+            uint32_t h = 0;
+            PRG_CUDA(cudaMemcpyAsync(&h, pos.get() + n, 4, cudaMemcpyDeviceToHost, s));
+            PRG_CUDA(cudaStreamSynchronize(s));
+            P.n_nd = (int64_t)h;
             static int ro_bits = -1;  // PRG_ROW_ORDER_BITS: column bits of the row order (default 16, 0 = off)
             if (ro_bits < 0) { const char* e = getenv("PRG_ROW_ORDER_BITS"); ro_bits = e ? atoi(e) : 16; }
             const int ro_exp = ro_bits > 0;
             const int fb = ro_exp ? std::min(P.sb, std::min(ro_bits, 24)) : 0;
-            sort::msd_sort(RowClassSrc{A->row_offsets, P.sb, ro_exp ? A->cols : nullptr, fb}, (size_t)n,
-                           P.sb + 8 + fb,
-                           PermDst{P.pinv.get(), P.newid.get(), P.sb}, ws, s, "k3rows", /*payload_bits=*/P.sb,
-                           /*stable=*/true);
-            unsigned long long h = 0;
-            PRG_CUDA(cudaMemcpyAsync(&h, cnt.get(), 8, cudaMemcpyDeviceToHost, s));
-            PRG_CUDA(cudaStreamSynchronize(s));
-            P.n_nd = (int64_t)h;
+            DevBuf<unsigned long long> keys((size_t)std::max<int64_t>(P.n_nd, 1), s);
+            row_keys_kernel<<<g, 1024, 0, s>>>(
+                RowClassSrc{A->row_offsets, P.sb, ro_exp ? A->cols : nullptr, fb}, n, pos.get(), keys.get(),
+                P.pinv.get(), P.newid.get(), (uint32_t)P.n_nd);
+            PRG_LAUNCH_CHECK();
+            if (P.n_nd) {
+                sort::SortWorkspace ws;
+                sort::msd_sort(KeyArraySrc{keys.get()}, (size_t)P.n_nd, P.sb + 8 + fb,
+                               PermDst{P.pinv.get(), P.newid.get(), P.sb}, ws, s, "k3rows", /*payload_bits=*/P.sb,
+                               /*stable=*/true);
+            }
         } else {
             iota_kernel<<<g, 1024, 0, s>>>(P.pinv.get(), P.newid.get(), n);
             PRG_LAUNCH_CHECK();

@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) seg_scatter_kernel(
             // off is relative to the concatenation of active segments
             if (threadIdx.x < kRadix)
                 gbase[threadIdx.x] = sg.start + (off[hb + (size_t)threadIdx.x * seg_nt + ti] - e0);
-            stable_tile_scatter(k, cnt, sg.shift, sg.bits, wc, lstart, scan_tmp, skeys);
+            stable_tile_scatter<false>(k, cnt, sg.shift, sg.bits, wc, lstart, scan_tmp, skeys);
         } else {
             __syncthreads();
             uint32_t v = threadIdx.x < kRadix ? h[threadIdx.x] : 0u, tot;

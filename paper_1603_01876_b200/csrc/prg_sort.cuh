@@ -16,7 +16,8 @@
 // memory (kLocalCap keys); the local stage then sorts each segment in SMEM with
 // a stable LSD over the segment's varying bits (5-bit digits, thread-private
 // packed counters). An 8-bit ballot-ranked local pass measured slower (K1
-// local 6.3 -> 8.4 ms): instruction-bound on the ballots.
+// local 6.3 -> 8.4 ms): instruction-bound on the ballots; with __match_any_sync
+// peers instead of ballots it is still slower (5.8 -> 9.0 ms).
 // For reference, CUB's onesweep DeviceRadixSort on this B200 takes 16.6 ms for
 // 2^28 48-bit keys; K1 (2^28 pairs in and out) takes 13.1 ms here.
 #pragma once

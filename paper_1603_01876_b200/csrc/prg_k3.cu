@@ -751,6 +751,7 @@ struct SellArgs {
     uint32_t* arrive;            // [n] per split column, never reset
     double* slice_sum;           // [nslices]
     const double* bgp;           // [1] = bg of this step
+    uint32_t* next_slice;        // work counter of this launch (starts at 0)
     int64_t n_nd;
     uint32_t nslices;
     double damping;
@@ -764,8 +765,13 @@ __global__ void __launch_bounds__(kSpmvThreads, 2) spmv_sell_kernel(SellArgs a) 
     const unsigned lane = dev::lane_id();
     const double bg = a.bgp[1];
     const uint64_t pol_stream = dev::policy_evict_first(), pol_keep = dev::policy_evict_last();
-    const uint32_t nwarps = gridDim.x * (kSpmvThreads / 32);
-    for (uint32_t sl = blockIdx.x * (kSpmvThreads / 32) + dev::warp_id(); sl < a.nslices; sl += nwarps) {
+    // Slices are handed out dynamically, longest first (they are sorted by length
+    // class): a static round-robin left some SMs with twice the average work.
+    for (;;) {
+        uint32_t sl = 0;
+        if (lane == 0) sl = atomicAdd(a.next_slice, 1u);
+        sl = __shfl_sync(0xffffffffu, sl, 0);
+        if (sl >= a.nslices) break;
         const uint32_t pos = sl * 32 + lane;
         const uint32_t len = a.lane_len[pos];
         const uint32_t base = a.slice_ptr[sl];
@@ -1132,6 +1138,8 @@ void iterate(const K3Plan& P, const double* r_in, double* r_out, int iters, doub
     // s = [row-scaled iterate (SELL row order, n_nd) | exception products (n_exc)]
     DevBuf<double> sbuf((size_t)std::max<int64_t>(P.n_nd + P.n_exc, 1), s), y0(NP ? NP : 1, s), y1(NP ? NP : 1, s),
         slice_sum(P.nslices ? P.nslices : 1, s), sum_part(kSumBlocks, s);
+    DevBuf<uint32_t> slice_ctr((size_t)std::max(iters, 1), s);
+    PRG_CUDA(cudaMemsetAsync(slice_ctr.get(), 0, (size_t)std::max(iters, 1) * 4, s));
     double* ys[2] = {y0.get(), y1.get()};
     for (int it = 0; it < iters; ++it) {
         double* y = ys[it & 1];
@@ -1157,6 +1165,7 @@ void iterate(const K3Plan& P, const double* r_in, double* r_out, int iters, doub
         a.arrive = P.arrive.get();
         a.slice_sum = slice_sum.get();
         a.bgp = S.out.get();
+        a.next_slice = slice_ctr.get() + it;
         a.n_nd = P.n_nd;
         a.nslices = P.nslices;
         a.damping = damping;

@@ -74,7 +74,9 @@ def spmv_traffic():
 
 
 # Random 8-byte gathers from an L2-resident vector: ~1.0 line/clk/SM measured
-# on this B200 (tools/microbench/mb2.cu); every SpMV entry is one such gather.
+# on this B200 (tools/microbench/mb2.cu) with no locality between lanes or in
+# time; every SpMV entry is one gather. Above 1.0 = the row/column ordering
+# turned gathers into L1 hits.
 GATHER_LINES_PER_CLK_SM = 1.0
 
 
@@ -85,8 +87,8 @@ def gather_bound(nnz, spmv_ms, clk):
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     rate = nnz / (spmv_ms * 1e-3) / (sms * clk["sm_mhz"] * 1e6)
     return {"gathers_per_launch": int(nnz), "achieved_per_clk_sm": rate,
-            "peak_per_clk_sm": GATHER_LINES_PER_CLK_SM, "frac": rate / GATHER_LINES_PER_CLK_SM,
-            "peak_source": "tools/microbench/mb2.cu random-gather sweep (64 MB working set)"}
+            "random_gather_per_clk_sm": GATHER_LINES_PER_CLK_SM, "ratio": rate / GATHER_LINES_PER_CLK_SM,
+            "source": "tools/microbench/mb2.cu random-gather sweep (64 MB working set, no locality)"}
 
 
 def alg_bytes(n, m, nnz, iters):
@@ -278,8 +280,8 @@ def run_ours(args):
                      "frac": achieved / peak if achieved else None, "traffic": spmv_traffic(),
                      "traffic_over_alg": (spmv_traffic() / b3_iter) if spmv_traffic() else None,
                      "alg_bytes_per_launch": b3_iter, "avg_launch_ms": spmv_avg, "peak_source": peak_src,
-                     # the binding limit in practice: random 8 B gathers through L1TEX
-                     "gather_bound": gather_bound(nnz, spmv_avg, clk)},
+                     # the SpMV's real currency: 8 B gathers through L1TEX, vs a random-gather rate
+                     "gather_rate": gather_bound(nnz, spmv_avg, clk)},
         "stage_roofline": {
             "k1_sort": {"alg_bytes": b1, "achieved_gbs": b1 / (k1_ms * 1e-3) / 1e9,
                         "frac": b1 / (k1_ms * 1e-3) / 1e9 / peak},

@@ -14,47 +14,74 @@ namespace prg::sort {
 // count of final segments (and their fixed per-segment cost) low. Children
 // larger than the cap become active for the next level (or final, if no key
 // bits are left: all their keys are equal).
-__device__ void emit_children(const uint64_t* child_start, const uint32_t* child_size, int nchild,
-                              uint8_t buf, int next_shift, int next_bits, Seg* __restrict__ next,
-                              uint32_t* __restrict__ n_next, Seg* __restrict__ fin, uint32_t* __restrict__ n_fin) {
+// Two passes over the children by one thread: the first only counts what will
+// be emitted, one atomic per list reserves the slots, the second writes them
+// (a returning atomic per emitted segment serialised ~1 us each).
+template <bool kWrite>
+__device__ __forceinline__ void emit_pass(const uint64_t* child_start, const uint32_t* child_size, int nchild,
+                                          uint8_t buf, int next_shift, int next_bits, Seg* __restrict__ next,
+                                          uint32_t& i_next, Seg* __restrict__ fin, uint32_t& i_fin) {
     Seg run;
     run.size = 0;
     run.buf = buf;
     run.bits = 0;
     run.shift = 0;
+    run.start = 0;
     for (int d = 0; d < nchild; ++d) {
         const uint32_t sz = child_size[d];
         if (sz == 0) continue;
         if (sz > (uint32_t)kLocalCap) {
-            if (run.size) { fin[atomicAdd(n_fin, 1u)] = run; run.size = 0; }
-            Seg c;
-            c.start = child_start[d];
-            c.size = sz;
-            c.buf = buf;
-            c.bits = (uint8_t)next_bits;
-            c.shift = (uint16_t)next_shift;
+            if (run.size) {
+                if (kWrite) fin[i_fin] = run;
+                ++i_fin;
+                run.size = 0;
+            }
+            Seg ch;
+            ch.start = child_start[d];
+            ch.size = sz;
+            ch.buf = buf;
+            ch.bits = (uint8_t)next_bits;
+            ch.shift = (uint16_t)next_shift;
             if (next_bits == 0) {
                 // no bits left: the keys are equal above the payload, so the
                 // child is already in order — hand it out in cap-sized pieces
                 // so no single CTA streams a huge run.
                 const uint32_t np = (sz + kLocalCap - 1) / kLocalCap;
-                const uint32_t f0 = atomicAdd(n_fin, np);  // one reservation, plain stores
-                for (uint32_t q = 0; q < np; ++q) {
-                    Seg p = c;
-                    p.start = c.start + (uint64_t)q * kLocalCap;
-                    p.size = min((uint32_t)kLocalCap, sz - q * (uint32_t)kLocalCap);
-                    fin[f0 + q] = p;
-                }
+                if (kWrite)
+                    for (uint32_t q = 0; q < np; ++q) {
+                        Seg p = ch;
+                        p.start = ch.start + (uint64_t)q * kLocalCap;
+                        p.size = min((uint32_t)kLocalCap, sz - q * (uint32_t)kLocalCap);
+                        fin[i_fin + q] = p;
+                    }
+                i_fin += np;
             } else {
-                next[atomicAdd(n_next, 1u)] = c;
+                if (kWrite) next[i_next] = ch;
+                ++i_next;
             }
             continue;
         }
-        if (run.size && run.size + sz > (uint32_t)kLocalCap) { fin[atomicAdd(n_fin, 1u)] = run; run.size = 0; }
+        if (run.size && run.size + sz > (uint32_t)kLocalCap) {
+            if (kWrite) fin[i_fin] = run;
+            ++i_fin;
+            run.size = 0;
+        }
         if (run.size == 0) run.start = child_start[d];
         run.size += sz;
     }
-    if (run.size) fin[atomicAdd(n_fin, 1u)] = run;
+    if (run.size) {
+        if (kWrite) fin[i_fin] = run;
+        ++i_fin;
+    }
+}
+
+__device__ void emit_children(const uint64_t* child_start, const uint32_t* child_size, int nchild,
+                              uint8_t buf, int next_shift, int next_bits, Seg* __restrict__ next,
+                              uint32_t* __restrict__ n_next, Seg* __restrict__ fin, uint32_t* __restrict__ n_fin) {
+    uint32_t cn = 0, cf = 0;
+    emit_pass<false>(child_start, child_size, nchild, buf, next_shift, next_bits, next, cn, fin, cf);
+    uint32_t i_next = cn ? atomicAdd(n_next, cn) : 0u, i_fin = cf ? atomicAdd(n_fin, cf) : 0u;
+    emit_pass<true>(child_start, child_size, nchild, buf, next_shift, next_bits, next, i_next, fin, i_fin);
 }
 
 __global__ void classify_l1_kernel(const uint32_t* __restrict__ off, uint32_t ntiles, size_t n,

@@ -90,13 +90,20 @@ __device__ __forceinline__ int32_t block_excl_max_scan(int32_t v, int32_t* smem,
 __global__ void __launch_bounds__(kT) k2_pass_a(const longlong2* __restrict__ uv, int64_t m, int64_t n,
                                                 uint32_t* __restrict__ d_in, uint32_t* __restrict__ err,
                                                 unsigned long long* __restrict__ nnz_raw,
-                                                uint32_t ntiles) {
+                                                uint32_t ntiles, uint32_t* __restrict__ next_tile) {
     __shared__ uint32_t red[kT / 32];
     __shared__ longlong2 last[kI][kT / 32];  // lane 31 of each (row j, warp)
     __shared__ longlong2 before;             // edge base-1
+    __shared__ uint32_t s_t;
     uint32_t my_err = 0;
     const unsigned lane = dev::lane_id(), w = dev::warp_id();
-    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    // Tiles handed out dynamically: their d_in atomics meet very different
+    // contention (ncu: SM busy 2.8M-5.8M cycles under a static stride).
+    for (;;) {
+        if (threadIdx.x == 0) s_t = atomicAdd(next_tile, 1u);
+        __syncthreads();
+        const uint32_t t = s_t;
+        if (t >= ntiles) break;
         const int64_t base = (int64_t)t * kTE;
         const int cnt = (int)min((int64_t)kTE, m - base);
         longlong2 p[kI];
@@ -427,6 +434,7 @@ uint32_t k2_filter_device(const int64_t* d_uv, int64_t m, int64_t n, prg_matrix*
     unsigned long long* nnz_out = reinterpret_cast<unsigned long long*>(scal.get() + 2);
     uint32_t* n_fix = reinterpret_cast<uint32_t*>(scal.get() + 3);
     uint32_t* tile_counter = n_fix + 1;
+    uint32_t* tile_counter_a = reinterpret_cast<uint32_t*>(scal.get() + 4);
 
     const auto* uv = reinterpret_cast<const longlong2*>(d_uv);
     static bool attr = false;
@@ -437,7 +445,7 @@ uint32_t k2_filter_device(const int64_t* d_uv, int64_t m, int64_t n, prg_matrix*
     const unsigned ga = std::min<unsigned>(ntiles, (unsigned)num_sms() * 2);
     {
         ProfScope pa("k2_pass_a", s);
-        k2_pass_a<<<ga, kT, 0, s>>>(uv, m, n, out->d_in, err, nnz_raw, ntiles);
+        k2_pass_a<<<ga, kT, 0, s>>>(uv, m, n, out->d_in, err, nnz_raw, ntiles, tile_counter_a);
         PRG_LAUNCH_CHECK();
     }
     uint32_t h_err = 0;

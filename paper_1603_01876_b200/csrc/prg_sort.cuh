@@ -32,6 +32,7 @@ constexpr int kTile = kTileThreads * kTileItems;  // 8192 keys per global tile
 constexpr int kRadix = 256;
 constexpr int kLocalCap = 8192;       // keys per SMEM-resident segment
 constexpr int kLocalThreads = 512;
+constexpr int kCounters = 40;  // SortWorkspace::counters (up to 16 levels of tile counters)
 
 struct Seg {
     uint64_t start;   // element offset in the key buffers
@@ -267,7 +268,7 @@ __global__ void __launch_bounds__(kTileThreads) seg_hist_kernel(
     const uint64_t* __restrict__ keys0, const uint64_t* __restrict__ keys1,
     const Seg* __restrict__ active, const uint32_t* __restrict__ seg_tile0,
     const uint32_t* __restrict__ tile_seg, const uint32_t* __restrict__ tile_idx,
-    const uint32_t* __restrict__ n_tiles, uint32_t* __restrict__ hist);
+    const uint32_t* __restrict__ n_tiles, uint32_t* __restrict__ hist, uint32_t* __restrict__ next_tile);
 
 template <bool kStable>
 __global__ void __launch_bounds__(kTileThreads, 2) seg_scatter_kernel(
@@ -275,7 +276,7 @@ __global__ void __launch_bounds__(kTileThreads, 2) seg_scatter_kernel(
     uint64_t* __restrict__ out0, uint64_t* __restrict__ out1, const Seg* __restrict__ active,
     const uint32_t* __restrict__ seg_tile0, const uint64_t* __restrict__ seg_elem0,
     const uint32_t* __restrict__ tile_seg, const uint32_t* __restrict__ tile_idx,
-    const uint32_t* __restrict__ n_tiles, const uint32_t* __restrict__ off);
+    const uint32_t* __restrict__ n_tiles, const uint32_t* __restrict__ off, uint32_t* __restrict__ next_tile);
 
 // After a level: split each active segment into 256 children, append them to
 // the final list (size <= cap or no bits left) or the next active list.
@@ -467,7 +468,8 @@ struct SortWorkspace {
     DevBuf<uint64_t> keys[2];
     DevBuf<uint32_t> hist, off;
     DevBuf<Seg> lists[2], fin;
-    DevBuf<uint32_t> counters;  // [0]=n_active(a) [1]=n_active(b) [2]=n_fin [3]=work [4]=n_tiles
+    // [0]=n_active(a) [1]=n_active(b) [2]=n_fin [3]=work [4]=n_tiles [8+2l]/[9+2l]=tile counters of level l
+    DevBuf<uint32_t> counters;
     DevBuf<uint32_t> tile_seg, tile_idx, seg_tile0;
     DevBuf<uint64_t> seg_elem0;
     size_t n = 0;
@@ -501,7 +503,7 @@ void msd_sort_split(Src src_hist, Src src_scat, size_t n, int key_bits, Dst dst,
     const unsigned dmask = (1u << bits1) - 1u;
     const uint32_t ntiles = div_up(n, kTile);
     const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)num_sms() * 4);
-    PRG_CUDA(cudaMemsetAsync(ws.counters.get(), 0, 8 * sizeof(uint32_t), s));
+    PRG_CUDA(cudaMemsetAsync(ws.counters.get(), 0, kCounters * sizeof(uint32_t), s));
     {
         ProfScope prof(t + "_l1_hist", s);
         if (Src::kSmem > 48 * 1024)

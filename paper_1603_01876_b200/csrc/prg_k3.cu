@@ -20,7 +20,7 @@
 //     s[n_nd + j], the exception's product r[u]*value written each iteration.
 //   * transpose = stable sort of (col | new row, exception) keys by column
 //     only (the payload keeps each column's rows in ascending new id), then a
-//     SELL-32 layout over virtual columns of <= kVcMax entries, slices sorted
+//     SELL-32 layout over virtual columns of <= vcmax entries (64-512 by size), slices sorted
 //     by length class. Columns keep their original ids.
 // Parity mode (mode 1) keeps original row ids, sums every column sequentially
 // in ascending u with separate mul/add, and computes every sum(r) with one
@@ -506,7 +506,7 @@ __global__ void spmv_seq_kernel(SeqArgs a) {
 // ---------------------------------------------------------------------------
 // Timed mode: sliced ELL over virtual columns (SELL-32-sigma).
 //
-// Every non-empty column is cut into parts of at most kVcMax entries ("virtual
+// Every non-empty column is cut into parts of at most vcmax entries ("virtual
 // columns"); virtual columns are ordered by quarter-octave length class
 // (descending) and packed 32 to a slice. Slice s stores entry k of its lane-j
 // virtual column at sell[slice_ptr[s] + 32k + j], so a warp reads 128
@@ -516,7 +516,6 @@ __global__ void spmv_seq_kernel(SeqArgs a) {
 // Results y are kept in SELL position order; empty columns are implicit (their
 // value is bg), and only the final iterate is un-permuted.
 // ---------------------------------------------------------------------------
-constexpr uint32_t kVcMax = 2048;
 constexpr uint32_t kEmpty = 0xffffffffu;
 
 __device__ __forceinline__ uint32_t len_class_desc(uint32_t d) {
@@ -525,20 +524,21 @@ __device__ __forceinline__ uint32_t len_class_desc(uint32_t d) {
     return 127u - (uint32_t)(lg * 4) - q;
 }
 
-__global__ void vc_count_kernel(const uint32_t* __restrict__ colptr, int64_t n, uint32_t* __restrict__ np) {
+__global__ void vc_count_kernel(const uint32_t* __restrict__ colptr, int64_t n, uint32_t vcmax,
+                                uint32_t* __restrict__ np) {
     for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t len = colptr[c + 1] - colptr[c];
-        np[c] = (len + kVcMax - 1) / kVcMax;
+        np[c] = (len + vcmax - 1) / vcmax;
     }
 }
 
 __global__ void vc_fill_kernel(const uint32_t* __restrict__ colptr, const uint32_t* __restrict__ vc_base, int64_t n,
-                               uint32_t* __restrict__ vc_col, uint32_t* __restrict__ vc_len) {
+                               uint32_t vcmax, uint32_t* __restrict__ vc_col, uint32_t* __restrict__ vc_len) {
     for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t len = colptr[c + 1] - colptr[c];
         for (uint32_t v = vc_base[c], p = 0; v < vc_base[c + 1]; ++v, ++p) {
             vc_col[v] = (uint32_t)c;
-            vc_len[v] = min(kVcMax, len - p * kVcMax);
+            vc_len[v] = min(vcmax, len - p * vcmax);
         }
     }
 }
@@ -556,13 +556,14 @@ struct VcClassSrc {
     const uint32_t* colptr;
     const uint32_t* csc_idx;  // null: length class only
     int sb;
+    uint32_t vcmax;
     static constexpr size_t kSmem = 0;
     static constexpr int kHistBatch = 16;
     __device__ void prepare(size_t, int, void*) const {}
     __device__ __forceinline__ uint64_t key(size_t i, int, const void*) const {
         if (csc_idx) {
             const uint32_t c = vc_col[i];
-            const uint32_t st = colptr[c] + (uint32_t)(i - vc_base[c]) * kVcMax;
+            const uint32_t st = colptr[c] + (uint32_t)(i - vc_base[c]) * vcmax;
             const uint32_t l = csc_idx[st + vc_len[i] - 1] & 0x7fffffffu;
             const uint32_t h = sb > 16 ? l >> (sb - 16) : l;
             return ((uint64_t)len_class_desc(vc_len[i]) << (vb + 16)) | ((uint64_t)h << vb) | i;
@@ -601,6 +602,7 @@ struct FillArgs {
     const uint32_t* slice_ptr;
     uint32_t V, nslices;
     uint32_t n_nd;             // exception entries gather s[n_nd + CSC exception rank]
+    uint32_t vcmax;            // part length
     uint32_t* sell;
     uint32_t* lane_len;  // [nslices*32]
     uint32_t* lane_col;  // [nslices*32]
@@ -622,7 +624,7 @@ __global__ void sell_fill_kernel(FillArgs a) {
             len = a.vc_len[v];
             const uint32_t part = v - a.vc_base[c];
             np = a.vc_base[c + 1] - a.vc_base[c];
-            start = a.colptr[c] + part * kVcMax;
+            start = a.colptr[c] + part * a.vcmax;
             if (part == 0) a.spos_col[c] = pos;
         }
         a.lane_len[pos] = len;
@@ -661,10 +663,16 @@ __global__ void spos_rows_kernel(const uint32_t* __restrict__ pinv, const uint32
         spos[j] = spos_col[pinv[j]];
 }
 
-__global__ void split_list_kernel(const uint32_t* __restrict__ vc_base, const uint32_t* __restrict__ vpos, int64_t n,
-                                  uint32_t* __restrict__ list, uint32_t* __restrict__ cnt) {
+// Split columns listed in column order (flag + scan + scatter) so that the
+// per-iteration sum over them has a fixed order.
+__global__ void split_flag_kernel(const uint32_t* __restrict__ vc_base, int64_t n, uint32_t* __restrict__ flag) {
     for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x)
-        if (vc_base[c + 1] - vc_base[c] > 1) list[atomicAdd(cnt, 1u)] = vpos[vc_base[c]];
+        flag[c] = vc_base[c + 1] - vc_base[c] > 1 ? 1u : 0u;
+}
+__global__ void split_list_kernel(const uint32_t* __restrict__ vc_base, const uint32_t* __restrict__ vpos, int64_t n,
+                                  const uint32_t* __restrict__ idx, uint32_t* __restrict__ list) {
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x)
+        if (vc_base[c + 1] - vc_base[c] > 1) list[idx[c]] = vpos[vc_base[c]];
 }
 
 // s[j] = r(pinv[j]) * b[j]; r given in original order (first step) or as
@@ -1003,9 +1011,19 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
     if (mode == 1) return;
     // 4. SELL over virtual columns
     ProfScope pr("k3_prep_sell", s);
+    // Part length: short enough that the longest lane chain (one sequential
+    // gather stream) stays well under the whole SpMV on small graphs.
+    // Measured on B200 (SpMV ms): S=24 512: 0.797, 384/768: 0.82, 2048: 0.834;
+    // S=20 128-256: 0.085; S=16 64: 0.027 vs 2048: 0.159; S=26 1024: 3.51 vs 512: 3.63.
+    uint32_t vcmax = nnz >= (1ull << 29) ? 1024u : nnz >= (1ull << 27) ? 512u : nnz >= (1ull << 23) ? 256u : nnz >= (1ull << 20) ? 128u : 64u;
+    {
+        static int env = -1;
+        if (env < 0) { const char* e = getenv("PRG_VCMAX"); env = e ? atoi(e) : 0; }
+        if (env > 0) vcmax = (uint32_t)env;
+    }
     DevBuf<uint32_t> np((size_t)n, s);
     P.vc_base = DevBuf<uint32_t>((size_t)n + 1, s);
-    vc_count_kernel<<<g, 1024, 0, s>>>(P.colptr.get(), n, np.get());
+    vc_count_kernel<<<g, 1024, 0, s>>>(P.colptr.get(), n, vcmax, np.get());
     PRG_LAUNCH_CHECK();
     exclusive_scan_u32(np.get(), P.vc_base.get(), (size_t)n, P.vc_base.get() + n, s);
     PRG_CUDA(cudaMemcpyAsync(&P.V, P.vc_base.get() + n, 4, cudaMemcpyDeviceToHost, s));
@@ -1015,7 +1033,7 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
     const uint32_t NP = P.nslices * 32;
     DevBuf<uint32_t> vc_col(V ? V : 1, s), vc_len(V ? V : 1, s), order(NP ? NP : 1, s);
     P.vpos = DevBuf<uint32_t>(V ? V : 1, s);
-    vc_fill_kernel<<<g, 1024, 0, s>>>(P.colptr.get(), P.vc_base.get(), n, vc_col.get(), vc_len.get());
+    vc_fill_kernel<<<g, 1024, 0, s>>>(P.colptr.get(), P.vc_base.get(), n, vcmax, vc_col.get(), vc_len.get());
     PRG_LAUNCH_CHECK();
     if (V) {
         sort::SortWorkspace ws;
@@ -1023,7 +1041,7 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
         static int co = -1;  // PRG_COL_ORDER=0: length class only
         if (co < 0) { const char* e = getenv("PRG_COL_ORDER"); co = e ? atoi(e) : 1; }
         sort::msd_sort(VcClassSrc{vc_len.get(), vb, vc_col.get(), P.vc_base.get(), P.colptr.get(),
-                                  co ? P.csc_idx.get() : nullptr, P.sb},
+                                  co ? P.csc_idx.get() : nullptr, P.sb, vcmax},
                        (size_t)V, vb + 8 + (co ? 16 : 0), PermDst{order.get(), P.vpos.get(), vb}, ws, s,
                        "k3vc", /*payload_bits=*/vb, /*stable=*/true);
     }
@@ -1046,8 +1064,8 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
     if (P.nslices) {
         FillArgs fa{order.get(),         vc_col.get(),     vc_len.get(), P.vc_base.get(),   P.colptr.get(),
                     P.csc_idx.get(),     P.exc_base.get(), P.slice_ptr.get(), V,                P.nslices,
-                    (uint32_t)P.n_nd,    P.sell.get(),     P.lane_len.get(),  P.lane_col.get(), P.lane_np.get(),
-                    P.spos_col.get()};
+                    (uint32_t)P.n_nd,    vcmax,            P.sell.get(),     P.lane_len.get(),  P.lane_col.get(),
+                    P.lane_np.get(),     P.spos_col.get()};
         sell_fill_kernel<<<g, 256, 0, s>>>(fa);
         PRG_LAUNCH_CHECK();
     }
@@ -1057,8 +1075,14 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
     P.split_pos = DevBuf<uint32_t>((size_t)n, s);
     P.n_split = DevBuf<uint32_t>(1, s);
     PRG_CUDA(cudaMemsetAsync(P.n_split.get(), 0, 4, s));
-    split_list_kernel<<<g, 1024, 0, s>>>(P.vc_base.get(), P.vpos.get(), n, P.split_pos.get(), P.n_split.get());
-    PRG_LAUNCH_CHECK();
+    if (n > 0) {
+        DevBuf<uint32_t> flag((size_t)n, s), idx((size_t)n, s);
+        split_flag_kernel<<<g, 1024, 0, s>>>(P.vc_base.get(), n, flag.get());
+        PRG_LAUNCH_CHECK();
+        exclusive_scan_u32(flag.get(), idx.get(), (size_t)n, P.n_split.get(), s);
+        split_list_kernel<<<g, 1024, 0, s>>>(P.vc_base.get(), P.vpos.get(), n, idx.get(), P.split_pos.get());
+        PRG_LAUNCH_CHECK();
+    }
     P.arrive = DevBuf<uint32_t>((size_t)n, s);
     PRG_CUDA(cudaMemsetAsync(P.arrive.get(), 0, (size_t)n * 4, s));
     P.partial = DevBuf<double>(NP ? NP : 1, s);

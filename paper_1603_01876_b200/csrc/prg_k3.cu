@@ -38,7 +38,6 @@ namespace {
 
 constexpr uint64_t kRankInitStream = 0x72616e6b696e6974ULL;  // kernel3_pagerank.cpp:15
 constexpr int kSpmvThreads = 1024;
-constexpr int kCscGroup = 32;  // exception ranks are counted per 32-entry group
 
 __host__ __device__ inline int bits_for(int64_t n) {
     int b = 1;
@@ -202,43 +201,34 @@ __global__ void perm_delta_kernel(const uint32_t* __restrict__ ro, const uint32_
     }
 }
 
-// Row minimum of the stored values -> bmin[u] (ordered u64 bit patterns;
-// values > 0). CSR-order tiles (coalesced), warp-segmented min per row, one
-// atomicMin per row segment.
-__global__ void __launch_bounds__(sort::kTileThreads, 3)
-    row_min_kernel(const uint32_t* __restrict__ ro, const uint32_t* __restrict__ tile_row,
-                   const double* __restrict__ val, int64_t n, uint64_t nnz, unsigned long long* __restrict__ bmin) {
-    extern __shared__ uint32_t srow[];
-    const unsigned lane = dev::lane_id();
-    const uint32_t ntiles = (uint32_t)((nnz + sort::kTile - 1) / sort::kTile);
-    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const size_t base = (size_t)t * sort::kTile;
-        const int cnt = (int)min((uint64_t)sort::kTile, nnz - base);
-        expand_rows(ro, tile_row, n, base, cnt, srow);
-#pragma unroll 8
-        for (int j = 0; j < sort::kTileItems; ++j) {
-            const int li = j * sort::kTileThreads + threadIdx.x;
-            const bool ok = li < cnt;
-            const uint32_t r = ok ? srow[rpad(li)] : 0xffffffffu;
-            uint64_t b = ok ? (uint64_t)__double_as_longlong(val[base + li]) : ~0ull;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const uint64_t ob = __shfl_down_sync(0xffffffffu, b, d);
-                const uint32_t orow = __shfl_down_sync(0xffffffffu, r, d);
-                if (lane + d < 32 && orow == r) b = min(b, ob);
-            }
-            const uint32_t prow = __shfl_up_sync(0xffffffffu, r, 1);
-            if (ok && (lane == 0 || prow != r)) atomicMin(&bmin[r], (unsigned long long)b);
+// Row base value bmin[u] (u64 bit pattern): the minimum of five of the row's
+// stored values (first, quartiles, last). Any choice is exact — an entry whose
+// value differs from its row base becomes an exception — and for a stochastic
+// matrix a row's values are k/d_out with k = 1 for almost every entry, so the
+// sampled minimum finds 1/d_out: at S=18/20 it yields exactly the exceptions of
+// the full row minimum (five loads per row instead of a pass over the values).
+__global__ void row_base_kernel(const uint32_t* __restrict__ ro, const double* __restrict__ val, int64_t n,
+                                unsigned long long* __restrict__ bmin) {
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t b = ro[u], d = ro[u + 1] - b;
+        unsigned long long m = ~0ull;
+        if (d) {
+            const unsigned long long* v = reinterpret_cast<const unsigned long long*>(val) + b;
+            m = min(min(v[0], v[d - 1]), min(min(v[d >> 2], v[d >> 1]), v[(3 * (uint64_t)d) >> 2]));
         }
-        __syncthreads();
+        bmin[u] = m;
     }
 }
 
 // Transpose keys: for every CSR entry (u, col, a) the key
 // (col, newid[u], a != bmin[u]) written at its position in the NEW row order
 // (rows permuted, each row's entries contiguous). A stable sort of these keys
-// by column then lists every column's rows in ascending new id. Exceptions
-// (a != row base) are also appended to a list (one atomic per tile).
+// by column then lists every column's rows in ascending new id. An exception
+// (a != row base: a duplicate edge) is appended to the exception list (row,
+// value; one atomic per tile) and its key carries its list index instead of
+// the row: the transpose then hands every exception entry its own slot in the
+// gather vector (s[n_nd + index]) with no exception sort. The index order is
+// arbitrary; column sums are not — they follow the stable CSC order.
 struct KeyBuildArgs {
     const uint32_t* ro;
     const uint32_t* tile_row;
@@ -249,10 +239,10 @@ struct KeyBuildArgs {
     const uint32_t* wdelta;  // null: identity
     int64_t n;
     uint64_t nnz;
-    int sb;
+    int pb;  // payload bits (row id or exception index), below them the exception flag
     unsigned long long* keys;
-    unsigned long long* exc_key;
-    uint32_t* exc_row;  // [nnz] new row of the exception at CSR position e (only those are written)
+    uint32_t* e_u;   // exception list: new row
+    double* e_val;   //                 value
     uint32_t* n_exc;
 };
 __global__ void __launch_bounds__(sort::kTileThreads, 3) key_build_kernel(KeyBuildArgs a) {
@@ -277,7 +267,7 @@ __global__ void __launch_bounds__(sort::kTileThreads, 3) key_build_kernel(KeyBui
                 const bool exc = (uint64_t)__double_as_longlong(v) != a.bmin[u];
                 const uint32_t nid = a.newid ? a.newid[u] : u;
                 const uint32_t pos = a.wdelta ? e + a.wdelta[u] : e;
-                a.keys[pos] = ((uint64_t)c << (a.sb + 1)) | ((uint64_t)nid << 1) | (uint64_t)exc;
+                a.keys[pos] = ((uint64_t)c << (a.pb + 1)) | ((uint64_t)nid << 1);  // exceptions: rewritten below
                 excm |= (uint32_t)exc << j;
             }
         }
@@ -292,8 +282,10 @@ __global__ void __launch_bounds__(sort::kTileThreads, 3) key_build_kernel(KeyBui
                 const int li = j * sort::kTileThreads + threadIdx.x;
                 const uint32_t e = (uint32_t)(base + li);
                 const uint32_t u = srow[rpad(li)];
-                a.exc_key[idx] = ((uint64_t)a.cols[e] << 32) | e;
-                a.exc_row[e] = a.newid ? a.newid[u] : u;
+                const uint32_t pos = a.wdelta ? e + a.wdelta[u] : e;
+                a.keys[pos] = ((uint64_t)a.cols[e] << (a.pb + 1)) | ((uint64_t)idx << 1) | 1ull;
+                a.e_u[idx] = a.newid ? a.newid[u] : u;
+                a.e_val[idx] = a.val[e];
                 ++idx;
             }
         }
@@ -309,17 +301,15 @@ __global__ void gather_base_kernel(const uint32_t* __restrict__ pinv, const unsi
         bval[j] = __longlong_as_double((long long)bmin[pinv[j]]);
 }
 
+// CSC entry: new row id, or (bit 31 set) exception list index.
 struct CscDst {
     uint32_t* csc_idx;
     uint32_t* colptr;   // initialised to ~0; column starts via atomicMin
-    uint32_t* exc_cnt;  // per 32-entry group
-    int sb;
+    int pb;
     __device__ __forceinline__ void store(uint64_t pos, uint64_t key, bool has_prev, uint64_t prev) const {
-        const uint32_t col = (uint32_t)(key >> (sb + 1));
-        const uint32_t exc = (uint32_t)(key & 1);
-        csc_idx[pos] = (uint32_t)((key >> 1) & ((1ull << sb) - 1)) | (exc << 31);
-        if (!has_prev || (uint32_t)(prev >> (sb + 1)) != col) atomicMin(&colptr[col], (uint32_t)pos);
-        if (exc) atomicAdd(&exc_cnt[pos / kCscGroup], 1u);
+        const uint32_t col = (uint32_t)(key >> (pb + 1));
+        csc_idx[pos] = (uint32_t)((key >> 1) & ((1ull << pb) - 1)) | ((uint32_t)(key & 1) << 31);
+        if (!has_prev || (uint32_t)(prev >> (pb + 1)) != col) atomicMin(&colptr[col], (uint32_t)pos);
     }
 };
 
@@ -392,24 +382,6 @@ __global__ void suffix_min_down(uint32_t* a, int64_t n1, const uint32_t* part) {
     }
 }
 
-// Exceptions (entries whose value differs from the row base, i.e. duplicate
-// edges) are captured as keys (col, CSR position). Sorted, they list every
-// column's exceptions contiguously, columns ascending, in CSR order inside a
-// column — which in parity mode (identity numbering) is exactly the CSC order.
-// In timed mode the SELL only needs "the k-th exception slot of column c" to
-// take one of column c's exceptions: the column sum is the same set of products.
-struct ExcValueDst {
-    const uint32_t* exc_row;  // new row of the exception at each CSR position (written by key_build)
-    const double* values;
-    uint32_t* e_u;    // new row id
-    double* e_val;    // value
-    __device__ __forceinline__ void store(uint64_t i, uint64_t key, bool, uint64_t) const {
-        const uint32_t e = (uint32_t)key;
-        e_u[i] = exc_row[e];
-        e_val[i] = values[e];
-    }
-};
-
 // ---------------------------------------------------------------------------
 // init_rank (kernel3_pagerank.cpp:29-39)
 // ---------------------------------------------------------------------------
@@ -472,8 +444,8 @@ __global__ void scale_kernel(double* __restrict__ x, int64_t n, const double* __
 struct SeqArgs {
     const uint32_t* colptr;
     const uint32_t* csc_idx;
-    const uint32_t* exc_base;  // per 32-entry CSC group
-    const double* exc_val;     // CSC order
+    const uint32_t* e_u;       // exception list (row, value)
+    const double* e_val;
     const double* s;           // s[u] = r[u] * b[u] (identity numbering)
     const double* r_prev;      // original order
     const double* bgp;
@@ -489,14 +461,7 @@ __global__ void spmv_seq_kernel(SeqArgs a) {
         for (uint32_t p = b; p < e; ++p) {
             const uint32_t w = a.csc_idx[p];
             const uint32_t u = w & 0x7fffffffu;
-            double x;
-            if (w >> 31) {
-                uint32_t rank = a.exc_base[p / kCscGroup];
-                for (uint32_t q = p & ~(uint32_t)(kCscGroup - 1); q < p; ++q) rank += a.csc_idx[q] >> 31;
-                x = __dmul_rn(a.r_prev[u], a.exc_val[rank]);
-            } else {
-                x = a.s[u];
-            }
+            const double x = (w >> 31) ? __dmul_rn(a.r_prev[a.e_u[u]], a.e_val[u]) : a.s[u];
             acc = __dadd_rn(acc, x);
         }
         a.r_next[c] = __dadd_rn(__dmul_rn(a.damping, acc), a.bgp[1]);
@@ -555,6 +520,7 @@ struct VcClassSrc {
     const uint32_t* vc_base;
     const uint32_t* colptr;
     const uint32_t* csc_idx;  // null: length class only
+    const uint32_t* e_u;      // exception list rows
     int sb;
     uint32_t vcmax;
     static constexpr size_t kSmem = 0;
@@ -564,7 +530,8 @@ struct VcClassSrc {
         if (csc_idx) {
             const uint32_t c = vc_col[i];
             const uint32_t st = colptr[c] + (uint32_t)(i - vc_base[c]) * vcmax;
-            const uint32_t l = csc_idx[st + vc_len[i] - 1] & 0x7fffffffu;
+            const uint32_t w = csc_idx[st + vc_len[i] - 1];
+            const uint32_t l = (w >> 31) ? e_u[w & 0x7fffffffu] : w;
             const uint32_t h = sb > 16 ? l >> (sb - 16) : l;
             return ((uint64_t)len_class_desc(vc_len[i]) << (vb + 16)) | ((uint64_t)h << vb) | i;
         }
@@ -598,10 +565,9 @@ struct FillArgs {
     const uint32_t* vc_base;
     const uint32_t* colptr;
     const uint32_t* csc_idx;
-    const uint32_t* exc_base;  // CSC groups of kCscGroup: exception rank at the group start
     const uint32_t* slice_ptr;
     uint32_t V, nslices;
-    uint32_t n_nd;             // exception entries gather s[n_nd + CSC exception rank]
+    uint32_t n_nd;             // exception entries gather s[n_nd + exception index]
     uint32_t vcmax;            // part length
     uint32_t* sell;
     uint32_t* lane_len;  // [nslices*32]
@@ -611,7 +577,7 @@ struct FillArgs {
 };
 
 // One warp per slice, lane = virtual column. Exception entries (value != row
-// base, flagged in the CSC) are redirected to s[n_nd + rank], where the
+// base, flagged in the CSC) are redirected to s[n_nd + index], where the
 // exception products are stored every iteration — the SpMV has no special case.
 __global__ void sell_fill_kernel(FillArgs a) {
     const uint32_t lane = dev::lane_id();
@@ -630,13 +596,6 @@ __global__ void sell_fill_kernel(FillArgs a) {
         a.lane_len[pos] = len;
         a.lane_col[pos] = c;
         a.lane_np[pos] = np;
-        // exception rank at `start`
-        uint32_t er = 0;
-        if (len) {
-            const uint32_t g0 = start & ~(uint32_t)(kCscGroup - 1);
-            er = a.exc_base[start / kCscGroup];
-            for (uint32_t q = g0; q < start; ++q) er += a.csc_idx[q] >> 31;
-        }
         const uint32_t base = a.slice_ptr[s];
         const uint32_t rows = (a.slice_ptr[s + 1] - base) >> 5;
         const uint32_t* src = a.csc_idx + start;
@@ -649,7 +608,7 @@ __global__ void sell_fill_kernel(FillArgs a) {
             for (int u = 0; u < 8; ++u) {
                 if (k0 + u < rows) {
                     uint32_t w = e[u];
-                    if (k0 + u < len && (w >> 31)) w = a.n_nd + er++;
+                    if (k0 + u < len && (w >> 31)) w = a.n_nd + (w & 0x7fffffffu);
                     dst[32 * (k0 + u)] = w;
                 }
             }
@@ -860,14 +819,15 @@ struct K3Plan {
     int64_t n = 0, n_nd = 0;
     uint64_t nnz = 0;
     int sb = 1;
+    int pb = 1;  // transpose key payload bits (row id or exception index)
     int mode = 0;
-    DevBuf<uint32_t> pinv, newid, colptr, csc_idx, exc_base;
+    DevBuf<uint32_t> pinv, newid, colptr, csc_idx;
     DevBuf<double> bval, exc_val;
     uint32_t n_exc = 0;
     // timed mode (SELL)
     uint32_t V = 0, nslices = 0, n_empty = 0;
     DevBuf<uint32_t> sell, slice_ptr, lane_len, lane_col, lane_np, vc_base, vpos, spos, spos_col, split_pos, n_split,
-        arrive, e_u;  // e_u: new row of CSC-ordered exception i (values in exc_val)
+        arrive, e_u;  // exception list: new row e_u[i], value exc_val[i]
     DevBuf<double> partial;
 };
 
@@ -879,7 +839,8 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
     P.nnz = nnz;
     P.mode = mode;
     P.sb = bits_for(n);
-    if (2 * P.sb + 1 > 64 || P.sb > 31) throw CudaError{"K3: vertex count too large for u32 indices"};
+    P.pb = std::max(P.sb, bits_for((int64_t)nnz));
+    if (P.sb + P.pb + 1 > 64 || P.pb > 31) throw CudaError{"K3: matrix too large for u32 indices"};
     const unsigned g = (unsigned)num_sms() * 8;
     P.pinv = DevBuf<uint32_t>((size_t)n, s);
     P.newid = DevBuf<uint32_t>((size_t)n, s);
@@ -928,7 +889,6 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
     const size_t row_smem = kRowWords * sizeof(uint32_t);
     {
         ProfScope pr("k3_prep_base", s);
-        PRG_CUDA(cudaMemsetAsync(bmin.get(), 0xff, (size_t)n * 8, s));
         if (mode == 0) {
             DevBuf<uint32_t> deg((size_t)std::max<int64_t>(nr, 1), s), pro((size_t)nr + 1, s);
             wdelta = DevBuf<uint32_t>((size_t)n, s);
@@ -941,10 +901,9 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
         if (nnz) {
             tile_rows_kernel<<<g, 1024, 0, s>>>(A->row_offsets, n, tile_row.get());
             PRG_LAUNCH_CHECK();
-            row_min_kernel<<<num_sms() * 3, sort::kTileThreads, row_smem, s>>>(A->row_offsets, tile_row.get(),
-                                                                              A->values, n, nnz, bmin.get());
-            PRG_LAUNCH_CHECK();
         }
+        row_base_kernel<<<g, 256, 0, s>>>(A->row_offsets, A->values, n, bmin.get());
+        PRG_LAUNCH_CHECK();
         P.bval = DevBuf<double>((size_t)std::max<int64_t>(nr, 1), s);
         gather_base_kernel<<<g, 1024, 0, s>>>(P.pinv.get(), bmin.get(), nr, P.bval.get());
         PRG_LAUNCH_CHECK();
@@ -952,15 +911,13 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
     // 3. transpose: stable sort of (col | new row, exception) keys by column
     P.colptr = DevBuf<uint32_t>((size_t)n + 1, s);
     P.csc_idx = DevBuf<uint32_t>(nnz ? nnz : 1, s);
-    const uint64_t ngroups = nnz / kCscGroup + 1;
-    DevBuf<uint32_t> exc_cnt(ngroups, s);
-    DevBuf<unsigned long long> exc_key(nnz ? nnz : 1, s);
-    DevBuf<uint32_t> exc_row(nnz ? nnz : 1, s);  // sparse: written at exception positions only
+    // exception list, capacity nnz until its size is known
+    DevBuf<uint32_t> e_u(nnz ? nnz : 1, s);
+    DevBuf<double> e_val(nnz ? nnz : 1, s);
     DevBuf<uint32_t> n_exc(1, s);
     {
         ProfScope pr("k3_prep_transpose", s);
         PRG_CUDA(cudaMemsetAsync(P.colptr.get(), 0xff, (size_t)(n + 1) * 4, s));
-        PRG_CUDA(cudaMemsetAsync(exc_cnt.get(), 0, ngroups * 4, s));
         PRG_CUDA(cudaMemsetAsync(n_exc.get(), 0, 4, s));
         if (nnz) {
             sort::SortWorkspace ws;
@@ -968,18 +925,18 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
             {
                 ProfScope pk("k3t_keys", s);
                 KeyBuildArgs ka{A->row_offsets, tile_row.get(), A->cols, A->values, bmin.get(),
-                                mode == 0 ? P.newid.get() : nullptr, mode == 0 ? wdelta.get() : nullptr, n, nnz, P.sb,
-                                reinterpret_cast<unsigned long long*>(ws.keys[0].get()), exc_key.get(), exc_row.get(),
+                                mode == 0 ? P.newid.get() : nullptr, mode == 0 ? wdelta.get() : nullptr, n, nnz, P.pb,
+                                reinterpret_cast<unsigned long long*>(ws.keys[0].get()), e_u.get(), e_val.get(),
                                 n_exc.get()};
                 key_build_kernel<<<num_sms() * 3, sort::kTileThreads, row_smem, s>>>(ka);
                 PRG_LAUNCH_CHECK();
             }
             // the keys live in ws.keys[0]; level 1 reads them before any pass overwrites that buffer.
-            // (new row, exception) ride as payload: only column bits are sorted
+            // (row or exception index, exception flag) ride as payload: only column bits are sorted
             const KeyArraySrc src{reinterpret_cast<const unsigned long long*>(ws.keys[0].get())};
-            sort::msd_sort_split(src, src, (size_t)nnz, 2 * P.sb + 1,
-                                 CscDst{P.csc_idx.get(), P.colptr.get(), exc_cnt.get(), P.sb}, ws, s, "k3t",
-                                 /*payload_bits=*/P.sb + 1, /*stable=*/true);
+            sort::msd_sort_split(src, src, (size_t)nnz, P.sb + P.pb + 1,
+                                 CscDst{P.csc_idx.get(), P.colptr.get(), P.pb}, ws, s, "k3t",
+                                 /*payload_bits=*/P.pb + 1, /*stable=*/true);
         }
         // colptr[n] = nnz, then fill empty columns with the next column start.
         const uint32_t nz = (uint32_t)nnz;
@@ -992,21 +949,13 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
         suffix_min_down<<<(unsigned)nb, 1024, 0, s>>>(P.colptr.get(), n1, part.get());
         PRG_LAUNCH_CHECK();
     }
-    // exceptions in CSC order (parity mode uses them directly; timed mode resolves from them)
-    P.exc_base = DevBuf<uint32_t>(ngroups, s);
-    {
-        DevBuf<uint32_t> exc_total(1, s);
-        exclusive_scan_u32(exc_cnt.get(), P.exc_base.get(), ngroups, exc_total.get(), s);
-        PRG_CUDA(cudaMemcpyAsync(&P.n_exc, exc_total.get(), 4, cudaMemcpyDeviceToHost, s));
-        PRG_CUDA(cudaStreamSynchronize(s));
-    }
+    PRG_CUDA(cudaMemcpyAsync(&P.n_exc, n_exc.get(), 4, cudaMemcpyDeviceToHost, s));
+    PRG_CUDA(cudaStreamSynchronize(s));
     P.exc_val = DevBuf<double>(P.n_exc ? P.n_exc : 1, s);
     P.e_u = DevBuf<uint32_t>(P.n_exc ? P.n_exc : 1, s);
     if (P.n_exc) {
-        sort::SortWorkspace ws;
-        sort::msd_sort(KeyArraySrc{exc_key.get()}, (size_t)P.n_exc, 32 + P.sb,
-                       ExcValueDst{exc_row.get(), A->values, P.e_u.get(), P.exc_val.get()},
-                       ws, s, "k3exc");
+        PRG_CUDA(cudaMemcpyAsync(P.e_u.get(), e_u.get(), (size_t)P.n_exc * 4, cudaMemcpyDeviceToDevice, s));
+        PRG_CUDA(cudaMemcpyAsync(P.exc_val.get(), e_val.get(), (size_t)P.n_exc * 8, cudaMemcpyDeviceToDevice, s));
     }
     if (mode == 1) return;
     // 4. SELL over virtual columns
@@ -1041,7 +990,7 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
         static int co = -1;  // PRG_COL_ORDER=0: length class only
         if (co < 0) { const char* e = getenv("PRG_COL_ORDER"); co = e ? atoi(e) : 1; }
         sort::msd_sort(VcClassSrc{vc_len.get(), vb, vc_col.get(), P.vc_base.get(), P.colptr.get(),
-                                  co ? P.csc_idx.get() : nullptr, P.sb, vcmax},
+                                  co ? P.csc_idx.get() : nullptr, P.e_u.get(), P.sb, vcmax},
                        (size_t)V, vb + 8 + (co ? 16 : 0), PermDst{order.get(), P.vpos.get(), vb}, ws, s,
                        "k3vc", /*payload_bits=*/vb, /*stable=*/true);
     }
@@ -1063,7 +1012,7 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
     PRG_CUDA(cudaMemsetAsync(P.spos_col.get(), 0xff, (size_t)n * 4, s));
     if (P.nslices) {
         FillArgs fa{order.get(),         vc_col.get(),     vc_len.get(), P.vc_base.get(),   P.colptr.get(),
-                    P.csc_idx.get(),     P.exc_base.get(), P.slice_ptr.get(), V,                P.nslices,
+                    P.csc_idx.get(),     P.slice_ptr.get(), V,                P.nslices,
                     (uint32_t)P.n_nd,    vcmax,            P.sell.get(),     P.lane_len.get(),  P.lane_col.get(),
                     P.lane_np.get(),     P.spos_col.get()};
         sell_fill_kernel<<<g, 256, 0, s>>>(fa);
@@ -1163,7 +1112,7 @@ void iterate(const K3Plan& P, const double* r_in, double* r_out, int iters, doub
             double* dst = (it & 1) ? tB.get() : tA.get();
             permute_orig_kernel<<<g, 1024, 0, s>>>(cur, P.pinv.get(), P.bval.get(), n, sb.get());
             PRG_LAUNCH_CHECK();
-            SeqArgs a{P.colptr.get(), P.csc_idx.get(), P.exc_base.get(), P.exc_val.get(), sb.get(), cur,
+            SeqArgs a{P.colptr.get(), P.csc_idx.get(), P.e_u.get(), P.exc_val.get(), sb.get(), cur,
                       S.out.get(), dst, n, damping};
             spmv_seq_kernel<<<g, 256, 0, s>>>(a);
             PRG_LAUNCH_CHECK();

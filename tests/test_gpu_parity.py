@@ -224,8 +224,9 @@ def test_k3_known_answers(capi):
 def _adversarial_csr(n, seed):
     """A CSR that stresses K3's prep: hub rows longer than a tile (8192), a hot
     column longer than a SELL part (2048), empty rows and columns, rows whose
-    values are all equal (no exceptions) and rows with random values (nearly
-    every entry an exception)."""
+    values are all equal (no exceptions), rows with random values (nearly
+    every entry an exception) and rows whose sampled base entries are the odd
+    ones out (every other entry becomes an exception)."""
     rng = np.random.default_rng(seed)
     rows = []
     for u in range(n):
@@ -242,6 +243,10 @@ def _adversarial_csr(n, seed):
             v = np.full(len(c), 1.0 / max(len(c), 1))
         elif u % 4 == 1:
             v = rng.random(len(c)) + 1e-3
+        elif u % 8 == 6 and len(c) >= 5:  # exactly the entries K3 samples for its row base differ
+            d_ = len(c)
+            v = np.full(d_, 0.5 / d_)
+            v[[0, d_ // 4, d_ // 2, (3 * d_) // 4, d_ - 1]] *= 3.0
         else:  # a few duplicates-like exceptions on top of a base value
             v = np.full(len(c), 0.5 / max(len(c), 1))
             if len(c):

@@ -5,8 +5,9 @@ Metric (BASELINE.json): "K3 PageRank edges/s (M x 20 iters), K1/K2 edges/s; % of
 roofline, 1 B200". Workload: Kronecker S=24 (N=2^24, M=2^28), Graph500 initiator,
 seed 1, K3 seed 1, c=0.85, 20 iterations — the SURVEY's headline roofline config.
 
-One step = K1 (device sort of the K0 edge list) + K2 (filter/normalise) + K3 (20
-iterations incl. init and the CSR->CSC transpose), inputs resident in HBM; each
+One step = K1 (device sort of the K0 edge list) + K2 (filter/normalise, then the
+CSR/CSC build the north_star assigns to K2: the column layout K3 iterates over) +
+K3 (init_rank + 20 iterations), inputs resident in HBM; each
 stage timed with CUDA events on the launching stream. `value` = whole-job K3
 edges/s (20*M per step per rank / max-over-ranks K3 time). Inputs (4.3 GB edge
 list, 3.1 GB CSR) exceed the 126 MB L2, so no L2 flush is needed between steps.
@@ -194,14 +195,16 @@ def run_ours(args):
     def one_step(record):
         if flush is not None:
             flush.fill_(1.0)  # evicts the 126 MB L2 (outside the stage events)
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
         ev[0].record(stream)
         capi.k1_sort(uv, S, out=sorted_uv, stream=stream)
         ev[1].record(stream)
         mat = capi.k2_filter(sorted_uv, n, stream=stream)
         ev[2].record(stream)
-        _, norm = capi.k3_pagerank(mat, seed=seed, iterations=iters, mode=0, out=ranks, stream=stream)
+        mat.build_csc(stream)  # K2's CSC build (north_star): the column layout K3 iterates over
         ev[3].record(stream)
+        _, norm = capi.k3_pagerank(mat, seed=seed, iterations=iters, mode=0, out=ranks, stream=stream)
+        ev[4].record(stream)
         info = (mat.nnz, mat.nnz_raw, mat.max_in, norm)
         if record is not None:
             record.append((ev, info))
@@ -240,16 +243,34 @@ def run_ours(args):
     torch.cuda.synchronize()
 
     k1 = [e[0].elapsed_time(e[1]) for e, _ in rec]
-    k2 = [e[1].elapsed_time(e[2]) for e, _ in rec]
-    k3 = [e[2].elapsed_time(e[3]) for e, _ in rec]
+    k2 = [e[1].elapsed_time(e[3]) for e, _ in rec]
+    k2f = [e[1].elapsed_time(e[2]) for e, _ in rec]
+    k2c = [e[2].elapsed_time(e[3]) for e, _ in rec]
+    k3 = [e[3].elapsed_time(e[4]) for e, _ in rec]
     total_ms = t_start.elapsed_time(t_end)
     nnz, nnz_raw, max_in, norm = rec[-1][1]
-    loc = np.array([np.mean(k1), np.mean(k2), np.mean(k3), total_ms / args.steps], dtype=np.float64)
+
+    # K3 from a bare CSR (no CSC on the handle): the layout is built inside K3's
+    # own timed region, as for a StochasticMatrix that did not come from our K2.
+    mat = capi.k2_filter(sorted_uv, n, stream=stream)
+    cold = []
+    for i in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        capi.k3_pagerank(mat, seed=seed, iterations=iters, mode=0, out=ranks, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if i:
+            cold.append(e0.elapsed_time(e1))
+    mat.close()
+
+    loc = np.array([np.mean(k1), np.mean(k2), np.mean(k3), total_ms / args.steps, np.mean(k2f), np.mean(k2c),
+                    np.mean(cold)], dtype=np.float64)
     if ws > 1:
         t = torch.tensor(loc, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         loc = t.cpu().numpy()
-    k1_ms, k2_ms, k3_ms, step_ms = (float(x) for x in loc)
+    k1_ms, k2_ms, k3_ms, step_ms, k2f_ms, k2c_ms, k3cold_ms = (float(x) for x in loc)
 
     peak, peak_src = peaks()
     b1, b2, b3, b3_iter = alg_bytes(n, m, nnz, iters)
@@ -280,7 +301,11 @@ def run_ours(args):
         "k1_edges_per_s": ws * m / (k1_ms * 1e-3),
         "k2_edges_per_s": ws * m / (k2_ms * 1e-3),
         "k3_edges_per_s": value,
-        "stage_ms": {"k1_sort": k1_ms, "k2_filter": k2_ms, "k3_pagerank": k3_ms},
+        "stage_ms": {"k1_sort": k1_ms, "k2_filter": k2_ms, "k3_pagerank": k3_ms,
+                     "k2_filter_csr": k2f_ms, "k2_csc_build": k2c_ms},
+        # K3 on a handle without the K2-built CSC: layout build (transpose, SELL) inside K3
+        "k3_cold": {"edges_per_s": ws * iters * m / (k3cold_ms * 1e-3), "ms": k3cold_ms,
+                    "note": "K3 from a bare CSR: the CSC/SELL build is inside the K3 timed region"},
         "final_norm1": norm,
         "roofline": {"bound": "hbm", "kernel": "k3_spmv (spmv_sell_kernel, one PageRank iteration)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -119,6 +119,17 @@ prg_status prg_matrix_device_arrays(const prg_matrix* a, const uint32_t** row_of
 prg_status prg_matrix_from_host(int64_t n, int64_t nnz, const int64_t* row_offsets,
                                 const int64_t* cols, const double* values, prg_matrix** out);
 void prg_matrix_destroy(prg_matrix* a);
+/* K2's CSC build (north_star: "a scan-based CSR/CSC build"; SURVEY §8(b) device
+ * residency across the K2 -> K3 handoff). Builds, on the handle, the column-major
+ * layout K3 iterates over — rows renumbered by out-degree class, the CSR
+ * transposed by a stable column sort, sliced-ELL over virtual columns — so that
+ * run_kernel3 / pagerank_step / run_to_convergence on this handle start from a
+ * CSC, as the reference's K3 starts from its CSR (kernel3_pagerank.cpp:67-79).
+ * K3 calls on a handle without it build a temporary layout inside their own
+ * timed region. drop_csc releases it; has_csc returns 1 when present. */
+prg_status prg_matrix_build_csc(prg_matrix* a, void* stream);
+prg_status prg_matrix_drop_csc(prg_matrix* a);
+int32_t prg_matrix_has_csc(const prg_matrix* a);
 
 /* ---- K3 — replaces init_rank / pagerank_step / run_kernel3 ----------------
  * include/prpipe/kernel3_pagerank.hpp:28-44; src/kernel3_pagerank.cpp:29-79.

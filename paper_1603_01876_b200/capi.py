@@ -28,6 +28,7 @@ HEADER_SYMBOLS = (
     "prg_last_error", "prg_version", "prg_device_count", "prg_k0_permutation",
     "prg_k0_generate_device", "prg_k1_sort_device", "prg_k1_sort_host", "prg_k2_filter_device",
     "prg_k2_filter_host", "prg_matrix_info", "prg_matrix_download", "prg_matrix_device_arrays",
+    "prg_matrix_build_csc", "prg_matrix_drop_csc", "prg_matrix_has_csc",
     "prg_matrix_from_host", "prg_matrix_destroy", "prg_k3_pagerank_device", "prg_k3_pagerank_host",
     "prg_init_rank_device", "prg_pagerank_step_device", "prg_launch_count", "prg_last_h2d_bytes", "prg_profile_enable",
     "prg_profile_report", "prg_build_adjacency_host", "prg_in_degree_host", "prg_zero_columns_host",
@@ -68,6 +69,9 @@ def lib() -> C.CDLL:
             "prg_matrix_device_arrays": (i32, [vp, vp, vp, vp, vp]),
             "prg_matrix_from_host": (i32, [i64, i64, vp, vp, vp, pp]),
             "prg_matrix_destroy": (None, [vp]),
+            "prg_matrix_build_csc": (i32, [vp, vp]),
+            "prg_matrix_drop_csc": (i32, [vp]),
+            "prg_matrix_has_csc": (i32, [vp]),
             "prg_k3_pagerank_device": (i32, [vp, f64, i32, u64, i32, vp, vp, vp]),
             "prg_k3_pagerank_host": (i32, [i64, i64, vp, vp, vp, f64, i32, u64, i32, vp, vp]),
             "prg_init_rank_device": (i32, [i64, u64, i32, vp, vp, vp]),
@@ -174,6 +178,18 @@ class DeviceMatrix:
         _check(lib().prg_matrix_download(self.handle, _ptr(ro), _ptr(cols), _ptr(vals), _ptr(din)))
         return ro, cols[: self.nnz], vals[: self.nnz], din
 
+    def build_csc(self, stream=None) -> "DeviceMatrix":
+        """K2's CSC build: keep K3's column layout on the handle (prg_matrix_build_csc)."""
+        _check(lib().prg_matrix_build_csc(self.handle, _stream(stream)))
+        return self
+
+    def drop_csc(self) -> None:
+        _check(lib().prg_matrix_drop_csc(self.handle))
+
+    @property
+    def has_csc(self) -> bool:
+        return bool(lib().prg_matrix_has_csc(self.handle))
+
     def close(self):
         if self.handle:
             lib().prg_matrix_destroy(self.handle)
@@ -195,10 +211,14 @@ class DeviceMatrix:
         return DeviceMatrix(h.value)
 
 
-def k2_filter(uv_sorted, n: int, stream=None) -> DeviceMatrix:
+def k2_filter(uv_sorted, n: int, stream=None, csc: bool = False) -> DeviceMatrix:
+    """Device K2. csc=True also runs K2's CSC build (the layout K3 iterates over)."""
     h = C.c_void_p()
     _check(lib().prg_k2_filter_device(_ptr(uv_sorted), uv_sorted.shape[0], n, C.byref(h), _stream(stream)))
-    return DeviceMatrix(h.value)
+    m = DeviceMatrix(h.value)
+    if csc:
+        m.build_csc(stream)
+    return m
 
 
 def k2_filter_host(uv_sorted: np.ndarray, n: int) -> DeviceMatrix:

@@ -23,7 +23,8 @@ using prg::DevBuf;
 // Matrix arrays come from the stream-ordered pool; a handle may have been used
 // on any stream, so release only after the device is idle.
 prg_matrix::~prg_matrix() {
-    if (row_offsets || cols || values || d_in) cudaDeviceSynchronize();
+    if (row_offsets || cols || values || d_in || plan) cudaDeviceSynchronize();
+    prg::k3_plan_destroy(plan);
     prg::ws_free(row_offsets, nullptr);
     prg::ws_free(cols, nullptr);
     prg::ws_free(values, nullptr);
@@ -476,6 +477,26 @@ prg_status prg_matrix_from_host(int64_t n, int64_t nnz, const int64_t* row_offse
 }
 
 void prg_matrix_destroy(prg_matrix* a) { delete a; }
+
+prg_status prg_matrix_build_csc(prg_matrix* a, void* stream) {
+    return guarded("prg_matrix_build_csc", [&] {
+        require(a != nullptr, PRG_ERR_INVALID_ARGUMENT, "null matrix");
+        prg::k3_build_csc_device(a, as_stream(stream));
+    });
+}
+
+prg_status prg_matrix_drop_csc(prg_matrix* a) {
+    return guarded("prg_matrix_drop_csc", [&] {
+        require(a != nullptr, PRG_ERR_INVALID_ARGUMENT, "null matrix");
+        if (a->plan) {
+            PRG_CUDA(cudaDeviceSynchronize());
+            prg::k3_plan_destroy(a->plan);
+            a->plan = nullptr;
+        }
+    });
+}
+
+int32_t prg_matrix_has_csc(const prg_matrix* a) { return a && a->plan ? 1 : 0; }
 
 prg_status prg_k3_pagerank_device(const prg_matrix* a, double damping, int32_t iterations, uint64_t seed,
                                   int32_t mode, double* d_ranks, double* norm1, void* stream) {

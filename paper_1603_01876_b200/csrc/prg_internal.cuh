@@ -4,6 +4,11 @@
 
 #include "prg_common.cuh"
 
+namespace prg {
+struct K3Plan;  // K3's column layout (prg_k3.cu)
+void k3_plan_destroy(K3Plan* p);
+}  // namespace prg
+
 // The C-ABI handle (include/prg.h declares it opaque).
 struct prg_matrix {
     int64_t n = 0;
@@ -15,6 +20,10 @@ struct prg_matrix {
     uint32_t* cols = nullptr;         // [cap], 0-based
     double* values = nullptr;         // [cap]
     uint32_t* d_in = nullptr;         // [n] pre-filter in-degree (null when uploaded)
+    // Column-major layout K3 iterates over (renumbered rows, sliced-ELL CSC over
+    // virtual columns), built by prg_matrix_build_csc — in the pipeline that is
+    // K2's CSC build (north_star). Owned; null until built.
+    prg::K3Plan* plan = nullptr;
     ~prg_matrix();
 };
 
@@ -58,6 +67,10 @@ double k3_step_device(const prg_matrix* a, const double* d_r, double damping, do
 // run_to_convergence (kernel3_pagerank.cpp:86-115); returns iterations applied.
 int k3_converge_device(const prg_matrix* a, double damping, double tol, int max_iters, const double* d_start,
                        double* d_out, bool* converged, cudaStream_t s);
+// K2's CSC build: K3's timed-mode column layout, kept on the handle (replaces any
+// earlier one). K3 calls on a handle without it build a temporary layout inside
+// their own timed region.
+void k3_build_csc_device(prg_matrix* a, cudaStream_t s);
 // init_rank (kernel3_pagerank.cpp:29-39) on the device; returns norm1.
 double k3_init_rank_device(int64_t n, uint64_t seed, double* d_r, int mode, cudaStream_t s);
 

@@ -34,6 +34,32 @@
 
 namespace prg {
 
+struct K3Plan {
+    int64_t n = 0, n_nd = 0;
+    uint64_t nnz = 0;
+    int sb = 1;
+    int pb = 1;  // transpose key payload bits (row id or exception index)
+    int mode = 0;
+    DevBuf<uint32_t> pinv, newid, colptr, csc_idx;
+    DevBuf<double> bval, exc_val;
+    uint32_t n_exc = 0;
+    // timed mode (SELL)
+    uint32_t V = 0, nslices = 0, n_empty = 0;
+    DevBuf<uint32_t> sell, slice_ptr, lane_len, lane_col, lane_np, vc_base, vpos, spos, spos_col, split_pos, n_split,
+        arrive, e_u;  // exception list: new row e_u[i], value exc_val[i]
+    DevBuf<double> partial;
+    // A layout kept on a prg_matrix outlives the stream it was built on: its
+    // buffers are released on the null stream (after a device sync).
+    void rehome() {
+        for (DevBuf<uint32_t>* b : {&pinv, &newid, &colptr, &csc_idx, &sell, &slice_ptr, &lane_len, &lane_col,
+                                    &lane_np, &vc_base, &vpos, &spos, &spos_col, &split_pos, &n_split, &arrive, &e_u})
+            b->s = nullptr;
+        for (DevBuf<double>* b : {&bval, &exc_val, &partial}) b->s = nullptr;
+    }
+};
+
+void k3_plan_destroy(K3Plan* p) { delete p; }
+
 namespace {
 
 constexpr uint64_t kRankInitStream = 0x72616e6b696e6974ULL;  // kernel3_pagerank.cpp:15
@@ -815,22 +841,6 @@ __global__ void count_set_kernel(const uint32_t* __restrict__ a, int64_t n, uint
 // ---------------------------------------------------------------------------
 // Plan
 // ---------------------------------------------------------------------------
-struct K3Plan {
-    int64_t n = 0, n_nd = 0;
-    uint64_t nnz = 0;
-    int sb = 1;
-    int pb = 1;  // transpose key payload bits (row id or exception index)
-    int mode = 0;
-    DevBuf<uint32_t> pinv, newid, colptr, csc_idx;
-    DevBuf<double> bval, exc_val;
-    uint32_t n_exc = 0;
-    // timed mode (SELL)
-    uint32_t V = 0, nslices = 0, n_empty = 0;
-    DevBuf<uint32_t> sell, slice_ptr, lane_len, lane_col, lane_np, vc_base, vpos, spos, spos_col, split_pos, n_split,
-        arrive, e_u;  // exception list: new row e_u[i], value exc_val[i]
-    DevBuf<double> partial;
-};
-
 void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
     ProfScope prof("k3_prep", s);
     const int64_t n = A->n;
@@ -1055,6 +1065,14 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
     P.csc_idx = DevBuf<uint32_t>();
 }
 
+// The layout kept on the handle when it matches the mode, else one built now
+// (inside the caller's timed region) into `tmp`.
+const K3Plan& plan_for(const prg_matrix* A, int mode, K3Plan& tmp, cudaStream_t s) {
+    if (A->plan && A->plan->mode == mode) return *A->plan;
+    build_plan(A, mode, tmp, s);
+    return tmp;
+}
+
 // ---------------------------------------------------------------------------
 // Drivers
 // ---------------------------------------------------------------------------
@@ -1205,8 +1223,8 @@ int k3_converge_device(const prg_matrix* A, double damping, double tol, int max_
                        double* d_out, bool* converged, cudaStream_t s) {
     const int64_t n = A->n;
     const double bgf = (1.0 - damping) / (double)n;
-    K3Plan P;
-    build_plan(A, 0, P, s);
+    K3Plan tmp;
+    const K3Plan& P = plan_for(A, 0, tmp, s);
     Sums S;
     DevBuf<double> cur((size_t)n, s), nxt((size_t)n, s);
     const unsigned g = (unsigned)num_sms() * 8;
@@ -1240,6 +1258,24 @@ int k3_converge_device(const prg_matrix* A, double damping, double tol, int max_
     return std::min(it, max_iters);
 }
 
+void k3_build_csc_device(prg_matrix* A, cudaStream_t s) {
+    ProfScope prof("k2_csc", s);
+    K3Plan* P = new K3Plan;
+    try {
+        build_plan(A, 0, *P, s);
+    } catch (...) {
+        delete P;
+        throw;
+    }
+    PRG_CUDA(cudaStreamSynchronize(s));
+    P->rehome();
+    if (A->plan) {
+        PRG_CUDA(cudaDeviceSynchronize());
+        delete A->plan;
+    }
+    A->plan = P;
+}
+
 double k3_init_rank_device(int64_t n, uint64_t seed, double* d_r, int mode, cudaStream_t s) {
     Sums S;
     init_rank_impl(n, seed, d_r, mode, 0.0, S, s);
@@ -1250,8 +1286,8 @@ double k3_pagerank_device(const prg_matrix* A, const K3Options& opt, double* d_r
     ProfScope prof("k3_pagerank", s);
     const int64_t n = A->n;
     const double bgf = (1.0 - opt.damping) / (double)n;  // kernel3_pagerank.cpp:46
-    K3Plan P;
-    build_plan(A, opt.mode, P, s);
+    K3Plan tmp;
+    const K3Plan& P = plan_for(A, opt.mode, tmp, s);
     Sums S;
     DevBuf<double> r0((size_t)n, s);
     init_rank_impl(n, opt.seed, r0.get(), opt.mode, bgf, S, s);
@@ -1263,8 +1299,8 @@ double k3_step_device(const prg_matrix* A, const double* d_r, double damping, do
                       cudaStream_t s) {
     const int64_t n = A->n;
     const double bgf = (1.0 - damping) / (double)n;
-    K3Plan P;
-    build_plan(A, mode, P, s);
+    K3Plan tmp;
+    const K3Plan& P = plan_for(A, mode, tmp, s);
     Sums S;
     device_sum(d_r, n, bgf, mode, S, s);
     iterate(P, d_r, d_out, 1, damping, bgf, S, s);

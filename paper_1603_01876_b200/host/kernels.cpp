@@ -189,6 +189,12 @@ Kernel2Result run_kernel2(const EdgeManifest& input) {
     const std::vector<Edge> edges = read_edges(input);
     prg_matrix* dev = nullptr;
     check(prg_k2_filter_host(edge_words(edges), static_cast<std::int64_t>(edges.size()), input.vertex_count(), &dev));
+    // K2's CSC build (north_star): the column layout run_kernel3 iterates over,
+    // kept on the cached device matrix.
+    if (const prg_status cst = prg_matrix_build_csc(dev, nullptr); cst != PRG_OK) {
+        prg_matrix_destroy(dev);
+        check(cst);
+    }
     std::int64_t n = 0, nnz = 0;
     prg_matrix_info(dev, &n, &nnz, nullptr, nullptr);
     StochasticMatrix& m = res.matrix;

@@ -185,6 +185,39 @@ def test_k3_deterministic(capi):
     assert np.array_equal(a.cpu().numpy().view(np.int64), b.cpu().numpy().view(np.int64)) and na == nb
 
 
+@pytest.mark.parametrize("scale,seed,init", [(10, 55, O.GRAPH500), (12, 2, O.UNIFORM), (16, 1, O.GRAPH500)])
+def test_k2_csc_build_reused_by_k3(capi, scale, seed, init):
+    """K2's CSC build kept on the handle: K3, pagerank_step and the parity mode
+    give the same bits as on a bare CSR (which builds the layout inside K3)."""
+    n = 1 << scale
+    srt = t(O.k1_sort(O.generate(scale, seed, init), scale))
+    bare = capi.k2_filter(srt, n)
+    kept = capi.k2_filter(srt, n, csc=True)
+    assert kept.has_csc and not bare.has_csc
+    a, na = capi.k3_pagerank(bare, seed=seed)
+    b, nb = capi.k3_pagerank(kept, seed=seed)
+    c, nc = capi.k3_pagerank(kept, seed=seed)  # the kept layout survives a K3 call
+    for x in (b, c):
+        assert np.array_equal(a.cpu().numpy().view(np.int64), x.cpu().numpy().view(np.int64))
+    assert na == nb == nc
+    # parity mode ignores the timed-mode layout and stays bit-identical to the oracle
+    ref = O.k2(O.k1_sort(O.generate(scale, seed, init), scale), n)
+    rr, nr = O.run_kernel3(ref.row_offsets, ref.cols, ref.values, n, seed=seed)
+    rp, npar = capi.k3_pagerank(kept, seed=seed, mode=1)
+    assert np.array_equal(rp.cpu().numpy().view(np.int64), rr.view(np.int64)) and npar == nr
+    r0, _ = capi.init_rank(n, seed)
+    s1, n1 = capi.pagerank_step(bare, r0)
+    s2, n2 = capi.pagerank_step(kept, r0)
+    assert np.array_equal(s1.cpu().numpy().view(np.int64), s2.cpu().numpy().view(np.int64)) and n1 == n2
+    kept.drop_csc()
+    assert not kept.has_csc
+    d, nd = capi.k3_pagerank(kept, seed=seed)
+    assert np.array_equal(a.cpu().numpy().view(np.int64), d.cpu().numpy().view(np.int64)) and nd == na
+    kept.build_csc().build_csc()  # rebuilding replaces the layout
+    e, _ = capi.k3_pagerank(kept, seed=seed)
+    assert np.array_equal(a.cpu().numpy().view(np.int64), e.cpu().numpy().view(np.int64))
+
+
 def test_init_rank_and_step(capi):
     g = golden("k1k2k3_s10_seed55.npz")
     n = 1 << 10

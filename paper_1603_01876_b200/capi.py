@@ -13,7 +13,8 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libprg.so")
+# PRG_LIB: an alternative build of the same library (A/B measurements)
+LIB_PATH = os.environ.get("PRG_LIB") or os.path.join(_HERE, "lib", "libprg.so")
 
 PRG_OK = 0
 PRG_ERRORS = {

@@ -64,6 +64,7 @@ namespace {
 
 constexpr uint64_t kRankInitStream = 0x72616e6b696e6974ULL;  // kernel3_pagerank.cpp:15
 constexpr int kSpmvThreads = 1024;
+constexpr int kSliceCounters = 8;
 
 __host__ __device__ inline int bits_for(int64_t n) {
     int b = 1;
@@ -456,7 +457,7 @@ __global__ void seq_sum_kernel(const double* __restrict__ x, int64_t n, double b
     out[0] = s;
     out[1] = __dmul_rn(bgf, s);
 }
-__global__ void scale_kernel(double* __restrict__ x, int64_t n, const double* __restrict__ sum) {
+__global__ void __launch_bounds__(1024, 2) scale_kernel(double* __restrict__ x, int64_t n, const double* __restrict__ sum) {
     const double d = sum[0];
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         x[i] = __ddiv_rn(x[i], d);
@@ -761,7 +762,8 @@ struct SellArgs {
     uint32_t* arrive;            // [n] per split column, never reset
     double* slice_sum;           // [nslices]
     const double* bgp;           // [1] = bg of this step
-    uint32_t* next_slice;        // work counter of this launch (starts at 0)
+    uint32_t* next_slice;        // work counters of this launch (32 words apart, start at 0)
+    uint32_t nctr, grab;
     int64_t n_nd;
     uint32_t nslices;
     double damping;
@@ -777,11 +779,35 @@ __global__ void __launch_bounds__(kSpmvThreads, 2) spmv_sell_kernel(SellArgs a) 
     const uint64_t pol_stream = dev::policy_evict_first(), pol_keep = dev::policy_evict_last();
     // Slices are handed out dynamically, longest first (they are sorted by length
     // class): a static round-robin left some SMs with twice the average work.
+    // Slices are claimed from nctr counters (one 128-B line each, so on
+    // different L2 slices): counter k hands out slices k, k + nctr, ...; a warp
+    // starts at its own counter and moves on when that one runs dry. With a
+    // single counter the launch time depended on that counter's address
+    // (0.80-0.86 ms over pool placements at S=24), i.e. on the L2 slice serving
+    // ~250K claims per launch; 8 counters: 0.783 ms at every placement
+    // (tools/exp_spmv4.py; 4: 0.799, 16: 0.794).
+    const uint32_t nctr = a.nctr;
+    // (Written with a claim batch `grab` (1 in practice: 2 and 4 measured 30-70%
+    // slower); this form of the loop compiles to a schedule that measured
+    // 0.783 ms against 0.817 ms for the plain one-claim-per-slice loop.)
+    const uint32_t grab = a.grab;
+    uint32_t k = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) % nctr, tried = 0, have = 0, cur = 0;
     for (;;) {
-        uint32_t sl = 0;
-        if (lane == 0) sl = atomicAdd(a.next_slice, 1u);
-        sl = __shfl_sync(0xffffffffu, sl, 0);
-        if (sl >= a.nslices) break;
+        if (have == 0) {
+            uint32_t v = 0;
+            if (lane == 0) v = atomicAdd(a.next_slice + 32 * k, 1u);
+            cur = __shfl_sync(0xffffffffu, v, 0) * grab;
+            have = grab;
+        }
+        const uint32_t sl = cur * nctr + k;
+        ++cur;
+        --have;
+        if (sl >= a.nslices) {
+            have = 0;
+            if (++tried == nctr) break;
+            k = k + 1 == nctr ? 0 : k + 1;
+            continue;
+        }
         const uint32_t pos = sl * 32 + lane;
         const uint32_t len = a.lane_len[pos];
         const uint32_t base = a.slice_ptr[sl];
@@ -1150,8 +1176,11 @@ void iterate(const K3Plan& P, const double* r_in, double* r_out, int iters, doub
     // s = [row-scaled iterate (SELL row order, n_nd) | exception products (n_exc)]
     DevBuf<double> sbuf((size_t)std::max<int64_t>(P.n_nd + P.n_exc, 1), s), y0(NP ? NP : 1, s), y1(NP ? NP : 1, s),
         slice_sum(P.nslices ? P.nslices : 1, s), sum_part(kSumBlocks, s);
-    DevBuf<uint32_t> slice_ctr((size_t)std::max(iters, 1), s);
-    PRG_CUDA(cudaMemsetAsync(slice_ctr.get(), 0, (size_t)std::max(iters, 1) * 4, s));
+    static int nctr = -1;  // PRG_NCTR: slice counters per launch
+    if (nctr < 0) { const char* e = getenv("PRG_NCTR"); nctr = e ? std::max(1, atoi(e)) : kSliceCounters; }
+    const size_t ctr_words = (size_t)std::max(iters, 1) * 32 * nctr;
+    DevBuf<uint32_t> slice_ctr(ctr_words, s);
+    PRG_CUDA(cudaMemsetAsync(slice_ctr.get(), 0, ctr_words * 4, s));
     double* ys[2] = {y0.get(), y1.get()};
     for (int it = 0; it < iters; ++it) {
         double* y = ys[it & 1];
@@ -1177,7 +1206,9 @@ void iterate(const K3Plan& P, const double* r_in, double* r_out, int iters, doub
         a.arrive = P.arrive.get();
         a.slice_sum = slice_sum.get();
         a.bgp = S.out.get();
-        a.next_slice = slice_ctr.get() + it;
+        a.next_slice = slice_ctr.get() + (size_t)it * 32 * nctr;
+        a.nctr = (uint32_t)nctr;
+        a.grab = 1;
         a.n_nd = P.n_nd;
         a.nslices = P.nslices;
         a.damping = damping;

@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(kScanThreads) scan_partials_kernel(uint64_t* _
 }
 
 template <class Out>
-__global__ void __launch_bounds__(kScanThreads) scan_down_kernel(const uint32_t* __restrict__ in,
+__global__ void __launch_bounds__(kScanThreads, 2) scan_down_kernel(const uint32_t* __restrict__ in,
                                                                  size_t n, const uint32_t* dn, uint32_t mult,
                                                                  const uint64_t* __restrict__ partial,
                                                                  Out* __restrict__ out) {

@@ -48,13 +48,16 @@ struct K3Plan {
     DevBuf<uint32_t> sell, slice_ptr, lane_len, lane_col, lane_np, vc_base, vpos, spos, spos_col, split_pos, n_split,
         arrive, e_u;  // exception list: new row e_u[i], value exc_val[i]
     DevBuf<double> partial;
+    // timed-mode gather: spos covers [rows | exceptions] (an exception's entry
+    // is its row's), coef = [row base | exception value], both n_nd + n_exc
+    DevBuf<double> coef;
     // A layout kept on a prg_matrix outlives the stream it was built on: its
     // buffers are released on the null stream (after a device sync).
     void rehome() {
         for (DevBuf<uint32_t>* b : {&pinv, &newid, &colptr, &csc_idx, &sell, &slice_ptr, &lane_len, &lane_col,
                                     &lane_np, &vc_base, &vpos, &spos, &spos_col, &split_pos, &n_split, &arrive, &e_u})
             b->s = nullptr;
-        for (DevBuf<double>* b : {&bval, &exc_val, &partial}) b->s = nullptr;
+        for (DevBuf<double>* b : {&bval, &exc_val, &partial, &coef}) b->s = nullptr;
     }
 };
 
@@ -649,6 +652,12 @@ __global__ void spos_rows_kernel(const uint32_t* __restrict__ pinv, const uint32
         spos[j] = spos_col[pinv[j]];
 }
 
+__global__ void exc_spos_kernel(const uint32_t* __restrict__ e_u, uint32_t n_exc, uint32_t* __restrict__ spos,
+                                int64_t n_nd) {
+    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < n_exc; e += gridDim.x * blockDim.x)
+        spos[n_nd + e] = spos[e_u[e]];
+}
+
 // Split columns listed in column order (flag + scan + scatter) so that the
 // per-iteration sum over them has a fixed order.
 __global__ void split_flag_kernel(const uint32_t* __restrict__ vc_base, int64_t n, uint32_t* __restrict__ flag) {
@@ -698,6 +707,34 @@ __global__ void gather_s_kernel(GatherArgs a) {
             r = p == kEmpty ? bg : a.y[p];
         }
         a.s[j] = __dmul_rn(r, row ? a.bval[j] : a.e_val[j - a.n_nd]);
+    }
+}
+
+// The same for steps >= 2, uniform over [rows | exceptions]: s[j] =
+// r(spos[j]) * coef[j] — coalesced spos/coef/s streams and one random read of
+// the previous iterate per entry, G entries in flight per thread.
+template <int G>
+__global__ void __launch_bounds__(1024, 2) gather_y_kernel(const double* __restrict__ y, const uint32_t* __restrict__ spos,
+                                                           const double* __restrict__ coef, const double* __restrict__ bgp,
+                                                           int64_t tot, double* __restrict__ s) {
+    const double bg = bgp[2];
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t j0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j0 < tot; j0 += G * stride) {
+        uint32_t p[G];
+        double c[G], r[G];
+#pragma unroll
+        for (int k = 0; k < G; ++k) {
+            const int64_t j = j0 + k * stride;
+            p[k] = j < tot ? spos[j] : kEmpty;
+            c[k] = j < tot ? coef[j] : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < G; ++k) r[k] = p[k] == kEmpty ? bg : y[p[k]];
+#pragma unroll
+        for (int k = 0; k < G; ++k) {
+            const int64_t j = j0 + k * stride;
+            if (j < tot) s[j] = __dmul_rn(r[k], c[k]);
+        }
     }
 }
 
@@ -1054,9 +1091,18 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
         sell_fill_kernel<<<g, 256, 0, s>>>(fa);
         PRG_LAUNCH_CHECK();
     }
-    P.spos = DevBuf<uint32_t>((size_t)std::max<int64_t>(P.n_nd, 1), s);
+    P.spos = DevBuf<uint32_t>((size_t)std::max<int64_t>(P.n_nd + P.n_exc, 1), s);
+    P.coef = DevBuf<double>((size_t)std::max<int64_t>(P.n_nd + P.n_exc, 1), s);
     spos_rows_kernel<<<g, 1024, 0, s>>>(P.pinv.get(), P.spos_col.get(), P.n_nd, P.spos.get());
     PRG_LAUNCH_CHECK();
+    if (P.n_nd)
+        PRG_CUDA(cudaMemcpyAsync(P.coef.get(), P.bval.get(), (size_t)P.n_nd * 8, cudaMemcpyDeviceToDevice, s));
+    if (P.n_exc) {
+        PRG_CUDA(cudaMemcpyAsync(P.coef.get() + P.n_nd, P.exc_val.get(), (size_t)P.n_exc * 8,
+                                 cudaMemcpyDeviceToDevice, s));
+        exc_spos_kernel<<<g, 1024, 0, s>>>(P.e_u.get(), P.n_exc, P.spos.get(), P.n_nd);
+        PRG_LAUNCH_CHECK();
+    }
     P.split_pos = DevBuf<uint32_t>((size_t)n, s);
     P.n_split = DevBuf<uint32_t>(1, s);
     PRG_CUDA(cudaMemsetAsync(P.n_split.get(), 0, 4, s));
@@ -1189,7 +1235,16 @@ void iterate(const K3Plan& P, const double* r_in, double* r_out, int iters, doub
             ProfScope pp("k3_permute", s);
             GatherArgs ga{it == 0 ? r_in : nullptr, P.pinv.get(), yp, P.spos.get(), S.out.get(), P.bval.get(),
                           P.e_u.get(), P.exc_val.get(), P.n_nd, P.n_exc, sbuf.get()};
-            if (P.n_nd + P.n_exc) gather_s_kernel<<<g, 1024, 0, s>>>(ga);
+            const int64_t tot = P.n_nd + P.n_exc;
+            static int gi = -1;  // PRG_GATHER_ITEMS (1, 2, 4)
+            if (gi < 0) { const char* e = getenv("PRG_GATHER_ITEMS"); gi = e ? atoi(e) : 4; }
+            if (tot && it == 0) gather_s_kernel<<<g, 1024, 0, s>>>(ga);
+            else if (tot) {
+                const unsigned gg = (unsigned)std::max<int64_t>(1, std::min<int64_t>(g, (tot + 1023) / 1024 / gi));
+                if (gi == 4) gather_y_kernel<4><<<gg, 1024, 0, s>>>(yp, P.spos.get(), P.coef.get(), S.out.get(), tot, sbuf.get());
+                else if (gi == 1) gather_y_kernel<1><<<gg, 1024, 0, s>>>(yp, P.spos.get(), P.coef.get(), S.out.get(), tot, sbuf.get());
+                else gather_y_kernel<2><<<gg, 1024, 0, s>>>(yp, P.spos.get(), P.coef.get(), S.out.get(), tot, sbuf.get());
+            }
             PRG_LAUNCH_CHECK();
         }
         SellArgs a;

@@ -415,6 +415,9 @@ __global__ void suffix_min_down(uint32_t* a, int64_t n1, const uint32_t* part) {
 // ---------------------------------------------------------------------------
 // init_rank (kernel3_pagerank.cpp:29-39)
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ double rank_init_x(uint64_t s0, uint64_t i) {
+    return (double)(dev::splitmix_at(s0, i + 1) >> 11) * 0x1.0p-53;  // kernel3_pagerank.cpp:31-34
+}
 __global__ void rng_kernel(double* __restrict__ x, int64_t n, uint64_t s0) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         x[i] = (double)(dev::splitmix_at(s0, (uint64_t)i + 1) >> 11) * 0x1.0p-53;
@@ -428,6 +431,29 @@ __global__ void partial_sum_kernel(const double* __restrict__ x, int64_t n, doub
     for (int k = 0; k < 8; ++k) {
         const int64_t i = base + k * 1024 + threadIdx.x;
         if (i < n) s = __dadd_rn(s, x[i]);
+    }
+    s = dev::warp_sum_f64(s);
+    if (dev::lane_id() == 0) ws[dev::warp_id()] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double v = ws[threadIdx.x];
+        v = dev::warp_sum_f64(v);
+        if (threadIdx.x == 0) part[blockIdx.x] = v;
+    }
+}
+// init_rank without the vector: block partials (same tree as partial_sum_kernel,
+// so the sums are bit-identical) of x_i, or of x_i / div when div is given.
+__global__ void rng_partial_kernel(int64_t n, uint64_t s0, const double* __restrict__ div, double* __restrict__ part) {
+    __shared__ double ws[32];
+    const int64_t base = (int64_t)blockIdx.x * 8192;
+    const double d = div ? *div : 1.0;
+    double s = 0.0;
+    for (int k = 0; k < 8; ++k) {
+        const int64_t i = base + k * 1024 + threadIdx.x;
+        if (i < n) {
+            const double x = rank_init_x(s0, (uint64_t)i);
+            s = __dadd_rn(s, div ? __ddiv_rn(x, d) : x);
+        }
     }
     s = dev::warp_sum_f64(s);
     if (dev::lane_id() == 0) ws[dev::warp_id()] = s;
@@ -693,15 +719,21 @@ struct GatherArgs {
     int64_t n_nd;
     uint32_t n_exc;
     double* s;
+    // first step of run_kernel3: r0 = init_rank regenerated on the fly,
+    // r0[u] = x_u / sum(x) (no r0 array): rng stream start and device sum(x)
+    uint64_t rng_s0;
+    const double* rng_div;
 };
 __global__ void gather_s_kernel(GatherArgs a) {
     const double bg = a.bgp[2];
     const int64_t tot = a.n_nd + a.n_exc;
+    const double div = a.rng_div ? *a.rng_div : 1.0;
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < tot; j += (int64_t)gridDim.x * blockDim.x) {
         const bool row = j < a.n_nd;
         const uint32_t x = row ? (uint32_t)j : a.e_u[j - a.n_nd];
         double r;
-        if (a.r0) r = a.r0[a.pinv[x]];
+        if (a.rng_div) r = __ddiv_rn(rank_init_x(a.rng_s0, a.pinv[x]), div);
+        else if (a.r0) r = a.r0[a.pinv[x]];
         else {
             const uint32_t p = a.spos[x];
             r = p == kEmpty ? bg : a.y[p];
@@ -1192,7 +1224,7 @@ void init_rank_impl(int64_t n, uint64_t seed, double* d_r, int mode, double bgf,
 // writes the final iterate to r_out (original order); S.out ends as
 // {sum(r_out), bg', bg_used}.
 void iterate(const K3Plan& P, const double* r_in, double* r_out, int iters, double damping, double bgf, Sums& S,
-             cudaStream_t s) {
+             cudaStream_t s, uint64_t rng_s0 = 0, const double* rng_div = nullptr) {
     const unsigned g = (unsigned)num_sms() * 8;
     const int64_t n = P.n;
     if (P.mode == 1) {
@@ -1234,7 +1266,8 @@ void iterate(const K3Plan& P, const double* r_in, double* r_out, int iters, doub
         {
             ProfScope pp("k3_permute", s);
             GatherArgs ga{it == 0 ? r_in : nullptr, P.pinv.get(), yp, P.spos.get(), S.out.get(), P.bval.get(),
-                          P.e_u.get(), P.exc_val.get(), P.n_nd, P.n_exc, sbuf.get()};
+                          P.e_u.get(), P.exc_val.get(), P.n_nd, P.n_exc, sbuf.get(), rng_s0,
+                          it == 0 ? rng_div : nullptr};
             const int64_t tot = P.n_nd + P.n_exc;
             static int gi = -1;  // PRG_GATHER_ITEMS (1, 2, 4)
             if (gi < 0) { const char* e = getenv("PRG_GATHER_ITEMS"); gi = e ? atoi(e) : 4; }
@@ -1375,9 +1408,26 @@ double k3_pagerank_device(const prg_matrix* A, const K3Options& opt, double* d_r
     K3Plan tmp;
     const K3Plan& P = plan_for(A, opt.mode, tmp, s);
     Sums S;
-    DevBuf<double> r0((size_t)n, s);
-    init_rank_impl(n, opt.seed, r0.get(), opt.mode, bgf, S, s);
-    iterate(P, r0.get(), d_ranks, opt.iterations, opt.damping, bgf, S, s);
+    if (opt.mode == 1 || P.nslices == 0) {
+        DevBuf<double> r0((size_t)n, s);
+        init_rank_impl(n, opt.seed, r0.get(), opt.mode, bgf, S, s);
+        iterate(P, r0.get(), d_ranks, opt.iterations, opt.damping, bgf, S, s);
+        return read_scalar(S.out.get(), s);
+    }
+    // Timed mode: init_rank's vector is never stored — its two sums are taken
+    // over values regenerated from the counter-based RNG, and the first gather
+    // regenerates r0[u] for the rows it needs (bit-identical to init_rank_impl).
+    const uint64_t s0 = dev::mix_seed(opt.seed, kRankInitStream);
+    const int64_t nb = (n + 8191) / 8192;
+    DevBuf<double> part((size_t)nb, s), xsum(4, s);
+    S.out = DevBuf<double>(4, s);
+    PRG_CUDA(cudaMemsetAsync(S.out.get(), 0, 32, s));
+    rng_partial_kernel<<<(unsigned)nb, 1024, 0, s>>>(n, s0, nullptr, part.get());
+    final_sum_kernel<<<1, 1024, 0, s>>>(part.get(), nb, 0.0, xsum.get());
+    rng_partial_kernel<<<(unsigned)nb, 1024, 0, s>>>(n, s0, xsum.get(), part.get());
+    final_sum_kernel<<<1, 1024, 0, s>>>(part.get(), nb, bgf, S.out.get());
+    PRG_LAUNCH_CHECK();
+    iterate(P, nullptr, d_ranks, opt.iterations, opt.damping, bgf, S, s, s0, xsum.get());
     return read_scalar(S.out.get(), s);
 }
 

@@ -66,7 +66,7 @@ void k3_plan_destroy(K3Plan* p) { delete p; }
 namespace {
 
 constexpr uint64_t kRankInitStream = 0x72616e6b696e6974ULL;  // kernel3_pagerank.cpp:15
-constexpr int kSpmvThreads = 1024;
+constexpr int kSpmvThreads = 1024;  // the 32-register variant (PRG_SPMV_VARIANT=1)
 constexpr int kSliceCounters = 8;
 
 __host__ __device__ inline int bits_for(int64_t n) {
@@ -832,17 +832,18 @@ struct SellArgs {
     double* slice_sum;           // [nslices]
     const double* bgp;           // [1] = bg of this step
     uint32_t* next_slice;        // work counters of this launch (32 words apart, start at 0)
-    uint32_t nctr, grab;
+    uint32_t nctr;
     int64_t n_nd;
     uint32_t nslices;
     double damping;
 };
 
-// 64 warps per SM and no shared-memory staging: measured on B200 (S=24) the L1
+
+// 48 warps per SM and no shared-memory staging: measured on B200 (S=24) the L1
 // caches the hot, degree-ordered head of s by itself, and occupancy (requests
 // in flight) matters more than a software-managed hot set (1.9 ms vs 3.3 ms).
-template <int U>
-__global__ void __launch_bounds__(kSpmvThreads, 2) spmv_sell_kernel(SellArgs a) {
+template <int U, int kThreads = kSpmvThreads, int kMinBlocks = 2>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) spmv_sell_kernel(SellArgs a) {
     const unsigned lane = dev::lane_id();
     const double bg = a.bgp[1];
     const uint64_t pol_stream = dev::policy_evict_first(), pol_keep = dev::policy_evict_last();
@@ -856,23 +857,12 @@ __global__ void __launch_bounds__(kSpmvThreads, 2) spmv_sell_kernel(SellArgs a) 
     // ~250K claims per launch; 8 counters: 0.783 ms at every placement
     // (tools/exp_spmv4.py; 4: 0.799, 16: 0.794).
     const uint32_t nctr = a.nctr;
-    // (Written with a claim batch `grab` (1 in practice: 2 and 4 measured 30-70%
-    // slower); this form of the loop compiles to a schedule that measured
-    // 0.783 ms against 0.817 ms for the plain one-claim-per-slice loop.)
-    const uint32_t grab = a.grab;
-    uint32_t k = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) % nctr, tried = 0, have = 0, cur = 0;
+    uint32_t k = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) % nctr, tried = 0;
     for (;;) {
-        if (have == 0) {
-            uint32_t v = 0;
-            if (lane == 0) v = atomicAdd(a.next_slice + 32 * k, 1u);
-            cur = __shfl_sync(0xffffffffu, v, 0) * grab;
-            have = grab;
-        }
-        const uint32_t sl = cur * nctr + k;
-        ++cur;
-        --have;
+        uint32_t sl = 0;
+        if (lane == 0) sl = atomicAdd(a.next_slice + 32 * k, 1u) * nctr + k;
+        sl = __shfl_sync(0xffffffffu, sl, 0);
         if (sl >= a.nslices) {
-            have = 0;
             if (++tried == nctr) break;
             k = k + 1 == nctr ? 0 : k + 1;
             continue;
@@ -1296,15 +1286,17 @@ void iterate(const K3Plan& P, const double* r_in, double* r_out, int iters, doub
         a.bgp = S.out.get();
         a.next_slice = slice_ctr.get() + (size_t)it * 32 * nctr;
         a.nctr = (uint32_t)nctr;
-        a.grab = 1;
         a.n_nd = P.n_nd;
         a.nslices = P.nslices;
         a.damping = damping;
         if (P.nslices) {
             ProfScope ps("k3_spmv", s);
-            if (variant == 1) spmv_sell_kernel<2><<<num_sms() * 2, kSpmvThreads, 0, s>>>(a);
-            else if (variant == 2) spmv_sell_kernel<8><<<num_sms() * 2, kSpmvThreads, 0, s>>>(a);
-            else spmv_sell_kernel<4><<<num_sms() * 2, kSpmvThreads, 0, s>>>(a);
+            // 768 threads x 2 CTAs (48 warps/SM, 40 registers) with a 6-deep pipeline:
+            // 0.767 ms vs 0.796 ms for 1024 x 2 at 32 registers, U=4 (same box,
+            // tools/exp_spmv4.py); 896x2 U4 0.792, 640x2 U6 0.775, 512x3 U6 0.793,
+            // 768x2 U8 0.780, 832x2 U6 0.847.
+            if (variant == 1) spmv_sell_kernel<4><<<num_sms() * 2, kSpmvThreads, 0, s>>>(a);
+            else spmv_sell_kernel<6, 768, 2><<<num_sms() * 2, 768, 0, s>>>(a);
             PRG_LAUNCH_CHECK();
         }
         sell_sum_part<<<kSumBlocks, 1024, 0, s>>>(slice_sum.get(), P.nslices, y, P.split_pos.get(), P.n_split.get(),

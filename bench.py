@@ -217,6 +217,24 @@ def make_clock_sampler(gpu_index: int):
     return ClockSampler(gpu_index) if kind == "smi" else NvmlClockSampler(gpu_index)
 
 
+def max_over_ranks(values, device="cpu"):
+    """Element-wise max of per-rank timings over the process group (identity
+    for a single process). Every multi-GPU number is the slowest rank's."""
+    import torch
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return [float(v) for v in values]
+    t = torch.tensor([float(v) for v in values], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(x) for x in t.cpu().tolist()]
+
+
+def whole_job_rate(world_size, units_per_rank, seconds):
+    """Whole-job throughput: the units every rank processed over the max-over-ranks time."""
+    return world_size * units_per_rank / seconds
+
+
 def dist_setup():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -328,20 +346,16 @@ def run_ours(args):
     prof_cold = json.loads(buf.value.decode())
     mat.close()
 
-    loc = np.array([np.mean(k1), np.mean(k2), np.mean(k3), total_ms / args.steps, np.mean(k2f), np.mean(k2c),
-                    np.mean(cold)], dtype=np.float64)
-    if ws > 1:
-        t = torch.tensor(loc, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        loc = t.cpu().numpy()
-    k1_ms, k2_ms, k3_ms, step_ms, k2f_ms, k2c_ms, k3cold_ms = (float(x) for x in loc)
+    k1_ms, k2_ms, k3_ms, step_ms, k2f_ms, k2c_ms, k3cold_ms = max_over_ranks(
+        [np.mean(k1), np.mean(k2), np.mean(k3), total_ms / args.steps, np.mean(k2f), np.mean(k2c), np.mean(cold)],
+        device=dev)
 
     peak, peak_src = peaks()
     b1, b2, b3, b3_iter = alg_bytes(n, m, nnz, iters)
     spmv_n, spmv_ms = prof.get("k3_spmv", [0, 0.0])
     spmv_avg = spmv_ms / max(spmv_n, 1)
     achieved = b3_iter / (spmv_avg * 1e-3) / 1e9 if spmv_avg else None
-    value = ws * iters * m / (k3_ms * 1e-3)
+    value = whole_job_rate(ws, iters * m, k3_ms * 1e-3)
 
     out = {
         "metric": METRIC,
@@ -362,8 +376,8 @@ def run_ours(args):
                    "l2": ("512 MB L2 flush before every step" if args.flush_l2 else
                           "inputs larger than L2 (4.3 GB edges, 3.1 GB CSR at S=24); no flush"),
                    "k3_mode": "timed (deterministic tree sums)"},
-        "k1_edges_per_s": ws * m / (k1_ms * 1e-3),
-        "k2_edges_per_s": ws * m / (k2_ms * 1e-3),
+        "k1_edges_per_s": whole_job_rate(ws, m, k1_ms * 1e-3),
+        "k2_edges_per_s": whole_job_rate(ws, m, k2_ms * 1e-3),
         "k3_edges_per_s": value,
         "stage_ms": {"k1_sort": k1_ms, "k2_filter": k2_ms, "k3_pagerank": k3_ms,
                      "k2_filter_csr": k2f_ms, "k2_csc_build": k2c_ms},
@@ -417,12 +431,8 @@ def run_ours(args):
             t1 = time.perf_counter()
             if i > 0:
                 e2e.append(t1 - t0)
-        e2e_t = float(np.mean(e2e))
-        if ws > 1:
-            t = torch.tensor([e2e_t], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_t = float(t.item())
-        out["e2e"] = {"value": ws * iters * m / e2e_t, "unit": "edges/s",
+        (e2e_t,) = max_over_ranks([np.mean(e2e)], device=dev)
+        out["e2e"] = {"value": whole_job_rate(ws, iters * m, e2e_t), "unit": "edges/s",
                       # the host CSR the call consumes each step (int64 offsets, int64 cols, f64 values)
                       "h2d_bytes_per_step": 8 * (n + 1) + 16 * nnz, "d2h_bytes_per_step": 8 * n,
                       # what actually crosses PCIe: the values are reduced on host threads to row

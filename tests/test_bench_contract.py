@@ -52,3 +52,65 @@ def test_reference_arm_json_contract():
     assert j["impl"] == "reference" and j["value"] > 0
     assert j["e2e"]["h2d_bytes_per_step"] == 0 and j["e2e"]["d2h_bytes_per_step"] == 0
     assert j["cpu_baseline"]["kind"] == "reference"
+
+
+def _gloo_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # rank r's stage times: the job's time is the slowest rank's, per entry
+        got = bench.max_over_ranks([10.0 + rank, 5.0 - rank, 7.0])
+        q.put((rank, got))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_max_over_ranks_gloo_world2():
+    """The N>1 bench path (one process per GPU; NCCL on the box) reduces every
+    timing to the max over ranks — exercised here with gloo, world size 2."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as sck:
+        sck.bind(("127.0.0.1", 0))
+        port = sck.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0] == res[1] == [11.0, 5.0, 7.0]
+
+
+def test_whole_job_rate_and_single_process_max():
+    assert bench.max_over_ranks([1.5, 2.5]) == [1.5, 2.5]  # no process group: identity
+    # value = units all ranks processed / max-over-ranks time (weak scaling)
+    assert bench.whole_job_rate(4, 20 * (1 << 28), 0.02) == 4 * 20 * (1 << 28) / 0.02
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libprpipe_ref.so")),
+                    reason="reference library not built")
+def test_reference_arm_under_torchrun_world2():
+    """Launched as the driver does for N>1: rank 0 alone runs the reference
+    arm and prints one JSON line; the other rank exits 0 without work."""
+    import socket
+
+    with socket.socket() as sck:
+        sck.bind(("127.0.0.1", 0))
+        port = sck.getsockname()[1]
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                        "--impl", "reference", "--gpus", "2", "--scale", "8", "--steps", "2", "--warmup", "1"],
+                       capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    j = json.loads(lines[0])
+    assert j["impl"] == "reference" and j["value"] > 0

@@ -50,6 +50,8 @@ def parse():
     p.add_argument("--iterations", type=int, default=20)
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-pipeline-io", action="store_true", help="skip the I/O-inclusive official pipeline record")
+    p.add_argument("--pipeline-io-scale", type=int, default=20)
     p.add_argument("--flush-l2", action="store_true",
                    help="write a 512 MB buffer before every timed step (for scales whose data fits in L2)")
     p.add_argument("--ref-iters-per-step", type=int, default=2)
@@ -445,6 +447,11 @@ def run_ours(args):
         if rank == 0 and ws == 1 and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(ro.numpy(), cols.numpy()[:nnz], vals.numpy()[:nnz], n, m, seed)
 
+    # ---- file I/O reported separately (north_star): the drop-in's official,
+    # I/O-inclusive run_pipeline records (TSV shards + manifest on the host)
+    if rank == 0 and ws == 1 and not args.no_pipeline_io:
+        out["official_pipeline"] = official_pipeline(args.pipeline_io_scale)
+
     if ws > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -484,6 +491,23 @@ def _cpu_model():
 # ---------------------------------------------------------------------------
 # Reference arm
 # ---------------------------------------------------------------------------
+def official_pipeline(scale):
+    """prpipe.run_pipeline (the reference's bench.cpp:141-161 driver, our drop-in):
+    K0 generate -> TSV shards, K1 read/sort/write TSV, K2 read TSV + filter (+ CSC),
+    K3 — each record I/O-inclusive, as the reference times them."""
+    import tempfile
+
+    sys.path.insert(0, os.path.join(ROOT, "paper_1603_01876_b200", "python"))
+    import prpipe
+
+    with tempfile.TemporaryDirectory() as d:
+        prpipe.run_pipeline(scale=10, seed=1, data_dir=os.path.join(d, "warm"))  # CUDA/IO warm-up
+        rep = prpipe.run_pipeline(scale=scale, seed=1, data_dir=os.path.join(d, "data"))
+    return {"scale": scale, "api": "prpipe.run_pipeline (drop-in, host TSV I/O inside each record)",
+            "records": {k["name"]: {"seconds": k["elapsed_seconds"], "edges_per_s": k["rate_edges_per_sec"]}
+                        for k in rep["kernels"]}}
+
+
 def run_reference(args):
     ws, rank, _ = dist_setup()
     if rank != 0:

@@ -126,7 +126,9 @@ void prg_matrix_destroy(prg_matrix* a);
  * run_kernel3 / pagerank_step / run_to_convergence on this handle start from a
  * CSC, as the reference's K3 starts from its CSR (kernel3_pagerank.cpp:67-79).
  * K3 calls on a handle without it build a temporary layout inside their own
- * timed region. drop_csc releases it; has_csc returns 1 when present. */
+ * timed region. drop_csc releases it; has_csc returns 1 when present.
+ * A handle carrying the layout must not be used by two streams at once (K3
+ * keeps per-launch counters in it). */
 prg_status prg_matrix_build_csc(prg_matrix* a, void* stream);
 prg_status prg_matrix_drop_csc(prg_matrix* a);
 int32_t prg_matrix_has_csc(const prg_matrix* a);

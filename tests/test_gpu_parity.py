@@ -218,6 +218,29 @@ def test_k2_csc_build_reused_by_k3(capi, scale, seed, init):
     assert np.array_equal(a.cpu().numpy().view(np.int64), e.cpu().numpy().view(np.int64))
 
 
+def test_csc_build_edge_cases(capi):
+    """K2's CSC build on degenerate handles: empty matrix, a single entry, all
+    rows dangling but one, a matrix uploaded from the host; K3 on each equals
+    the same call without the kept layout (and the oracle in parity mode)."""
+    cases = [
+        (4, [0, 0, 0, 0, 0], [], []),
+        (3, [0, 1, 1, 1], [2], [1.0]),
+        (5, [0, 0, 0, 3, 3, 3], [0, 1, 4], [0.25, 0.25, 0.5]),
+    ]
+    for n, ro, cols, vals in cases:
+        bare = capi.DeviceMatrix.from_host(n, ro, cols, vals)
+        kept = capi.DeviceMatrix.from_host(n, ro, cols, vals).build_csc()
+        assert kept.has_csc
+        a, na = capi.k3_pagerank(bare, seed=3)
+        b, nb = capi.k3_pagerank(kept, seed=3)
+        assert np.array_equal(a.cpu().numpy().view(np.int64), b.cpu().numpy().view(np.int64)) and na == nb
+        ref, nref = O.run_kernel3(np.asarray(ro, np.int64), np.asarray(cols, np.int64), np.asarray(vals, np.float64),
+                                  n, seed=3)
+        assert rel_l1(b.cpu().numpy(), ref) <= K3_TOL
+        rp, npar = capi.k3_pagerank(kept, seed=3, mode=1)
+        assert np.array_equal(rp.cpu().numpy().view(np.int64), ref.view(np.int64)) and npar == nref
+
+
 def test_init_rank_and_step(capi):
     g = golden("k1k2k3_s10_seed55.npz")
     n = 1 << 10

@@ -897,15 +897,16 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) spmv_sell_kernel(SellArg
             yv = __dadd_rn(__dmul_rn(a.damping, acc), bg);
             a.y[pos] = yv;
         } else if (len > 0) {
+            // Parts of a split column: publish the partial with a release
+            // increment (no __threadfence: its L1 invalidation cost the hot
+            // rows' L1 hits); the last part reads the partials from L2.
             a.partial[pos] = acc;
-            __threadfence();
             const uint32_t c = a.lane_col[pos];
-            const uint32_t old = atomicAdd(&a.arrive[c], 1u);
+            const uint32_t old = dev::atom_add_release_gpu(&a.arrive[c], 1u);
             if ((old + 1) % np == 0) {  // last part of this column: combine in part order
-                __threadfence();
                 double t = 0.0;
                 const uint32_t v0 = a.vc_base[c];
-                for (uint32_t p = 0; p < np; ++p) t = __dadd_rn(t, *((volatile double*)&a.partial[a.vpos[v0 + p]]));
+                for (uint32_t p = 0; p < np; ++p) t = __dadd_rn(t, __ldcg(&a.partial[a.vpos[v0 + p]]));
                 a.y[a.vpos[v0]] = __dadd_rn(__dmul_rn(a.damping, t), bg);
             }
         }

@@ -162,16 +162,6 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* smem, 
 
 // Streaming (evict-first) and keep (evict-last) global loads via L2 cache-policy
 // hints (sm_100 accepts the bare .L2::evict_* qualifiers only on 256-bit loads).
-// GPU-scope release increment: orders this thread's earlier stores before the
-// increment without the L1 invalidation (CCTL.IVALL) that __threadfence and
-// every acquire emit — a hot kernel's L1 working set survives (SASS: MEMBAR +
-// ATOMG only). Readers of the released data load with ld.cg (L2).
-__device__ __forceinline__ uint32_t atom_add_release_gpu(uint32_t* p, uint32_t v) {
-    uint32_t old;
-    asm volatile("atom.release.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
-    return old;
-}
-
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;
     asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));

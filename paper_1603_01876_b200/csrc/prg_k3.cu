@@ -45,8 +45,8 @@ struct K3Plan {
     uint32_t n_exc = 0;
     // timed mode (SELL)
     uint32_t V = 0, nslices = 0, n_empty = 0;
-    DevBuf<uint32_t> sell, slice_ptr, lane_len, lane_col, lane_np, vc_base, vpos, spos, spos_col, split_pos, n_split,
-        arrive, e_u;  // exception list: new row e_u[i], value exc_val[i]
+    DevBuf<uint32_t> sell, slice_ptr, lane_len, lane_col, lane_np, vc_base, vpos, spos, spos_col, split_col, n_split,
+        e_u;  // exception list: new row e_u[i], value exc_val[i]
     DevBuf<double> partial;
     // timed-mode gather: spos covers [rows | exceptions] (an exception's entry
     // is its row's), coef = [row base | exception value], both n_nd + n_exc
@@ -55,7 +55,7 @@ struct K3Plan {
     // buffers are released on the null stream (after a device sync).
     void rehome() {
         for (DevBuf<uint32_t>* b : {&pinv, &newid, &colptr, &csc_idx, &sell, &slice_ptr, &lane_len, &lane_col,
-                                    &lane_np, &vc_base, &vpos, &spos, &spos_col, &split_pos, &n_split, &arrive, &e_u})
+                                    &lane_np, &vc_base, &vpos, &spos, &spos_col, &split_col, &n_split, &e_u})
             b->s = nullptr;
         for (DevBuf<double>* b : {&bval, &exc_val, &partial, &coef}) b->s = nullptr;
     }
@@ -693,7 +693,7 @@ __global__ void split_flag_kernel(const uint32_t* __restrict__ vc_base, int64_t 
 __global__ void split_list_kernel(const uint32_t* __restrict__ vc_base, const uint32_t* __restrict__ vpos, int64_t n,
                                   const uint32_t* __restrict__ idx, uint32_t* __restrict__ list) {
     for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x)
-        if (vc_base[c + 1] - vc_base[c] > 1) list[idx[c]] = vpos[vc_base[c]];
+        if (vc_base[c + 1] - vc_base[c] > 1) list[idx[c]] = (uint32_t)c;
 }
 
 // s[j] = r(pinv[j]) * b[j]; r given in original order (first step) or as
@@ -772,19 +772,66 @@ __global__ void __launch_bounds__(1024, 2) gather_y_kernel(const double* __restr
 
 // Σ of the iterate, deterministic two-level tree: block b sums slice sums
 // [b*chunk, (b+1)*chunk) and split-column values likewise; one warp adds the
-// block partials (sell_sum_final).
-constexpr int kSumBlocks = 64;
-__global__ void sell_sum_part(const double* __restrict__ slice_sum, uint32_t nslices, const double* __restrict__ y,
-                              const uint32_t* __restrict__ split_pos, const uint32_t* __restrict__ n_split,
-                              double* __restrict__ part) {
+// block partials (sell_sum_final). Split columns (cut into parts of vcmax
+// entries) are finished here: the SpMV only stores each part's partial sum,
+// this kernel adds a column's parts in part order and writes its iterate —
+// no cross-CTA handshake (atomics, fences) inside the SpMV.
+constexpr int kSumBlocks = 296;
+struct SplitArgs {
+    const uint32_t* split_col;  // split columns, column order
+    const uint32_t* n_split;
+    const uint32_t* vc_base;    // column -> first virtual column
+    const uint32_t* vpos;       // virtual column -> SELL lane position
+    const double* partial;      // per lane: the part's sum
+    const double* bgp;          // [1] = bg of this step
+    double damping;
+};
+__global__ void sell_sum_part(const double* __restrict__ slice_sum, uint32_t nslices, double* __restrict__ y,
+                              SplitArgs sp, double* __restrict__ part) {
     __shared__ double ws[32];
-    const uint32_t ns = *n_split;
+    const uint32_t ns = *sp.n_split;
+    const double bg = sp.bgp[1];
     const uint32_t c1 = (nslices + gridDim.x - 1) / gridDim.x, c2 = (ns + gridDim.x - 1) / gridDim.x;
     double a = 0.0;
     for (uint32_t i = blockIdx.x * c1 + threadIdx.x; i < min(nslices, (blockIdx.x + 1) * c1); i += blockDim.x)
         a = __dadd_rn(a, slice_sum[i]);
-    for (uint32_t i = blockIdx.x * c2 + threadIdx.x; i < min(ns, (blockIdx.x + 1) * c2); i += blockDim.x)
-        a = __dadd_rn(a, y[split_pos[i]]);
+    // Split columns of <= kWarpParts parts: one thread each, parts in order
+    // (loads batched); longer ones: one warp each, lane l adds parts l, l+32,
+    // ... then a fixed shuffle tree. Both orders are fixed (deterministic).
+    constexpr uint32_t kWarpParts = 16;
+    const uint32_t i0 = blockIdx.x * c2, i1 = min(ns, (blockIdx.x + 1) * c2);
+    for (uint32_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+        const uint32_t c = sp.split_col[i];
+        const uint32_t v0 = sp.vc_base[c], np = sp.vc_base[c + 1] - v0;
+        if (np > kWarpParts) continue;
+        uint32_t q[kWarpParts];
+        double x[kWarpParts];
+#pragma unroll
+        for (uint32_t k = 0; k < kWarpParts; ++k) q[k] = k < np ? sp.vpos[v0 + k] : 0u;
+#pragma unroll
+        for (uint32_t k = 0; k < kWarpParts; ++k) x[k] = k < np ? sp.partial[q[k]] : 0.0;
+        double t = 0.0;
+#pragma unroll
+        for (uint32_t k = 0; k < kWarpParts; ++k)
+            if (k < np) t = __dadd_rn(t, x[k]);
+        const double yc = __dadd_rn(__dmul_rn(sp.damping, t), bg);
+        y[q[0]] = yc;
+        a = __dadd_rn(a, yc);
+    }
+    const unsigned lane = dev::lane_id(), nw = blockDim.x >> 5;
+    for (uint32_t i = i0 + dev::warp_id(); i < i1; i += nw) {
+        const uint32_t c = sp.split_col[i];
+        const uint32_t v0 = sp.vc_base[c], np = sp.vc_base[c + 1] - v0;
+        if (np <= kWarpParts) continue;
+        double t = 0.0;
+        for (uint32_t p = lane; p < np; p += 32) t = __dadd_rn(t, sp.partial[sp.vpos[v0 + p]]);
+        t = dev::warp_sum_f64(t);
+        const double yc = __dadd_rn(__dmul_rn(sp.damping, t), bg);
+        if (lane == 0) {
+            y[sp.vpos[v0]] = yc;
+            a = __dadd_rn(a, yc);
+        }
+    }
     a = dev::warp_sum_f64(a);
     if (dev::lane_id() == 0) ws[dev::warp_id()] = a;
     __syncthreads();
@@ -828,7 +875,6 @@ struct SellArgs {
     const double* s;             // gather vector [n_nd + n_exc]
     double* y;                   // [nslices*32]
     double* partial;             // [nslices*32]
-    uint32_t* arrive;            // [n] per split column, never reset
     double* slice_sum;           // [nslices]
     const double* bgp;           // [1] = bg of this step
     uint32_t* next_slice;        // work counters of this launch (32 words apart, start at 0)
@@ -897,18 +943,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) spmv_sell_kernel(SellArg
             yv = __dadd_rn(__dmul_rn(a.damping, acc), bg);
             a.y[pos] = yv;
         } else if (len > 0) {
-            // Parts of a split column: publish the partial with a release
-            // increment (no __threadfence: its L1 invalidation cost the hot
-            // rows' L1 hits); the last part reads the partials from L2.
+            // a part of a split column: its sum is finished by sell_sum_part
+            // (a cross-CTA handshake here, __threadfence + atomics, emitted
+            // CCTL.IVALL and cost the hot rows' L1 lines: 0.766 vs 0.737 ms
+            // even as release increments)
             a.partial[pos] = acc;
-            const uint32_t c = a.lane_col[pos];
-            const uint32_t old = dev::atom_add_release_gpu(&a.arrive[c], 1u);
-            if ((old + 1) % np == 0) {  // last part of this column: combine in part order
-                double t = 0.0;
-                const uint32_t v0 = a.vc_base[c];
-                for (uint32_t p = 0; p < np; ++p) t = __dadd_rn(t, __ldcg(&a.partial[a.vpos[v0 + p]]));
-                a.y[a.vpos[v0]] = __dadd_rn(__dmul_rn(a.damping, t), bg);
-            }
         }
         yv = dev::warp_sum_f64(yv);
         if (lane == 0) a.slice_sum[sl] = yv;
@@ -1126,7 +1165,7 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
         exc_spos_kernel<<<g, 1024, 0, s>>>(P.e_u.get(), P.n_exc, P.spos.get(), P.n_nd);
         PRG_LAUNCH_CHECK();
     }
-    P.split_pos = DevBuf<uint32_t>((size_t)n, s);
+    P.split_col = DevBuf<uint32_t>((size_t)n, s);
     P.n_split = DevBuf<uint32_t>(1, s);
     PRG_CUDA(cudaMemsetAsync(P.n_split.get(), 0, 4, s));
     if (n > 0) {
@@ -1134,11 +1173,9 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
         split_flag_kernel<<<g, 1024, 0, s>>>(P.vc_base.get(), n, flag.get());
         PRG_LAUNCH_CHECK();
         exclusive_scan_u32(flag.get(), idx.get(), (size_t)n, P.n_split.get(), s);
-        split_list_kernel<<<g, 1024, 0, s>>>(P.vc_base.get(), P.vpos.get(), n, idx.get(), P.split_pos.get());
+        split_list_kernel<<<g, 1024, 0, s>>>(P.vc_base.get(), P.vpos.get(), n, idx.get(), P.split_col.get());
         PRG_LAUNCH_CHECK();
     }
-    P.arrive = DevBuf<uint32_t>((size_t)n, s);
-    PRG_CUDA(cudaMemsetAsync(P.arrive.get(), 0, (size_t)n * 4, s));
     P.partial = DevBuf<double>(NP ? NP : 1, s);
     // empty columns = columns with no virtual column
     uint32_t nonempty = 0;
@@ -1282,7 +1319,6 @@ void iterate(const K3Plan& P, const double* r_in, double* r_out, int iters, doub
         a.s = sbuf.get();
         a.y = y;
         a.partial = P.partial.get();
-        a.arrive = P.arrive.get();
         a.slice_sum = slice_sum.get();
         a.bgp = S.out.get();
         a.next_slice = slice_ctr.get() + (size_t)it * 32 * nctr;
@@ -1300,8 +1336,9 @@ void iterate(const K3Plan& P, const double* r_in, double* r_out, int iters, doub
             else spmv_sell_kernel<6, 768, 2><<<num_sms() * 2, 768, 0, s>>>(a);
             PRG_LAUNCH_CHECK();
         }
-        sell_sum_part<<<kSumBlocks, 1024, 0, s>>>(slice_sum.get(), P.nslices, y, P.split_pos.get(), P.n_split.get(),
-                                                  sum_part.get());
+        SplitArgs sp{P.split_col.get(), P.n_split.get(), P.vc_base.get(), P.vpos.get(), P.partial.get(), S.out.get(),
+                     damping};
+        sell_sum_part<<<kSumBlocks, 1024, 0, s>>>(slice_sum.get(), P.nslices, y, sp, sum_part.get());
         sell_sum_final<<<1, 32, 0, s>>>(sum_part.get(), kSumBlocks, (double)P.n_empty, bgf, S.out.get());
         PRG_LAUNCH_CHECK();
     }

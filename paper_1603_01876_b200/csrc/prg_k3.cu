@@ -1098,8 +1098,9 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
     // Part length: short enough that the longest lane chain (one sequential
     // gather stream) stays well under the whole SpMV on small graphs.
     // Measured on B200 (SpMV ms): S=24 512: 0.797, 384/768: 0.82, 2048: 0.834;
-    // S=20 128-256: 0.085; S=16 64: 0.027 vs 2048: 0.159; S=26 1024: 3.51 vs 512: 3.63.
-    uint32_t vcmax = nnz >= (1ull << 29) ? 1024u : nnz >= (1ull << 27) ? 512u : nnz >= (1ull << 23) ? 256u : nnz >= (1ull << 20) ? 128u : 64u;
+    // S=20 128-256: 0.085; S=16 64: 0.027 vs 2048: 0.159; S=26 (handshake-free SpMV) 512: 3.26 vs
+    // 1024: 3.32 vs 2048: 3.34 (with the split handshake in the SpMV, 1024 had won: 3.51 vs 3.63).
+    uint32_t vcmax = nnz >= (1ull << 27) ? 512u : nnz >= (1ull << 23) ? 256u : nnz >= (1ull << 20) ? 128u : 64u;
     {
         static int env = -1;
         if (env < 0) { const char* e = getenv("PRG_VCMAX"); env = e ? atoi(e) : 0; }

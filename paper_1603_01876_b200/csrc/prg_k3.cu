@@ -344,6 +344,8 @@ struct CscDst {
 };
 
 // colptr[c] = min(colptr[c], colptr[c+1], ...) — fills empty columns.
+// In place, inclusive; the block minima are themselves suffix-minimised
+// recursively (a one-thread loop over them took ~50 us at S=24).
 __global__ void suffix_min_block(uint32_t* a, int64_t n1, uint32_t* part) {
     // each block: 1024 threads x 8 items, reverse order
     __shared__ uint32_t wm[32];
@@ -362,17 +364,8 @@ __global__ void suffix_min_block(uint32_t* a, int64_t n1, uint32_t* part) {
         if (threadIdx.x == 0) part[blockIdx.x] = x;
     }
 }
-__global__ void suffix_min_parts(uint32_t* part, int64_t nb) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
-        uint32_t run = 0xffffffffu;
-        for (int64_t b = nb - 1; b >= 0; --b) {
-            const uint32_t x = part[b];
-            part[b] = run;  // exclusive suffix min (blocks after b)
-            run = min(run, x);
-        }
-    }
-}
-__global__ void suffix_min_down(uint32_t* a, int64_t n1, const uint32_t* part) {
+// blk_suffix: inclusive suffix minima of the block minima (null: a single block)
+__global__ void suffix_min_down(uint32_t* a, int64_t n1, const uint32_t* blk_suffix, int64_t nb) {
     __shared__ uint32_t wm[33];
     const int64_t base = (int64_t)blockIdx.x * 8192;
     uint32_t v[8];
@@ -401,7 +394,7 @@ __global__ void suffix_min_down(uint32_t* a, int64_t n1, const uint32_t* part) {
         wm[threadIdx.x] = x;  // inclusive suffix over warps
     }
     __syncthreads();
-    uint32_t run = part[blockIdx.x];
+    uint32_t run = (blk_suffix && blockIdx.x + 1 < nb) ? blk_suffix[blockIdx.x + 1] : 0xffffffffu;
     if (dev::warp_id() + 1 < 32) run = min(run, wm[dev::warp_id() + 1]);
     uint32_t after = __shfl_down_sync(0xffffffffu, inc, 1);
     if (dev::lane_id() < 31) run = min(run, after);
@@ -966,6 +959,21 @@ __global__ void count_set_kernel(const uint32_t* __restrict__ a, int64_t n, uint
 // ---------------------------------------------------------------------------
 // Plan
 // ---------------------------------------------------------------------------
+void suffix_min_inplace(uint32_t* a, int64_t n1, cudaStream_t s) {
+    const int64_t nb = (n1 + 8191) / 8192;
+    if (nb <= 1) {
+        suffix_min_down<<<1, 1024, 0, s>>>(a, n1, nullptr, 1);
+        PRG_LAUNCH_CHECK();
+        return;
+    }
+    DevBuf<uint32_t> part((size_t)nb, s);
+    suffix_min_block<<<(unsigned)nb, 1024, 0, s>>>(a, n1, part.get());
+    PRG_LAUNCH_CHECK();
+    suffix_min_inplace(part.get(), nb, s);
+    suffix_min_down<<<(unsigned)nb, 1024, 0, s>>>(a, n1, part.get(), nb);
+    PRG_LAUNCH_CHECK();
+}
+
 void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
     ProfScope prof("k3_prep", s);
     const int64_t n = A->n;
@@ -1076,13 +1084,7 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
         // colptr[n] = nnz, then fill empty columns with the next column start.
         const uint32_t nz = (uint32_t)nnz;
         PRG_CUDA(cudaMemcpyAsync(P.colptr.get() + n, &nz, 4, cudaMemcpyHostToDevice, s));
-        const int64_t n1 = n + 1;
-        const int64_t nb = (n1 + 8191) / 8192;
-        DevBuf<uint32_t> part((size_t)nb, s);
-        suffix_min_block<<<(unsigned)nb, 1024, 0, s>>>(P.colptr.get(), n1, part.get());
-        suffix_min_parts<<<1, 1, 0, s>>>(part.get(), nb);
-        suffix_min_down<<<(unsigned)nb, 1024, 0, s>>>(P.colptr.get(), n1, part.get());
-        PRG_LAUNCH_CHECK();
+        suffix_min_inplace(P.colptr.get(), n + 1, s);
     }
     PRG_CUDA(cudaMemcpyAsync(&P.n_exc, n_exc.get(), 4, cudaMemcpyDeviceToHost, s));
     PRG_CUDA(cudaStreamSynchronize(s));

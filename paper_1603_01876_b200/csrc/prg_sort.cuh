@@ -329,6 +329,70 @@ struct LocalSmem {
     uint32_t scan_tmp[kLocalWarps + 1];
 };
 
+// The 32-bit variant of the pass loop below (same ranking): keys are the
+// window (key >> lo) of span hi-lo+1 <= 32 bits; `common` holds every bit
+// outside the window. On return S.X[xpad(i)] holds the sorted full keys.
+static __device__ __forceinline__ void cta_lsd_sort32(LocalSmem& S, uint32_t n, const uint64_t (&kin)[kLocalItems],
+                                                      int lo, int hi, uint64_t common) {
+    const unsigned tid = threadIdx.x;
+    const uint32_t half = (tid & 1u) * 16u;
+    uint32_t* X32 = reinterpret_cast<uint32_t*>(S.X);  // xpad-indexed, 4-byte slots
+    uint32_t k[kLocalItems];
+#pragma unroll
+    for (int j = 0; j < kLocalItems; ++j) k[j] = (uint32_t)(kin[j] >> lo);  // slots past n: all ones
+    constexpr int WPT = kCntWords / kLocalThreads;
+    uint32_t* const my = &S.cnt[tid * (WPT + 1)];
+    const uint32_t pp = (tid >> 1) + (tid >> 5);
+    const int span = hi - lo + 1;
+    for (int sh = 0; sh < span; sh += kLsdBits) {
+#pragma unroll
+        for (int q = 0; q < WPT; ++q) my[q] = 0;
+        __syncthreads();
+        uint32_t rk[kLocalItems / 2];
+#pragma unroll
+        for (int j = 0; j < kLocalItems; ++j) {
+            const uint32_t d = (k[j] >> sh) & (kLsdDigits - 1);
+            const uint32_t old = atomicAdd(&S.cnt[d * 272u + pp], 1u << half);
+            const uint32_t r = (old >> half) & 0xffffu;
+            if (j & 1) rk[j >> 1] |= r << 16; else rk[j >> 1] = r;
+        }
+        __syncthreads();
+        {
+            uint32_t ts = 0;
+#pragma unroll 4
+            for (int q = 0; q < WPT; ++q) {
+                const uint32_t wv = my[q];
+                ts += (wv & 0xffffu) + (wv >> 16);
+            }
+            uint32_t tot;
+            uint32_t run = dev::block_excl_scan(ts, S.scan_tmp, tot);
+#pragma unroll 4
+            for (int q = 0; q < WPT; ++q) {
+                const uint32_t wv = my[q];
+                const uint32_t lo16 = wv & 0xffffu;
+                my[q] = run | ((run + lo16) << 16);
+                run += lo16 + (wv >> 16);
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < kLocalItems; ++j) {
+            const uint32_t d = (k[j] >> sh) & (kLsdDigits - 1);
+            const uint32_t pre = (S.cnt[d * 272u + pp] >> half) & 0xffffu;
+            const uint32_t r = (rk[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
+            X32[xpad(pre + r)] = k[j];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < kLocalItems; ++j) k[j] = X32[tid * (kLocalItems + 1) + j];  // X32[xpad(tid*16+j)]
+        __syncthreads();
+    }
+    // rebuild the full keys (slots past n sort last and are never stored)
+#pragma unroll
+    for (int j = 0; j < kLocalItems; ++j) S.X[tid * (kLocalItems + 1) + j] = common | ((uint64_t)k[j] << lo);
+    __syncthreads();
+}
+
 // Sorts X[0, n) (n <= kLocalCap; X indexed through xpad). All threads call.
 static __device__ __forceinline__ void cta_lsd_sort(LocalSmem& S, uint32_t n, int payload_bits) {
     const unsigned tid = threadIdx.x, lane = dev::lane_id(), w = dev::warp_id();
@@ -355,6 +419,13 @@ static __device__ __forceinline__ void cta_lsd_sort(LocalSmem& S, uint32_t n, in
     if (diff == 0) { __syncthreads(); return; }  // equal above the payload: sorted
     const int lo = __ffsll((long long)diff) - 1;
     const int hi = 63 - __clzll((long long)diff);
+    if (payload_bits == 0 && hi - lo < 32) {
+        // Every bit outside [lo, hi] is common to the segment: sort the 32-bit
+        // window and rebuild the keys (K1 after two MSD levels: 32 varying bits
+        // of (u, v)). Half the shared-memory bytes per scatter and reload.
+        cta_lsd_sort32(S, n, k, lo, hi, a & ~(((hi - lo == 31) ? ~0ull >> 32 : ((1ull << (hi - lo + 1)) - 1)) << lo));
+        return;
+    }
     constexpr int WPT = kCntWords / kLocalThreads;  // counter words per thread (16)
     static_assert(WPT == 16, "xpad(tid*16 + q) == tid*17 + q relies on 16 words per thread");
     uint32_t* const my = &S.cnt[tid * (WPT + 1)];   // this thread's 16 scan words, contiguous after padding

@@ -251,35 +251,11 @@ __global__ void __launch_bounds__(kT) k2_pass_b(
     uint32_t tile_kh;
     const uint32_t kh_excl = dev::block_excl_scan(nkh, S.scan_u, tile_kh);
 
-    // Decoupled look-back for the tile's global kept-entry base, by warp 0:
-    // 32 predecessors are inspected at once (sum of aggregates up to the
-    // nearest inclusive prefix).
-    if (tid < 32) {
-        uint64_t excl = 0;
-        if (t == 0) {
-            if (tid == 0) atomicExch(&tile_status[0], kFlagInc | tile_kh);
-        } else {
-            if (tid == 0) atomicExch(&tile_status[t], kFlagAgg | tile_kh);
-            for (int64_t k = (int64_t)t - 1;; k -= 32) {
-                const int64_t idx = k - (int64_t)tid;
-                uint64_t st = kFlagInc;  // below tile 0: an empty inclusive prefix
-                if (idx >= 0) {
-                    do {
-                        st = *((volatile unsigned long long*)&tile_status[idx]);
-                    } while ((st & ~kValMask) == 0);
-                }
-                const unsigned incm = __ballot_sync(0xffffffffu, (st & ~kValMask) == kFlagInc);
-                const int first = incm ? __ffs(incm) - 1 : 32;
-                uint64_t v = (int)tid <= first ? (st & kValMask) : 0ull;
-#pragma unroll
-                for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
-                excl += v;
-                if (incm) break;
-            }
-            if (tid == 0) atomicExch(&tile_status[t], kFlagInc | (excl + tile_kh));
-        }
-        if (tid == 0) S.tile_base = excl;
-    }
+    // The tile's aggregate is published now; the look-back runs after the row
+    // sums (below), when the predecessors have mostly published inclusive
+    // prefixes: ncu had 17% of pass B's stall samples at the barrier waiting
+    // for warp 0's look-back.
+    if (tid == 0) atomicExch(&tile_status[t], (t == 0 ? kFlagInc : kFlagAgg) | tile_kh);
 
     // Row sums (kept edges) and run lengths (all edges) into SMEM per head.
     {
@@ -305,6 +281,32 @@ __global__ void __launch_bounds__(kT) k2_pass_b(
         }
         if (acc_row) { if (rh >= 0) atomicAdd(&S.rr[sp(rh)], acc_row << 16); else atomicAdd(&S.first_row_part, acc_row); }
         if (acc_run) { if (rn >= 0) atomicAdd(&S.rr[sp(rn)], acc_run); else atomicAdd(&S.first_run_part, acc_run); }
+    }
+    // Decoupled look-back for the tile's global kept-entry base, by warp 0:
+    // 32 predecessors are inspected at once (sum of aggregates up to the
+    // nearest inclusive prefix).
+    if (tid < 32) {
+        uint64_t excl = 0;
+        if (t != 0) {
+            for (int64_t k = (int64_t)t - 1;; k -= 32) {
+                const int64_t idx = k - (int64_t)tid;
+                uint64_t st = kFlagInc;  // below tile 0: an empty inclusive prefix
+                if (idx >= 0) {
+                    do {
+                        st = *((volatile unsigned long long*)&tile_status[idx]);
+                    } while ((st & ~kValMask) == 0);
+                }
+                const unsigned incm = __ballot_sync(0xffffffffu, (st & ~kValMask) == kFlagInc);
+                const int first = incm ? __ffs(incm) - 1 : 32;
+                uint64_t v = (int)tid <= first ? (st & kValMask) : 0ull;
+#pragma unroll
+                for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+                excl += v;
+                if (incm) break;
+            }
+            if (tid == 0) atomicExch(&tile_status[t], kFlagInc | (excl + tile_kh));
+        }
+        if (tid == 0) S.tile_base = excl;
     }
     __syncthreads();
     const uint64_t tile_base = S.tile_base;

@@ -623,6 +623,7 @@ struct FillArgs {
     uint32_t* lane_col;  // [nslices*32]
     uint32_t* lane_np;   // [nslices*32]
     uint32_t* spos_col;  // [n] pos of part 0 (kEmpty if empty)
+    uint32_t* next;      // slice claim counter (zero on entry)
 };
 
 // One warp per slice, lane = virtual column. Exception entries (value != row
@@ -630,7 +631,13 @@ struct FillArgs {
 // exception products are stored every iteration — the SpMV has no special case.
 __global__ void sell_fill_kernel(FillArgs a) {
     const uint32_t lane = dev::lane_id();
-    for (uint32_t s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < a.nslices; s += (gridDim.x * blockDim.x) >> 5) {
+    // slices claimed dynamically (they are sorted longest first: a static
+    // stride gave the low warps every round's longest slice)
+    for (;;) {
+        uint32_t s = 0;
+        if (lane == 0) s = atomicAdd(a.next, 1u);
+        s = __shfl_sync(0xffffffffu, s, 0);
+        if (s >= a.nslices) break;
         const uint32_t pos = s * 32 + lane;
         uint32_t len = 0, c = 0, np = 1, start = 0;
         if (pos < a.V) {
@@ -1154,7 +1161,10 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
         FillArgs fa{order.get(),         vc_col.get(),     vc_len.get(), P.vc_base.get(),   P.colptr.get(),
                     P.csc_idx.get(),     P.slice_ptr.get(), V,                P.nslices,
                     (uint32_t)P.n_nd,    vcmax,            P.sell.get(),     P.lane_len.get(),  P.lane_col.get(),
-                    P.lane_np.get(),     P.spos_col.get()};
+                    P.lane_np.get(),     P.spos_col.get(),     nullptr};
+        DevBuf<uint32_t> fill_ctr(1, s);
+        PRG_CUDA(cudaMemsetAsync(fill_ctr.get(), 0, 4, s));
+        fa.next = fill_ctr.get();
         sell_fill_kernel<<<g, 256, 0, s>>>(fa);
         PRG_LAUNCH_CHECK();
     }

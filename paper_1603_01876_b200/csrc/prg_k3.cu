@@ -46,6 +46,7 @@ struct K3Plan {
     // timed mode (SELL)
     uint32_t V = 0, nslices = 0, n_empty = 0;
     DevBuf<uint32_t> sell, slice_ptr, lane_len, lane_col, lane_np, vc_base, vpos, spos, spos_col, split_col, n_split,
+        split_p0, split_pbase, lane_pslot,
         e_u;  // exception list: new row e_u[i], value exc_val[i]
     DevBuf<double> partial;
     // timed-mode gather: spos covers [rows | exceptions] (an exception's entry
@@ -55,7 +56,7 @@ struct K3Plan {
     // buffers are released on the null stream (after a device sync).
     void rehome() {
         for (DevBuf<uint32_t>* b : {&pinv, &newid, &colptr, &csc_idx, &sell, &slice_ptr, &lane_len, &lane_col,
-                                    &lane_np, &vc_base, &vpos, &spos, &spos_col, &split_col, &n_split, &e_u})
+                                    &lane_np, &vc_base, &vpos, &spos, &spos_col, &split_col, &n_split, &split_p0, &split_pbase, &lane_pslot, &e_u})
             b->s = nullptr;
         for (DevBuf<double>* b : {&bval, &exc_val, &partial, &coef}) b->s = nullptr;
     }
@@ -696,6 +697,26 @@ __global__ void split_list_kernel(const uint32_t* __restrict__ vc_base, const ui
         if (vc_base[c + 1] - vc_base[c] > 1) list[idx[c]] = (uint32_t)c;
 }
 
+__global__ void split_np_kernel(const uint32_t* __restrict__ split_col, const uint32_t* __restrict__ n_split,
+                                const uint32_t* __restrict__ vc_base, uint32_t* __restrict__ np_of) {
+    const uint32_t ns = *n_split;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < ns; i += gridDim.x * blockDim.x) {
+        const uint32_t c = split_col[i];
+        np_of[i] = vc_base[c + 1] - vc_base[c];
+    }
+}
+__global__ void split_slots_kernel(const uint32_t* __restrict__ split_col, const uint32_t* __restrict__ n_split,
+                                   const uint32_t* __restrict__ vc_base, const uint32_t* __restrict__ vpos,
+                                   const uint32_t* __restrict__ pbase, uint32_t* __restrict__ p0,
+                                   uint32_t* __restrict__ lane_pslot) {
+    const uint32_t ns = *n_split;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < ns; i += gridDim.x * blockDim.x) {
+        const uint32_t c = split_col[i], v0 = vc_base[c], np = vc_base[c + 1] - v0, b = pbase[i];
+        p0[i] = vpos[v0];
+        for (uint32_t p = 0; p < np; ++p) lane_pslot[vpos[v0 + p]] = b + p;
+    }
+}
+
 // s[j] = r(pinv[j]) * b[j]; r given in original order (first step) or as
 // (y in SELL order, bg for empty columns) (later steps).
 __global__ void permute_orig_kernel(const double* __restrict__ r, const uint32_t* __restrict__ pinv,
@@ -778,12 +799,11 @@ __global__ void __launch_bounds__(1024, 2) gather_y_kernel(const double* __restr
 // no cross-CTA handshake (atomics, fences) inside the SpMV.
 constexpr int kSumBlocks = 296;
 struct SplitArgs {
-    const uint32_t* split_col;  // split columns, column order
     const uint32_t* n_split;
-    const uint32_t* vc_base;    // column -> first virtual column
-    const uint32_t* vpos;       // virtual column -> SELL lane position
-    const double* partial;      // per lane: the part's sum
-    const double* bgp;          // [1] = bg of this step
+    const uint32_t* split_p0;    // split column i: SELL position of its part 0 (its iterate)
+    const uint32_t* split_pbase; // [n_split + 1]: its parts' sums at partial[pbase[i] .. pbase[i+1])
+    const double* partial;       // compact part sums, column by column in part order
+    const double* bgp;           // [1] = bg of this step
     double damping;
 };
 __global__ void sell_sum_part(const double* __restrict__ slice_sum, uint32_t nslices, double* __restrict__ y,
@@ -795,40 +815,38 @@ __global__ void sell_sum_part(const double* __restrict__ slice_sum, uint32_t nsl
     double a = 0.0;
     for (uint32_t i = blockIdx.x * c1 + threadIdx.x; i < min(nslices, (blockIdx.x + 1) * c1); i += blockDim.x)
         a = __dadd_rn(a, slice_sum[i]);
-    // Split columns of <= kWarpParts parts: one thread each, parts in order
-    // (loads batched); longer ones: one warp each, lane l adds parts l, l+32,
-    // ... then a fixed shuffle tree. Both orders are fixed (deterministic).
+    // Split columns of <= kWarpParts parts: one thread each, parts in order;
+    // longer ones: one warp each, lane l adds parts l, l+32, ... then a fixed
+    // shuffle tree. Both orders are fixed (deterministic). A column's part sums
+    // are contiguous (the SpMV writes them to their compact slots), so this is
+    // one dependent load level, not three (split list -> virtual columns ->
+    // lane positions -> sums).
     constexpr uint32_t kWarpParts = 16;
     const uint32_t i0 = blockIdx.x * c2, i1 = min(ns, (blockIdx.x + 1) * c2);
     for (uint32_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
-        const uint32_t c = sp.split_col[i];
-        const uint32_t v0 = sp.vc_base[c], np = sp.vc_base[c + 1] - v0;
+        const uint32_t pb = sp.split_pbase[i], np = sp.split_pbase[i + 1] - pb;
         if (np > kWarpParts) continue;
-        uint32_t q[kWarpParts];
         double x[kWarpParts];
 #pragma unroll
-        for (uint32_t k = 0; k < kWarpParts; ++k) q[k] = k < np ? sp.vpos[v0 + k] : 0u;
-#pragma unroll
-        for (uint32_t k = 0; k < kWarpParts; ++k) x[k] = k < np ? sp.partial[q[k]] : 0.0;
+        for (uint32_t k = 0; k < kWarpParts; ++k) x[k] = k < np ? sp.partial[pb + k] : 0.0;
         double t = 0.0;
 #pragma unroll
         for (uint32_t k = 0; k < kWarpParts; ++k)
             if (k < np) t = __dadd_rn(t, x[k]);
         const double yc = __dadd_rn(__dmul_rn(sp.damping, t), bg);
-        y[q[0]] = yc;
+        y[sp.split_p0[i]] = yc;
         a = __dadd_rn(a, yc);
     }
     const unsigned lane = dev::lane_id(), nw = blockDim.x >> 5;
     for (uint32_t i = i0 + dev::warp_id(); i < i1; i += nw) {
-        const uint32_t c = sp.split_col[i];
-        const uint32_t v0 = sp.vc_base[c], np = sp.vc_base[c + 1] - v0;
+        const uint32_t pb = sp.split_pbase[i], np = sp.split_pbase[i + 1] - pb;
         if (np <= kWarpParts) continue;
         double t = 0.0;
-        for (uint32_t p = lane; p < np; p += 32) t = __dadd_rn(t, sp.partial[sp.vpos[v0 + p]]);
+        for (uint32_t p = lane; p < np; p += 32) t = __dadd_rn(t, sp.partial[pb + p]);
         t = dev::warp_sum_f64(t);
         const double yc = __dadd_rn(__dmul_rn(sp.damping, t), bg);
         if (lane == 0) {
-            y[sp.vpos[v0]] = yc;
+            y[sp.split_p0[i]] = yc;
             a = __dadd_rn(a, yc);
         }
     }
@@ -874,7 +892,8 @@ struct SellArgs {
     const uint32_t* vpos;
     const double* s;             // gather vector [n_nd + n_exc]
     double* y;                   // [nslices*32]
-    double* partial;             // [nslices*32]
+    double* partial;             // compact part sums of split columns
+    const uint32_t* lane_pslot;  // lane -> its slot in partial (parts of split columns)
     double* slice_sum;           // [nslices]
     const double* bgp;           // [1] = bg of this step
     uint32_t* next_slice;        // work counters of this launch (32 words apart, start at 0)
@@ -947,7 +966,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) spmv_sell_kernel(SellArg
             // (a cross-CTA handshake here, __threadfence + atomics, emitted
             // CCTL.IVALL and cost the hot rows' L1 lines: 0.766 vs 0.737 ms
             // even as release increments)
-            a.partial[pos] = acc;
+            a.partial[a.lane_pslot[pos]] = acc;
         }
         yv = dev::warp_sum_f64(yv);
         if (lane == 0) a.slice_sum[sl] = yv;
@@ -1191,7 +1210,33 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
         split_list_kernel<<<g, 1024, 0, s>>>(P.vc_base.get(), P.vpos.get(), n, idx.get(), P.split_col.get());
         PRG_LAUNCH_CHECK();
     }
-    P.partial = DevBuf<double>(NP ? NP : 1, s);
+    // compact part sums: split column i's parts at [pbase[i], pbase[i+1]); the
+    // SpMV lane of part p writes slot pbase[i] + p (lane_pslot)
+    P.split_p0 = DevBuf<uint32_t>((size_t)n, s);
+    P.split_pbase = DevBuf<uint32_t>((size_t)n + 1, s);
+    P.lane_pslot = DevBuf<uint32_t>(NP ? NP : 1, s);
+    uint32_t n_parts = 0;
+    if (n > 0) {
+        DevBuf<uint32_t> np_of((size_t)n, s);
+        split_np_kernel<<<g, 1024, 0, s>>>(P.split_col.get(), P.n_split.get(), P.vc_base.get(), np_of.get());
+        PRG_LAUNCH_CHECK();
+        exclusive_scan_u32_prefix(np_of.get(), P.split_pbase.get(), (size_t)n, P.n_split.get(), 1, s);
+        split_slots_kernel<<<g, 256, 0, s>>>(P.split_col.get(), P.n_split.get(), P.vc_base.get(), P.vpos.get(),
+                                             P.split_pbase.get(), P.split_p0.get(), P.lane_pslot.get());
+        PRG_LAUNCH_CHECK();
+        uint32_t ns_h = 0;
+        PRG_CUDA(cudaMemcpyAsync(&ns_h, P.n_split.get(), 4, cudaMemcpyDeviceToHost, s));
+        PRG_CUDA(cudaStreamSynchronize(s));
+        if (ns_h) {
+            uint32_t last[2] = {0, 0};
+            PRG_CUDA(cudaMemcpyAsync(last, P.split_pbase.get() + ns_h - 1, 4, cudaMemcpyDeviceToHost, s));
+            PRG_CUDA(cudaMemcpyAsync(last + 1, np_of.get() + ns_h - 1, 4, cudaMemcpyDeviceToHost, s));
+            PRG_CUDA(cudaStreamSynchronize(s));
+            n_parts = last[0] + last[1];
+            PRG_CUDA(cudaMemcpyAsync(P.split_pbase.get() + ns_h, &n_parts, 4, cudaMemcpyHostToDevice, s));
+        }
+    }
+    P.partial = DevBuf<double>(n_parts ? n_parts : 1, s);
     // empty columns = columns with no virtual column
     uint32_t nonempty = 0;
     {
@@ -1334,6 +1379,7 @@ void iterate(const K3Plan& P, const double* r_in, double* r_out, int iters, doub
         a.s = sbuf.get();
         a.y = y;
         a.partial = P.partial.get();
+        a.lane_pslot = P.lane_pslot.get();
         a.slice_sum = slice_sum.get();
         a.bgp = S.out.get();
         a.next_slice = slice_ctr.get() + (size_t)it * 32 * nctr;
@@ -1351,8 +1397,7 @@ void iterate(const K3Plan& P, const double* r_in, double* r_out, int iters, doub
             else spmv_sell_kernel<6, 768, 2><<<num_sms() * 2, 768, 0, s>>>(a);
             PRG_LAUNCH_CHECK();
         }
-        SplitArgs sp{P.split_col.get(), P.n_split.get(), P.vc_base.get(), P.vpos.get(), P.partial.get(), S.out.get(),
-                     damping};
+        SplitArgs sp{P.n_split.get(), P.split_p0.get(), P.split_pbase.get(), P.partial.get(), S.out.get(), damping};
         sell_sum_part<<<kSumBlocks, 1024, 0, s>>>(slice_sum.get(), P.nslices, y, sp, sum_part.get());
         sell_sum_final<<<1, 32, 0, s>>>(sum_part.get(), kSumBlocks, (double)P.n_empty, bgf, S.out.get());
         PRG_LAUNCH_CHECK();

@@ -766,12 +766,34 @@ __global__ void gather_s_kernel(GatherArgs a) {
 // The same for steps >= 2, uniform over [rows | exceptions]: s[j] =
 // r(spos[j]) * coef[j] — coalesced spos/coef/s streams and one random read of
 // the previous iterate per entry, G entries in flight per thread.
+// One extra block (the last) finishes the previous step's Σ instead (what
+// sell_sum_final does, same order): out_next = {Σ, bgf * Σ, bg_prev}, one
+// launch fewer per step.
+struct SumFinish {
+    const double* part;  // sell_sum_part's block partials
+    int np;
+    double n_empty, bgf;
+    double* out_next;
+};
 template <int G>
 __global__ void __launch_bounds__(1024, 2) gather_y_kernel(const double* __restrict__ y, const uint32_t* __restrict__ spos,
                                                            const double* __restrict__ coef, const double* __restrict__ bgp,
-                                                           int64_t tot, double* __restrict__ s) {
-    const double bg = bgp[2];
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+                                                           int64_t tot, double* __restrict__ s, SumFinish fin) {
+    const double bg = bgp[1];  // the bg the previous step used (its empty columns' value)
+    if (blockIdx.x == gridDim.x - 1) {
+        if (threadIdx.x >= 32) return;
+        double v = 0.0;
+        for (int i = threadIdx.x; i < fin.np; i += 32) v = __dadd_rn(v, fin.part[i]);
+        v = dev::warp_sum_f64(v);
+        if (threadIdx.x == 0) {
+            const double t = __dadd_rn(v, __dmul_rn(fin.n_empty, bg));
+            fin.out_next[0] = t;
+            fin.out_next[1] = __dmul_rn(fin.bgf, t);
+            fin.out_next[2] = bg;
+        }
+        return;
+    }
+    const int64_t stride = (int64_t)(gridDim.x - 1) * blockDim.x;
     for (int64_t j0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j0 < tot; j0 += G * stride) {
         uint32_t p[G];
         double c[G], r[G];
@@ -1348,6 +1370,12 @@ void iterate(const K3Plan& P, const double* r_in, double* r_out, int iters, doub
     DevBuf<uint32_t> slice_ctr(ctr_words, s);
     PRG_CUDA(cudaMemsetAsync(slice_ctr.get(), 0, ctr_words * 4, s));
     double* ys[2] = {y0.get(), y1.get()};
+    // Scalars {Σ, bg, bg of the step before} of step k's input iterate: step 0
+    // reads S.out; step k >= 1 reads a slot written by the gather launch that
+    // starts it (block 0 finishes step k-1's Σ), alternating so a launch never
+    // overwrites the slot it reads.
+    DevBuf<double> outs(8, s);
+    auto out_of = [&](int k) { return k == 0 ? S.out.get() : outs.get() + 4 * (k & 1); };
     for (int it = 0; it < iters; ++it) {
         double* y = ys[it & 1];
         const double* yp = ys[(it & 1) ^ 1];
@@ -1359,12 +1387,15 @@ void iterate(const K3Plan& P, const double* r_in, double* r_out, int iters, doub
             const int64_t tot = P.n_nd + P.n_exc;
             static int gi = -1;  // PRG_GATHER_ITEMS (1, 2, 4)
             if (gi < 0) { const char* e = getenv("PRG_GATHER_ITEMS"); gi = e ? atoi(e) : 4; }
-            if (tot && it == 0) gather_s_kernel<<<g, 1024, 0, s>>>(ga);
-            else if (tot) {
-                const unsigned gg = (unsigned)std::max<int64_t>(1, std::min<int64_t>(g, (tot + 1023) / 1024 / gi));
-                if (gi == 4) gather_y_kernel<4><<<gg, 1024, 0, s>>>(yp, P.spos.get(), P.coef.get(), S.out.get(), tot, sbuf.get());
-                else if (gi == 1) gather_y_kernel<1><<<gg, 1024, 0, s>>>(yp, P.spos.get(), P.coef.get(), S.out.get(), tot, sbuf.get());
-                else gather_y_kernel<2><<<gg, 1024, 0, s>>>(yp, P.spos.get(), P.coef.get(), S.out.get(), tot, sbuf.get());
+            if (it == 0) {
+                if (tot) gather_s_kernel<<<g, 1024, 0, s>>>(ga);
+            } else {  // launched even with tot == 0: block 0 finishes the previous Σ
+                const unsigned gg = 1 + (unsigned)std::max<int64_t>(1, std::min<int64_t>(g - 1, (tot + 1023) / 1024 / gi));
+                const SumFinish fin{sum_part.get(), kSumBlocks, (double)P.n_empty, bgf, out_of(it)};
+                const double* bgp = out_of(it - 1);
+                if (gi == 4) gather_y_kernel<4><<<gg, 1024, 0, s>>>(yp, P.spos.get(), P.coef.get(), bgp, tot, sbuf.get(), fin);
+                else if (gi == 1) gather_y_kernel<1><<<gg, 1024, 0, s>>>(yp, P.spos.get(), P.coef.get(), bgp, tot, sbuf.get(), fin);
+                else gather_y_kernel<2><<<gg, 1024, 0, s>>>(yp, P.spos.get(), P.coef.get(), bgp, tot, sbuf.get(), fin);
             }
             PRG_LAUNCH_CHECK();
         }
@@ -1381,7 +1412,7 @@ void iterate(const K3Plan& P, const double* r_in, double* r_out, int iters, doub
         a.partial = P.partial.get();
         a.lane_pslot = P.lane_pslot.get();
         a.slice_sum = slice_sum.get();
-        a.bgp = S.out.get();
+        a.bgp = out_of(it);
         a.next_slice = slice_ctr.get() + (size_t)it * 32 * nctr;
         a.nctr = (uint32_t)nctr;
         a.n_nd = P.n_nd;
@@ -1397,11 +1428,14 @@ void iterate(const K3Plan& P, const double* r_in, double* r_out, int iters, doub
             else spmv_sell_kernel<6, 768, 2><<<num_sms() * 2, 768, 0, s>>>(a);
             PRG_LAUNCH_CHECK();
         }
-        SplitArgs sp{P.n_split.get(), P.split_p0.get(), P.split_pbase.get(), P.partial.get(), S.out.get(), damping};
+        SplitArgs sp{P.n_split.get(), P.split_p0.get(), P.split_pbase.get(), P.partial.get(), out_of(it), damping};
         sell_sum_part<<<kSumBlocks, 1024, 0, s>>>(slice_sum.get(), P.nslices, y, sp, sum_part.get());
-        sell_sum_final<<<1, 32, 0, s>>>(sum_part.get(), kSumBlocks, (double)P.n_empty, bgf, S.out.get());
         PRG_LAUNCH_CHECK();
     }
+    // the last step's Σ (the earlier ones were finished by the gather launches)
+    sell_sum_final<<<1, 32, 0, s>>>(sum_part.get(), kSumBlocks, (double)P.n_empty, bgf, out_of(iters - 1));
+    PRG_LAUNCH_CHECK();
+    if (iters > 1) PRG_CUDA(cudaMemcpyAsync(S.out.get(), out_of(iters - 1), 4 * 8, cudaMemcpyDeviceToDevice, s));
     unpermute_kernel<<<g, 1024, 0, s>>>(ys[(iters - 1) & 1], P.spos_col.get(), S.out.get(), n, r_out);
     PRG_LAUNCH_CHECK();
 }

@@ -177,8 +177,17 @@ __global__ void __launch_bounds__(kScanThreads, 2) scan_down_kernel(const uint32
     // Blocked arrangement: thread t owns items [base + t*8, base + t*8 + 8).
     uint32_t v[kScanItems];
     const size_t my = base + (size_t)threadIdx.x * kScanItems;
+    // A thread's 8 items are 32 contiguous bytes: two 16-byte loads when the
+    // block is whole and aligned (8 separate 4-byte loads at a 32-byte lane
+    // stride cost 8 L1 wavefronts each: the kernel ran at ~1.6 TB/s).
+    const bool vec = my + kScanItems <= n && ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+    if (vec) {
+        const uint4 a = reinterpret_cast<const uint4*>(in + my)[0], b = reinterpret_cast<const uint4*>(in + my)[1];
+        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    } else {
 #pragma unroll
-    for (int k = 0; k < kScanItems; ++k) v[k] = (my + k < n) ? in[my + k] : 0u;
+        for (int k = 0; k < kScanItems; ++k) v[k] = (my + k < n) ? in[my + k] : 0u;
+    }
     uint64_t tsum = 0;
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) tsum += v[k];
@@ -192,10 +201,22 @@ __global__ void __launch_bounds__(kScanThreads, 2) scan_down_kernel(const uint32
     }
     __syncthreads();
     uint64_t run = partial[blockIdx.x] + warp_tot[dev::warp_id()] + inc - tsum;
+    Out o[kScanItems];
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
-        if (my + k < n) out[my + k] = static_cast<Out>(run);
+        o[k] = static_cast<Out>(run);
         run += v[k];
+    }
+    if (vec) {
+        static_assert(sizeof(Out) == 4 || sizeof(Out) == 8, "u32 or u64 output");
+        uint4* d = reinterpret_cast<uint4*>(out + my);
+        constexpr int kVec = kScanItems * (int)sizeof(Out) / 16;
+#pragma unroll
+        for (int q = 0; q < kVec; ++q) d[q] = reinterpret_cast<const uint4*>(o)[q];
+    } else {
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k)
+            if (my + k < n) out[my + k] = o[k];
     }
 }
 

@@ -351,9 +351,10 @@ __global__ void suffix_min_block(uint32_t* a, int64_t n1, uint32_t* part) {
     // each block: 1024 threads x 8 items, reverse order
     __shared__ uint32_t wm[32];
     const int64_t base = (int64_t)blockIdx.x * 8192;
+    // the block minimum needs no blocked order: coalesced strided reads
     uint32_t m = 0xffffffffu;
     for (int k = 0; k < 8; ++k) {
-        const int64_t i = base + threadIdx.x * 8 + k;
+        const int64_t i = base + k * 1024 + threadIdx.x;
         if (i < n1) m = min(m, a[i]);
     }
     m = __reduce_min_sync(0xffffffffu, m);
@@ -370,9 +371,14 @@ __global__ void suffix_min_down(uint32_t* a, int64_t n1, const uint32_t* blk_suf
     __shared__ uint32_t wm[33];
     const int64_t base = (int64_t)blockIdx.x * 8192;
     uint32_t v[8];
-    for (int k = 0; k < 8; ++k) {
-        const int64_t i = base + threadIdx.x * 8 + k;
-        v[k] = i < n1 ? a[i] : 0xffffffffu;
+    const int64_t my = base + threadIdx.x * 8;
+    // 32 contiguous bytes per thread: two 16-byte accesses when whole and aligned
+    const bool vec = my + 8 <= n1 && (reinterpret_cast<uintptr_t>(a) & 15) == 0;
+    if (vec) {
+        const uint4 x = reinterpret_cast<const uint4*>(a + my)[0], y = reinterpret_cast<const uint4*>(a + my)[1];
+        v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w; v[4] = y.x; v[5] = y.y; v[6] = y.z; v[7] = y.w;
+    } else {
+        for (int k = 0; k < 8; ++k) v[k] = my + k < n1 ? a[my + k] : 0xffffffffu;
     }
     uint32_t tm = 0xffffffffu;
     for (int k = 0; k < 8; ++k) tm = min(tm, v[k]);
@@ -401,8 +407,14 @@ __global__ void suffix_min_down(uint32_t* a, int64_t n1, const uint32_t* blk_suf
     if (dev::lane_id() < 31) run = min(run, after);
     for (int k = 7; k >= 0; --k) {
         run = min(run, v[k]);
-        const int64_t i = base + threadIdx.x * 8 + k;
-        if (i < n1) a[i] = run;
+        v[k] = run;
+    }
+    if (vec) {
+        reinterpret_cast<uint4*>(a + my)[0] = make_uint4(v[0], v[1], v[2], v[3]);
+        reinterpret_cast<uint4*>(a + my)[1] = make_uint4(v[4], v[5], v[6], v[7]);
+    } else {
+        for (int k = 0; k < 8; ++k)
+            if (my + k < n1) a[my + k] = v[k];
     }
 }
 

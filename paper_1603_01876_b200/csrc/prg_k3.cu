@@ -224,11 +224,14 @@ __global__ void perm_degree_kernel(const uint32_t* __restrict__ ro, const uint32
         deg[i] = ro[u + 1] - ro[u];
     }
 }
-__global__ void perm_delta_kernel(const uint32_t* __restrict__ ro, const uint32_t* __restrict__ pinv,
-                                  const uint32_t* __restrict__ pro, int64_t nr, uint32_t* __restrict__ wdelta) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nr; i += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t u = pinv[i];
-        wdelta[u] = pro[i] - ro[u];
+// Walked in the original row order (a gather of pro through newid, coalesced
+// stores): walking the new order scattered the stores (0.21 ms at S=24).
+__global__ void perm_delta_kernel(const uint32_t* __restrict__ ro, const uint32_t* __restrict__ newid,
+                                  const uint32_t* __restrict__ pro, int64_t n, int64_t nr,
+                                  uint32_t* __restrict__ wdelta) {
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t j = newid[u];
+        if (j < (uint64_t)nr) wdelta[u] = pro[j] - ro[u];
     }
 }
 
@@ -1112,7 +1115,7 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
             perm_degree_kernel<<<g, 1024, 0, s>>>(A->row_offsets, P.pinv.get(), nr, deg.get());
             PRG_LAUNCH_CHECK();
             exclusive_scan_u32(deg.get(), pro.get(), (size_t)nr, pro.get() + nr, s);
-            perm_delta_kernel<<<g, 1024, 0, s>>>(A->row_offsets, P.pinv.get(), pro.get(), nr, wdelta.get());
+            perm_delta_kernel<<<g, 1024, 0, s>>>(A->row_offsets, P.newid.get(), pro.get(), n, nr, wdelta.get());
             PRG_LAUNCH_CHECK();
         }
         if (nnz) {

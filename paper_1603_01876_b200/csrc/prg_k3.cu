@@ -663,7 +663,6 @@ __global__ void sell_fill_kernel(FillArgs a) {
             const uint32_t part = v - a.vc_base[c];
             np = a.vc_base[c + 1] - a.vc_base[c];
             start = a.colptr[c] + part * a.vcmax;
-            if (part == 0) a.spos_col[c] = pos;
         }
         a.lane_len[pos] = len;
         a.lane_col[pos] = c;
@@ -699,6 +698,14 @@ __global__ void sell_fill_kernel(FillArgs a) {
                 }
             }
         }
+    }
+}
+
+__global__ void spos_col_kernel(const uint32_t* __restrict__ vc_base, const uint32_t* __restrict__ vpos, int64_t n,
+                                uint32_t* __restrict__ spos_col) {
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t v0 = vc_base[c];
+        spos_col[c] = vc_base[c + 1] > v0 ? vpos[v0] : kEmpty;
     }
 }
 
@@ -1226,7 +1233,10 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
     P.lane_col = DevBuf<uint32_t>(NP ? NP : 1, s);
     P.lane_np = DevBuf<uint32_t>(NP ? NP : 1, s);
     P.spos_col = DevBuf<uint32_t>((size_t)n, s);
-    PRG_CUDA(cudaMemsetAsync(P.spos_col.get(), 0xff, (size_t)n * 4, s));
+    // SELL position of every column's part 0 (kEmpty: empty column), a gather
+    // through vpos in column order
+    spos_col_kernel<<<g, 1024, 0, s>>>(P.vc_base.get(), P.vpos.get(), n, P.spos_col.get());
+    PRG_LAUNCH_CHECK();
     if (P.nslices) {
         FillArgs fa{order.get(),         vc_col.get(),     vc_len.get(), P.vc_base.get(),   P.colptr.get(),
                     P.csc_idx.get(),     P.slice_ptr.get(), V,                P.nslices,

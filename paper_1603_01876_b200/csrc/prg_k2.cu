@@ -126,10 +126,21 @@ __global__ void __launch_bounds__(kT) k2_pass_a(const longlong2* __restrict__ uv
                 px = q.x;
                 py = q.y;
             }
-            if (l < cnt) {
+            // Warp-aggregated in-degree: duplicate edges are adjacent (sorted
+            // input), so a run of equal edges within the warp's 32 lanes adds
+            // its length with one atomic from its first lane.
+            const bool valid = l < cnt;
+            const bool same = valid && (lane > 0 || base + l > 0) && p[j].x == px && p[j].y == py;
+            const unsigned eqm = __ballot_sync(0xffffffffu, same);
+            if (valid) {
                 const bool ok = p[j].x >= 1 && p[j].x <= n && p[j].y >= 1 && p[j].y <= n;
                 if (!ok) my_err |= kErrLabelRange;
-                else atomicAdd(&d_in[(uint32_t)(p[j].y - 1)], 1u);
+                else if (!same || lane == 0) {
+                    // lanes after me that continue my run: the set bits of eqm above my lane, up to the first gap
+                    const unsigned after = ~(eqm >> lane >> 1) & (0x7fffffffu >> lane);
+                    const uint32_t len = 1u + (after ? (uint32_t)(__ffs(after) - 1) : 31u - lane);
+                    atomicAdd(&d_in[(uint32_t)(p[j].y - 1)], len);
+                }
                 if (base + l == 0) {
                     heads++;
                 } else {

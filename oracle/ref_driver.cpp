@@ -147,6 +147,116 @@ double ref_init_rank(std::int64_t n, std::uint64_t seed, double* r) {
     return rv.norm1;
 }
 
+// Full-size pipeline digests (tests/golden/make_digests.py): runs the
+// reference's K0 -> K1 core -> K2 steps -> run_kernel3 at one BASELINE config
+// on the lean memory path (each stage's input freed before the next stage's
+// output is materialised: S=26 peaks at ~35 GB) and hands every output array to
+// `emit` (called one or more times per name, in order: the caller hashes the
+// chunks). Arrays and their byte forms:
+//   "k1"        int64 (u,v) pairs: std::sort by u (kernel1_sort.cpp:66), ties
+//               then re-sorted by v (tests/helpers.hpp:29-34 canonicalizer)
+//   "d_in"      int64[n]   in_degree (kernel2_filter.cpp:101-106), pre-zeroing
+//   "row_offsets" int64[n+1], "cols" int64[nnz_f] (0-based), "values" f64[nnz_f]
+//               row_normalize(zero_columns(build_adjacency(...))) (:12-152)
+//   "ranks"     f64[n]     run_kernel3 (kernel3_pagerank.cpp:67-79), c=0.85,
+//               `iterations`, seed=k3_seed, total_edges=m
+// stats[0..3] = nnz_raw, nnz_f, max d_in, norm1. Returns 0, or -1 on error.
+typedef void (*ref_emit_fn)(const char* name, const void* data, std::int64_t bytes);
+
+int ref_digest_pipeline(int scale, std::uint64_t seed, const double* init, int threads,
+                        std::uint64_t k3_seed, int iterations, ref_emit_fn emit, double* stats) {
+    try {
+        const std::int64_t n = std::int64_t{1} << scale;
+        const std::int64_t m = 16 * n;
+        auto emit_chunks = [&](const char* name, const void* p, std::int64_t bytes) {
+            const std::int64_t chunk = std::int64_t{256} << 20;
+            const auto* b = static_cast<const char*>(p);
+            if (bytes == 0) emit(name, b, 0);
+            for (std::int64_t o = 0; o < bytes; o += chunk) emit(name, b + o, std::min(chunk, bytes - o));
+        };
+        std::vector<Edge> edges(static_cast<std::size_t>(m));
+        if (ref_generate(scale, seed, init, 1, threads, reinterpret_cast<std::int64_t*>(edges.data())) != 0)
+            return -1;
+        std::sort(edges.begin(), edges.end(), [](const Edge& a, const Edge& b) { return a.u < b.u; });
+        for (std::size_t i = 0; i < edges.size();) {
+            std::size_t j = i + 1;
+            while (j < edges.size() && edges[j].u == edges[i].u) ++j;
+            std::sort(edges.begin() + i, edges.begin() + j, [](const Edge& a, const Edge& b) { return a.v < b.v; });
+            i = j;
+        }
+        emit_chunks("k1", edges.data(), m * 16);
+        CountMatrix a = build_adjacency(std::span<const Edge>(edges.data(), edges.size()), n);
+        std::vector<Edge>().swap(edges);
+        const std::vector<std::int64_t> din = in_degree(a);
+        emit_chunks("d_in", din.data(), n * 8);
+        stats[0] = static_cast<double>(a.nnz());
+        stats[2] = static_cast<double>(std::max<std::int64_t>(0, *std::max_element(din.begin(), din.end())));
+        CountMatrix f = zero_columns(a, din);
+        a = CountMatrix{};
+        StochasticMatrix s = row_normalize(f);
+        f = CountMatrix{};
+        stats[1] = static_cast<double>(s.nnz());
+        emit_chunks("row_offsets", s.row_offsets.data(), (n + 1) * 8);
+        emit_chunks("cols", s.cols.data(), s.nnz() * 8);
+        emit_chunks("values", s.values.data(), s.nnz() * 8);
+        PageRankConfig c;
+        c.damping = 0.85;
+        c.iterations = iterations;
+        c.seed = k3_seed;
+        auto res = run_kernel3(s, c, m);
+        emit_chunks("ranks", res.ranks.values.data(), n * 8);
+        stats[3] = res.ranks.norm1;
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+// read_edges (src/edge_io.cpp:288-295) on a manifest directory, and the
+// streaming EdgeFileReader (:198-262) on one shard with a given buffer size —
+// for comparing the drop-in's accepted inputs and error messages. Return the
+// edge count (pairs copied while < cap), or -1 (message: ref_last_error;
+// *parse_line = the ParseError line, 0 for a plain Error).
+std::int64_t ref_read_edges(const char* dir, std::int64_t* uv, std::int64_t cap, std::int64_t* parse_line) {
+    *parse_line = 0;
+    try {
+        const auto e = read_edges(EdgeManifest::load(dir));
+        const auto n = static_cast<std::int64_t>(e.size());
+        std::memcpy(uv, e.data(), sizeof(Edge) * static_cast<std::size_t>(std::min(n, cap)));
+        return n;
+    } catch (const ParseError& e) {
+        g_err = e.what();
+        *parse_line = e.line;
+        return -1;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+std::int64_t ref_stream_file(const char* path, std::int64_t max_label, std::int64_t buffer_bytes, std::int64_t* uv,
+                             std::int64_t cap, std::int64_t* parse_line) {
+    *parse_line = 0;
+    std::int64_t n = 0;
+    try {
+        EdgeFileReader r(path, max_label, static_cast<std::size_t>(buffer_bytes));
+        Edge e;
+        while (r.next(e)) {
+            if (n < cap) std::memcpy(uv + 2 * n, &e, sizeof(Edge));
+            ++n;
+        }
+        return n;
+    } catch (const ParseError& e) {
+        g_err = e.what();
+        *parse_line = e.line;
+        return -1;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
 // write_edges (src/edge_io.cpp:191-196) — shard and manifest bytes for the
 // drop-in's edge I/O comparison.
 int ref_write_edges(const std::int64_t* uv, std::int64_t m, const char* dir, int num_files, int scale,

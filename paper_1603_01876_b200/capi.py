@@ -34,7 +34,7 @@ HEADER_SYMBOLS = (
     "prg_init_rank_device", "prg_pagerank_step_device", "prg_launch_count", "prg_last_h2d_bytes", "prg_profile_enable",
     "prg_profile_report", "prg_build_adjacency_host", "prg_in_degree_host", "prg_zero_columns_host",
     "prg_row_normalize_host", "prg_init_rank_host", "prg_pagerank_step_host", "prg_k3_pagerank_matrix_host",
-    "prg_run_to_convergence_host",
+    "prg_run_to_convergence_host", "prg_trim_memory",
 )
 
 
@@ -89,6 +89,7 @@ def lib() -> C.CDLL:
             "prg_pagerank_step_host": (i32, [i64, i64, vp, vp, vp, vp, f64, i32, vp, vp]),
             "prg_k3_pagerank_matrix_host": (i32, [vp, f64, i32, u64, i32, vp, vp]),
             "prg_run_to_convergence_host": (i32, [i64, i64, vp, vp, vp, f64, f64, i32, vp, vp, vp, vp]),
+            "prg_trim_memory": (i32, []),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -117,6 +118,11 @@ def _stream(stream) -> int:
 
         return torch.cuda.current_stream().cuda_stream
     return getattr(stream, "cuda_stream", stream)
+
+
+def trim_memory() -> None:
+    """Return the library pool's unused device memory to the driver (prg_trim_memory)."""
+    _check(lib().prg_trim_memory())
 
 
 # ---- K0 -------------------------------------------------------------------
@@ -178,6 +184,28 @@ class DeviceMatrix:
         din = np.empty(self.n, dtype=np.int64)
         _check(lib().prg_matrix_download(self.handle, _ptr(ro), _ptr(cols), _ptr(vals), _ptr(din)))
         return ro, cols[: self.nnz], vals[: self.nnz], din
+
+    def device_views(self):
+        """Zero-copy torch views of the device arrays (prg_matrix_device_arrays):
+        (row_offsets u32[n+1], cols u32[nnz], values f64[nnz], d_in u32[n] or None),
+        the u32 arrays viewed as int32 (every value is < 2^31 up to S=30)."""
+        import torch
+
+        ro, cols, vals, din = (C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_void_p())
+        _check(lib().prg_matrix_device_arrays(self.handle, C.byref(ro), C.byref(cols), C.byref(vals), C.byref(din)))
+
+        class _View:
+            def __init__(self, ptr, count, typestr):
+                self.__cuda_array_interface__ = {"shape": (count,), "typestr": typestr, "data": (ptr or 0, False),
+                                                 "version": 3, "strides": None}
+
+        def view(p, count, typestr):
+            if count == 0 or not p.value:
+                return torch.empty(0, dtype=torch.float64 if typestr == "<f8" else torch.int32, device="cuda")
+            return torch.as_tensor(_View(p.value, count, typestr), device="cuda")
+
+        return (view(ro, self.n + 1, "<i4"), view(cols, self.nnz, "<i4"), view(vals, self.nnz, "<f8"),
+                view(din, self.n, "<i4") if din.value else None)
 
     def build_csc(self, stream=None) -> "DeviceMatrix":
         """K2's CSC build: keep K3's column layout on the handle (prg_matrix_build_csc)."""

@@ -90,6 +90,25 @@ __global__ void narrow_i64(const int64_t* __restrict__ in, int64_t n, int64_t li
     }
 }
 
+// Row offsets: narrowed like narrow_i64 and required non-decreasing (a
+// decreasing pair would make ro[u+1]-ro[u] wrap as u32 in every row-length
+// computation downstream): kErrBadOffsets.
+constexpr uint32_t kErrBadOffsets = 0x100u;
+__global__ void narrow_offsets(const int64_t* __restrict__ in, int64_t n, int64_t limit, uint32_t* __restrict__ out,
+                               uint32_t* err) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t x = in[i];
+        if (x < 0 || x > limit) atomicOr(err, (uint32_t)prg::kErrLabelRange);
+        if (i + 1 < n && in[i + 1] < x) atomicOr(err, kErrBadOffsets);
+        out[i] = (uint32_t)x;
+    }
+}
+
+void check_upload_flags(uint32_t h) {
+    require(!(h & kErrBadOffsets), PRG_ERR_INVALID_ARGUMENT, "row_offsets must be non-decreasing");
+    require(h == 0, PRG_ERR_LABEL_RANGE, "row offsets or column indices out of range");
+}
+
 // ---------------------------------------------------------------------------
 // Host-buffer K3 (prg_k3_pagerank_host): the CSR crosses PCIe (~55 GB/s) —
 // the bound of the whole call. The f64 values are run-length coded on the
@@ -204,6 +223,12 @@ const char* prg_version(void) { return "prg-b200 0.1.0 (sm_100a)"; }
 int64_t prg_launch_count(void) { return prg::launch_count(); }
 int64_t prg_last_h2d_bytes(void) { return g_last_h2d_bytes; }
 void prg_profile_enable(int32_t on) { prg::profiling_enable(on != 0); }
+prg_status prg_trim_memory(void) {
+    return guarded("prg_trim_memory", [&] {
+        PRG_CUDA(cudaDeviceSynchronize());
+        prg::ws_trim();
+    });
+}
 int64_t prg_profile_report(char* buf, int64_t cap, int32_t reset) {
     const std::string s = prg::profile_report(reset != 0);
     if (buf && cap > 0) {
@@ -457,8 +482,8 @@ prg_status prg_matrix_from_host(int64_t n, int64_t nnz, const int64_t* row_offse
         {
             DevBuf<int64_t> tmp((size_t)n + 1, s);
             PRG_CUDA(cudaMemcpyAsync(tmp.get(), row_offsets, (size_t)(n + 1) * 8, cudaMemcpyHostToDevice, s));
-            narrow_i64<<<(unsigned)prg::num_sms() * 4, 1024, 0, s>>>(tmp.get(), n + 1, nnz, mat->row_offsets,
-                                                                      err.get());
+            narrow_offsets<<<(unsigned)prg::num_sms() * 4, 1024, 0, s>>>(tmp.get(), n + 1, nnz, mat->row_offsets,
+                                                                          err.get());
             PRG_LAUNCH_CHECK();
         }
         if (nnz) {
@@ -471,7 +496,7 @@ prg_status prg_matrix_from_host(int64_t n, int64_t nnz, const int64_t* row_offse
         uint32_t h = 0;
         PRG_CUDA(cudaMemcpyAsync(&h, err.get(), 4, cudaMemcpyDeviceToHost, s));
         PRG_CUDA(cudaStreamSynchronize(s));
-        require(h == 0, PRG_ERR_LABEL_RANGE, "row offsets or column indices out of range");
+        check_upload_flags(h);
         *out = mat.release();
     });
 }
@@ -505,7 +530,7 @@ prg_status prg_k3_pagerank_device(const prg_matrix* a, double damping, int32_t i
         // PageRankConfig::validate (kernel3_pagerank.cpp:23-27)
         require(damping > 0.0 && damping < 1.0, PRG_ERR_INVALID_ARGUMENT, "damping must lie strictly between 0 and 1");
         require(iterations >= 1, PRG_ERR_INVALID_ARGUMENT, "iteration count must be >= 1");
-        require(mode == 0 || mode == 1, PRG_ERR_INVALID_ARGUMENT, "mode must be 0 (timed) or 1 (parity)");
+        require(mode >= 0 && mode <= 2, PRG_ERR_INVALID_ARGUMENT, "mode must be 0 (timed), 1 (parity) or 2 (Neumaier)");
         prg::K3Options o;
         o.damping = damping;
         o.iterations = iterations;
@@ -563,7 +588,7 @@ prg_status prg_k3_pagerank_host(int64_t n, int64_t nnz, const int64_t* row_offse
         // caller's buffers are pinned; staged, but still concurrent, when pageable)
         DevBuf<int64_t> tro((size_t)n + 1, s), tcol(nnz ? (size_t)nnz : 1, s);
         PRG_CUDA(cudaMemcpyAsync(tro.get(), row_offsets, (size_t)(n + 1) * 8, cudaMemcpyHostToDevice, s));
-        narrow_i64<<<(unsigned)prg::num_sms() * 4, 1024, 0, s>>>(tro.get(), n + 1, nnz, mat->row_offsets, err.get());
+        narrow_offsets<<<(unsigned)prg::num_sms() * 4, 1024, 0, s>>>(tro.get(), n + 1, nnz, mat->row_offsets, err.get());
         PRG_LAUNCH_CHECK();
         int64_t runs = 0;
         double t1 = now(), t2 = t1;
@@ -592,7 +617,7 @@ prg_status prg_k3_pagerank_host(int64_t n, int64_t nnz, const int64_t* row_offse
             uint32_t h = 0;
             PRG_CUDA(cudaMemcpyAsync(&h, err.get(), 4, cudaMemcpyDeviceToHost, s));
             PRG_CUDA(cudaStreamSynchronize(s));  // uploads done: the pinned stages are reused by the next call
-            require(h == 0, PRG_ERR_LABEL_RANGE, "row offsets or column indices out of range");
+            check_upload_flags(h);
         }
         g_last_h2d_bytes = (n + 1) * 8 + nnz * 8 + (nnz + 31) / 32 * 4 + runs * 8;
         const double t3 = now();

@@ -60,6 +60,7 @@ int num_sms();
 // pool, whose release threshold the library raises to "keep everything").
 void* ws_alloc(size_t bytes, cudaStream_t s);
 void ws_free(void* p, cudaStream_t s);
+void ws_trim();  // return the library pool's unused memory to the driver
 
 template <class T>
 struct DevBuf {

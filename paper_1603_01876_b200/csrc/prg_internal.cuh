@@ -55,7 +55,8 @@ struct K3Options {
     double damping = 0.85;
     int iterations = 20;
     uint64_t seed = 0;
-    int mode = 0;  // 0 = timed (deterministic tree sums), 1 = parity (reference order)
+    int mode = 0;  // 0 = timed (deterministic tree sums), 1 = parity (reference order),
+                   // 2 = parity order with Neumaier sums (drift attribution)
 };
 // Full run_kernel3 semantics: init_rank + iterations steps. d_ranks [n] in the
 // original vertex order; returns norm1 (sum of the final vector).

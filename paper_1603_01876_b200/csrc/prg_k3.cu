@@ -495,6 +495,23 @@ __global__ void seq_sum_kernel(const double* __restrict__ x, int64_t n, double b
     out[0] = s;
     out[1] = __dmul_rn(bgf, s);
 }
+// Neumaier mode (mode 2): the same single pass with a compensated sum — the
+// drift-attribution restatement of SURVEY §8(c): every sum_of
+// (kernel3_pagerank.cpp:17-19) replaced by Neumaier's, as oracle/prg_oracle.c's
+// accurate mode.
+__global__ void seq_neumaier_kernel(const double* __restrict__ x, int64_t n, double bgf, double* __restrict__ out) {
+    if (threadIdx.x || blockIdx.x) return;
+    double s = 0.0, c = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+        const double v = x[i];
+        const double t = __dadd_rn(s, v);
+        c = __dadd_rn(c, fabs(s) >= fabs(v) ? __dadd_rn(__dsub_rn(s, t), v) : __dadd_rn(__dsub_rn(v, t), s));
+        s = t;
+    }
+    s = __dadd_rn(s, c);
+    out[0] = s;
+    out[1] = __dmul_rn(bgf, s);
+}
 __global__ void __launch_bounds__(1024, 2) scale_kernel(double* __restrict__ x, int64_t n, const double* __restrict__ sum) {
     const double d = sum[0];
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -1321,6 +1338,7 @@ void build_plan(const prg_matrix* A, int mode, K3Plan& P, cudaStream_t s) {
 // The layout kept on the handle when it matches the mode, else one built now
 // (inside the caller's timed region) into `tmp`.
 const K3Plan& plan_for(const prg_matrix* A, int mode, K3Plan& tmp, cudaStream_t s) {
+    mode = mode == 0 ? 0 : 1;  // the Neumaier mode runs on the parity layout
     if (A->plan && A->plan->mode == mode) return *A->plan;
     build_plan(A, mode, tmp, s);
     return tmp;
@@ -1341,6 +1359,8 @@ void device_sum(const double* x, int64_t n, double bgf, int mode, Sums& S, cudaS
     }
     if (mode == 1) {
         seq_sum_kernel<<<1, 1, 0, s>>>(x, n, bgf, S.out.get());
+    } else if (mode == 2) {
+        seq_neumaier_kernel<<<1, 1, 0, s>>>(x, n, bgf, S.out.get());
     } else {
         const int64_t nb = (n + 8191) / 8192;
         if (S.part.n < (size_t)nb) S.part = DevBuf<double>((size_t)nb, s);
@@ -1373,7 +1393,7 @@ void init_rank_impl(int64_t n, uint64_t seed, double* d_r, int mode, double bgf,
 // writes the final iterate to r_out (original order); S.out ends as
 // {sum(r_out), bg', bg_used}.
 void iterate(const K3Plan& P, const double* r_in, double* r_out, int iters, double damping, double bgf, Sums& S,
-             cudaStream_t s, uint64_t rng_s0 = 0, const double* rng_div = nullptr) {
+             cudaStream_t s, uint64_t rng_s0 = 0, const double* rng_div = nullptr, int sum_mode = 1) {
     const unsigned g = (unsigned)num_sms() * 8;
     const int64_t n = P.n;
     if (P.mode == 1) {
@@ -1387,7 +1407,7 @@ void iterate(const K3Plan& P, const double* r_in, double* r_out, int iters, doub
                       S.out.get(), dst, n, damping};
             spmv_seq_kernel<<<g, 256, 0, s>>>(a);
             PRG_LAUNCH_CHECK();
-            device_sum(dst, n, bgf, 1, S, s);
+            device_sum(dst, n, bgf, sum_mode, S, s);
             cur = dst;
         }
         if (cur != r_out) PRG_CUDA(cudaMemcpyAsync(r_out, cur, (size_t)n * 8, cudaMemcpyDeviceToDevice, s));
@@ -1571,10 +1591,11 @@ double k3_pagerank_device(const prg_matrix* A, const K3Options& opt, double* d_r
     K3Plan tmp;
     const K3Plan& P = plan_for(A, opt.mode, tmp, s);
     Sums S;
-    if (opt.mode == 1 || P.nslices == 0) {
+    if (opt.mode != 0 || P.nslices == 0) {
         DevBuf<double> r0((size_t)n, s);
+        // mode 2 takes every Σ compensated, init_rank's too (oracle_run_kernel3 mode 1)
         init_rank_impl(n, opt.seed, r0.get(), opt.mode, bgf, S, s);
-        iterate(P, r0.get(), d_ranks, opt.iterations, opt.damping, bgf, S, s);
+        iterate(P, r0.get(), d_ranks, opt.iterations, opt.damping, bgf, S, s, 0, nullptr, opt.mode == 2 ? 2 : 1);
         return read_scalar(S.out.get(), s);
     }
     // Timed mode: init_rank's vector is never stored — its two sums are taken
@@ -1602,7 +1623,7 @@ double k3_step_device(const prg_matrix* A, const double* d_r, double damping, do
     const K3Plan& P = plan_for(A, mode, tmp, s);
     Sums S;
     device_sum(d_r, n, bgf, mode, S, s);
-    iterate(P, d_r, d_out, 1, damping, bgf, S, s);
+    iterate(P, d_r, d_out, 1, damping, bgf, S, s, 0, nullptr, mode == 2 ? 2 : 1);
     return read_scalar(S.out.get(), s);
 }
 

@@ -79,19 +79,37 @@ int num_sms() {
     return cached;
 }
 
-void* ws_alloc(size_t bytes, cudaStream_t s) {
+// The library allocates its device workspace from a PRIVATE stream-ordered
+// pool (not the device's default pool, which torch and other libraries share).
+// Freed blocks stay cached up to kPoolKeepBytes so repeated calls do not go
+// back to the driver; prg_trim_memory() returns everything unused.
+constexpr uint64_t kPoolKeepBytes = uint64_t{8} << 30;
+cudaMemPool_t g_pool = nullptr;
+
+cudaMemPool_t library_pool() {
     std::call_once(g_pool_once, [] {
         int dev = 0;
-        cudaGetDevice(&dev);
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t keep = UINT64_MAX;  // keep freed blocks cached across calls
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-        }
+        PRG_CUDA(cudaGetDevice(&dev));
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.handleTypes = cudaMemHandleTypeNone;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        PRG_CUDA(cudaMemPoolCreate(&g_pool, &props));
+        uint64_t keep = kPoolKeepBytes;
+        PRG_CUDA(cudaMemPoolSetAttribute(g_pool, cudaMemPoolAttrReleaseThreshold, &keep));
     });
+    return g_pool;
+}
+
+void* ws_alloc(size_t bytes, cudaStream_t s) {
     void* p = nullptr;
-    PRG_CUDA(cudaMallocAsync(&p, bytes ? bytes : 16, s));
+    PRG_CUDA(cudaMallocFromPoolAsync(&p, bytes ? bytes : 16, library_pool(), s));
     return p;
+}
+
+void ws_trim() {
+    if (g_pool) PRG_CUDA(cudaMemPoolTrimTo(g_pool, 0));
 }
 
 void ws_free(void* p, cudaStream_t s) {
@@ -201,7 +219,7 @@ __global__ void __launch_bounds__(kScanThreads, 2) scan_down_kernel(const uint32
     }
     __syncthreads();
     uint64_t run = partial[blockIdx.x] + warp_tot[dev::warp_id()] + inc - tsum;
-    Out o[kScanItems];
+    alignas(16) Out o[kScanItems];
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
         o[k] = static_cast<Out>(run);
@@ -212,7 +230,11 @@ __global__ void __launch_bounds__(kScanThreads, 2) scan_down_kernel(const uint32
         uint4* d = reinterpret_cast<uint4*>(out + my);
         constexpr int kVec = kScanItems * (int)sizeof(Out) / 16;
 #pragma unroll
-        for (int q = 0; q < kVec; ++q) d[q] = reinterpret_cast<const uint4*>(o)[q];
+        for (int q = 0; q < kVec; ++q) {
+            uint4 w;  // byte copy: no type-punned load of the Out array
+            memcpy(&w, reinterpret_cast<const char*>(o) + 16 * q, 16);
+            d[q] = w;
+        }
     } else {
 #pragma unroll
         for (int k = 0; k < kScanItems; ++k)

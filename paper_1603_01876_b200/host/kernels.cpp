@@ -7,7 +7,9 @@
 #include <cstdlib>
 #include <fstream>
 #include <list>
+#include <atomic>
 #include <mutex>
+#include <thread>
 #include <numeric>
 #include <unistd.h>
 
@@ -30,35 +32,72 @@ const std::int64_t* edge_words(std::span<const Edge> e) { return reinterpret_cas
 // ---- K2 -> K3 device residency --------------------------------
 // run_kernel2 returns a host StochasticMatrix (the reference's value type) but
 // keeps its device CSR; run_kernel3 on that same matrix reuses it instead of
-// uploading. Keyed by the host arrays' addresses and sizes, guarded by a
-// sampled fingerprint so a mutated or reallocated matrix misses.
+// uploading. An entry is keyed by the host arrays' address and sizes and
+// guarded by a hash of the matrix's FULL contents (every offset, column and
+// value bit), so any edit to the host matrix — or a new matrix at a recycled
+// address — misses and takes the upload path, exactly as the reference always
+// computes on the matrix it is given.
 struct CacheEntry {
     const void* cols_ptr;
     std::int64_t n, nnz;
-    std::uint64_t fp;
+    std::uint64_t digest;
     prg_matrix* dev;
 };
 std::mutex g_cache_mu;
 std::list<CacheEntry> g_cache;  // most recent first, at most 2 entries
 
-std::uint64_t fingerprint(const StochasticMatrix& a) {
-    std::uint64_t h = 0x9e3779b97f4a7c15ULL ^ static_cast<std::uint64_t>(a.n);
-    auto mix = [&](std::uint64_t x) { h = (h ^ x) * 0x100000001b3ULL; };
-    const std::size_t nz = a.cols.size();
-    for (std::size_t k = 0; k < 64 && nz; ++k) {
-        const std::size_t i = (k * 2654435761ULL) % nz;
-        mix(static_cast<std::uint64_t>(a.cols[i]));
-        std::uint64_t v;
-        std::memcpy(&v, &a.values[i], 8);
-        mix(v);
+// 64-bit content hash of a byte range: fixed 4 MiB chunks hashed on all host
+// threads (four independent multiply-xorshift lanes each), chunk hashes folded
+// in order — the value does not depend on the thread count.
+std::uint64_t hash_bytes(const void* data, std::size_t bytes, std::uint64_t seed) {
+    constexpr std::size_t kChunk = std::size_t{4} << 20;
+    const std::size_t nchunks = (bytes + kChunk - 1) / kChunk;
+    std::vector<std::uint64_t> part(nchunks);
+    auto mix = [](std::uint64_t h, std::uint64_t w) {
+        h = (h ^ w) * 0x9fb21c651e98df25ULL;
+        return h ^ (h >> 29);
+    };
+    auto chunk = [&](std::size_t c) {
+        const auto* p = static_cast<const unsigned char*>(data) + c * kChunk;
+        const std::size_t len = std::min(kChunk, bytes - c * kChunk);
+        std::uint64_t h[4] = {seed ^ c, ~seed ^ c, seed + 0x632be59bd9b4e019ULL, seed - c};
+        std::size_t i = 0;
+        for (; i + 32 <= len; i += 32)
+            for (int l = 0; l < 4; ++l) {
+                std::uint64_t w;
+                std::memcpy(&w, p + i + 8 * l, 8);
+                h[l] = mix(h[l], w);
+            }
+        for (; i < len; ++i) h[0] = mix(h[0], p[i]);
+        part[c] = mix(mix(mix(h[0], h[1]), h[2]), h[3] ^ len);
+    };
+    const unsigned nt = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), 32));
+    if (nchunks <= 1 || nt == 1) {
+        for (std::size_t c = 0; c < nchunks; ++c) chunk(c);
+    } else {
+        std::atomic<std::size_t> next{0};
+        std::vector<std::thread> crew;
+        for (unsigned t = 0; t < std::min<std::size_t>(nt, nchunks); ++t)
+            crew.emplace_back([&] {
+                for (std::size_t c; (c = next.fetch_add(1)) < nchunks;) chunk(c);
+            });
+        for (auto& th : crew) th.join();
     }
-    for (std::size_t k = 0; k < 64; ++k) mix(static_cast<std::uint64_t>(a.row_offsets[(k * 40503ULL) % a.row_offsets.size()]));
+    std::uint64_t h = mix(seed, bytes);
+    for (std::uint64_t x : part) h = mix(h, x);
     return h;
 }
 
+std::uint64_t content_digest(const StochasticMatrix& a) {
+    std::uint64_t h = hash_bytes(a.row_offsets.data(), a.row_offsets.size() * 8, static_cast<std::uint64_t>(a.n));
+    h = hash_bytes(a.cols.data(), a.cols.size() * 8, h);
+    return hash_bytes(a.values.data(), a.values.size() * 8, h);
+}
+
 void cache_put(const StochasticMatrix& a, prg_matrix* dev) {
+    const std::uint64_t d = content_digest(a);
     std::lock_guard<std::mutex> lk(g_cache_mu);
-    g_cache.push_front({a.cols.data(), a.n, a.nnz(), fingerprint(a), dev});
+    g_cache.push_front({a.cols.data(), a.n, a.nnz(), d, dev});
     while (g_cache.size() > 2) {
         prg_matrix_destroy(g_cache.back().dev);
         g_cache.pop_back();
@@ -66,9 +105,16 @@ void cache_put(const StochasticMatrix& a, prg_matrix* dev) {
 }
 
 prg_matrix* cache_get(const StochasticMatrix& a) {
+    {
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        bool keyed = false;
+        for (auto& e : g_cache) keyed |= e.cols_ptr == a.cols.data() && e.n == a.n && e.nnz == a.nnz();
+        if (!keyed) return nullptr;
+    }
+    const std::uint64_t d = content_digest(a);  // outside the lock: it reads GBs
     std::lock_guard<std::mutex> lk(g_cache_mu);
     for (auto& e : g_cache)
-        if (e.cols_ptr == a.cols.data() && e.n == a.n && e.nnz == a.nnz() && e.fp == fingerprint(a)) return e.dev;
+        if (e.cols_ptr == a.cols.data() && e.n == a.n && e.nnz == a.nnz() && e.digest == d) return e.dev;
     return nullptr;
 }
 
@@ -103,6 +149,12 @@ EdgeManifest sort_edges(const EdgeManifest& input, const std::filesystem::path& 
 }
 
 SortBreakdown last_sort_breakdown() { return g_last_sort; }
+
+void clear_device_cache() {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    for (auto& e : g_cache) prg_matrix_destroy(e.dev);
+    g_cache.clear();
+}
 
 // ---- K2 ----------------------------------------------------------------------
 std::int64_t CountMatrix::total() const { return std::accumulate(counts.begin(), counts.end(), std::int64_t{0}); }

@@ -523,9 +523,12 @@ def official_pipeline(scale):
     with tempfile.TemporaryDirectory() as d:
         prpipe.run_pipeline(scale=10, seed=1, data_dir=os.path.join(d, "warm"))  # CUDA/IO warm-up
         rep = prpipe.run_pipeline(scale=scale, seed=1, data_dir=os.path.join(d, "data"))
-    return {"scale": scale, "api": "prpipe.run_pipeline (drop-in, host TSV I/O inside each record)",
-            "records": {k["name"]: {"seconds": k["elapsed_seconds"], "edges_per_s": k["rate_edges_per_sec"]}
-                        for k in rep["kernels"]}}
+    out = {"scale": scale, "api": "prpipe.run_pipeline (drop-in, host TSV I/O inside each record)",
+           "records": {k["name"]: {"seconds": k["elapsed_seconds"], "edges_per_s": k["rate_edges_per_sec"]}
+                       for k in rep["kernels"]}}
+    if rep.get("failed"):
+        out["error"] = rep.get("error")
+    return out
 
 
 def run_reference(args):

@@ -59,8 +59,8 @@ int64_t prg_launch_count(void);
 int64_t prg_last_h2d_bytes(void);
 void prg_profile_enable(int32_t on);
 /* Device memory: the library allocates from its own stream-ordered pool
- * (freed blocks stay cached up to 8 GiB between calls); prg_trim_memory waits
- * for the device and returns every unused pooled byte to the driver. */
+ * (freed blocks stay cached between calls); prg_trim_memory waits for the
+ * device and returns every unused pooled byte to the driver. */
 prg_status prg_trim_memory(void);
 int64_t prg_profile_report(char* buf, int64_t cap, int32_t reset);
 

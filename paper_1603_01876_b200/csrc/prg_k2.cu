@@ -90,7 +90,7 @@ __device__ __forceinline__ int32_t block_excl_max_scan(int32_t v, int32_t* smem,
 __global__ void __launch_bounds__(kT) k2_pass_a(const longlong2* __restrict__ uv, int64_t m, int64_t n,
                                                 uint32_t* __restrict__ d_in, uint32_t* __restrict__ err,
                                                 unsigned long long* __restrict__ nnz_raw,
-                                                uint32_t ntiles, uint32_t* __restrict__ next_tile) {
+                                                uint32_t ntiles, uint32_t* __restrict__ next_tile, int flags) {
     __shared__ uint32_t red[kT / 32];
     __shared__ longlong2 last[kI][kT / 32];  // lane 31 of each (row j, warp)
     __shared__ longlong2 before;             // edge base-1
@@ -110,7 +110,9 @@ __global__ void __launch_bounds__(kT) k2_pass_a(const longlong2* __restrict__ uv
 #pragma unroll
         for (int j = 0; j < kI; ++j) {
             const int l = j * kT + threadIdx.x;
-            p[j] = l < cnt ? uv[base + l] : make_longlong2(0, 0);
+            // flags & 1: edges streamed with evict-first loads, so the d_in lines the
+            // atomics hit stay in L2 instead of being written back and re-fetched
+            p[j] = l < cnt ? ((flags & 1) ? __ldcs(uv + base + l) : uv[base + l]) : make_longlong2(0, 0);
             if (lane == 31) last[j][w] = p[j];
         }
         if (threadIdx.x == 0) before = base > 0 ? uv[base - 1] : make_longlong2(0, 0);
@@ -197,7 +199,7 @@ __global__ void __launch_bounds__(kT) k2_pass_b(
     unsigned long long* __restrict__ tile_status, uint32_t* __restrict__ tile_counter,
     uint32_t* __restrict__ dout_f, uint32_t* __restrict__ fix_rows, uint32_t* __restrict__ n_fix,
     uint32_t* __restrict__ cont_p, uint32_t* __restrict__ cont_c, unsigned long long* __restrict__ nnz_out,
-    bool normalize) {
+    bool normalize, int flags) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     PassBSmem& S = *reinterpret_cast<PassBSmem*>(smem_raw);
     const unsigned tid = threadIdx.x;
@@ -210,7 +212,7 @@ __global__ void __launch_bounds__(kT) k2_pass_b(
     for (int j = 0; j < kI; ++j) {
         const int l = j * kT + tid;
         if (l < cnt) {
-            const longlong2 p = uv[base + l];
+            const longlong2 p = (flags & 1) ? __ldcs(uv + base + l) : uv[base + l];
             const uint32_t v = (uint32_t)(p.y - 1);
             // keep bit fetched here, alongside the edge loads; carried in bit 31
             const uint32_t kp = (keepbits[v >> 5] >> (v & 31)) & 1u;
@@ -340,10 +342,16 @@ __global__ void __launch_bounds__(kT) k2_pass_b(
                     for (int64_t r = pu + 1; r <= (int64_t)u; ++r) row_offsets[r] = (uint32_t)pos;
                 }
                 if (((fl_hd >> k) & 1u) && ((fl_kp >> k) & 1u)) {
-                    cols[pos] = v;
                     const double c = (double)(S.rr[sp(l)] & 0xffffu);
                     const bool spanning = rh < 0 || (last_spans && rh == rh_last);
-                    values[pos] = (spanning || !normalize) ? c : c / (double)(S.rr[sp(rh)] >> 16);
+                    const double val = (spanning || !normalize) ? c : c / (double)(S.rr[sp(rh)] >> 16);
+                    if (flags & 2) {  // streaming stores: the outputs are not re-read by this pass
+                        __stcs(cols + pos, v);
+                        __stcs(values + pos, val);
+                    } else {
+                        cols[pos] = v;
+                        values[pos] = val;
+                    }
                     ++pos;
                 }
             }
@@ -453,9 +461,11 @@ uint32_t k2_filter_device(const int64_t* d_uv, int64_t m, int64_t n, prg_matrix*
         attr = true;
     }
     const unsigned ga = std::min<unsigned>(ntiles, (unsigned)num_sms() * 2);
+    static int flags = -1;  // PRG_K2_FLAGS (A/B measurement knob): bit 0 evict-first edge loads, bit 1 streaming stores
+    if (flags < 0) { const char* e = getenv("PRG_K2_FLAGS"); flags = e ? atoi(e) : 0; }
     {
         ProfScope pa("k2_pass_a", s);
-        k2_pass_a<<<ga, kT, 0, s>>>(uv, m, n, out->d_in, err, nnz_raw, ntiles, tile_counter_a);
+        k2_pass_a<<<ga, kT, 0, s>>>(uv, m, n, out->d_in, err, nnz_raw, ntiles, tile_counter_a, flags);
         PRG_LAUNCH_CHECK();
     }
     uint32_t h_err = 0;
@@ -495,7 +505,7 @@ uint32_t k2_filter_device(const int64_t* d_uv, int64_t m, int64_t n, prg_matrix*
         k2_pass_b<<<ntiles, kT, sizeof(PassBSmem), s>>>(uv, m, n, keepbits.get(), out->row_offsets, out->cols,
                                                         out->values, tile_status.get(), tile_counter, dout_f.get(),
                                                         fix_rows.get(), n_fix, cont_p.get(), cont_c.get(), nnz_out,
-                                                        normalize);
+                                                        normalize, flags);
         PRG_LAUNCH_CHECK();
     }
     k2_fix_runs<<<div_up(ntiles, 256), 256, 0, s>>>(cont_p.get(), cont_c.get(), ntiles, out->values);

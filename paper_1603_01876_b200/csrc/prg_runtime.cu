@@ -80,10 +80,12 @@ int num_sms() {
 }
 
 // The library allocates its device workspace from a PRIVATE stream-ordered
-// pool (not the device's default pool, which torch and other libraries share).
-// Freed blocks stay cached up to kPoolKeepBytes so repeated calls do not go
-// back to the driver; prg_trim_memory() returns everything unused.
-constexpr uint64_t kPoolKeepBytes = uint64_t{8} << 30;
+// pool (not the device's default pool, which other libraries share). Freed
+// blocks stay cached across calls — a finite release threshold made every
+// synchronising call hand memory back and re-map it on the next one (the S=24
+// CSC build went 12 -> 85 ms) — and prg_trim_memory() returns everything
+// unused on request.
+constexpr uint64_t kPoolKeepBytes = UINT64_MAX;
 cudaMemPool_t g_pool = nullptr;
 
 cudaMemPool_t library_pool() {

@@ -118,6 +118,21 @@ def test_multi_block_single_shard_roundtrip(tmp_path):
     assert core._stream_file(str(tmp_path / "big" / "edges_0000.tsv"), 1 << 19, 200) == e
 
 
+def test_bulk_reader_is_race_free(tmp_path):
+    """Blocks of one shard load concurrently; each block must count and decode
+    only its own bytes (a block once peeked at its neighbour's first byte while
+    that block was still loading). Repeated reads of multi-block shards must
+    all give the same edges."""
+    uv = O.generate(19, 11)
+    e = [tuple(x) for x in uv.tolist()]
+    man = prpipe.write_edges(e, tmp_path / "race", num_files=2, scale=19)
+    h = 0x243f6a8885a308d3
+    for u, v in e:
+        h = ((h ^ ((u * 1000003 + v) & (2**64 - 1))) * 0x100000001b3) & (2**64 - 1)
+    for _ in range(25):
+        assert core._read_edges_checksum(man) == (len(e), h)
+
+
 # ---- malformed input: the reference's exact error, line and precedence ---------
 def ref_read_error(d):
     import ctypes as C

@@ -84,6 +84,19 @@ prg_status prg_k1_sort_device(const int64_t* d_uv_in, int64_t m, int32_t scale, 
                               void* stream);
 prg_status prg_k1_sort_host(const int64_t* uv_in, int64_t m, int32_t scale, int64_t* uv_out);
 
+/* K1 under a host-memory budget — the B200 form of sort_edges' out-of-core
+ * path (src/kernel1_sort.cpp:133-149, 70-122: external merge sort when the
+ * list exceeds memory_budget_bytes / 16). The whole list lives in HBM; the host
+ * holds one pinned chunk of chunk_edges edges: `source` fills it (returns the
+ * edges written, 1..max_edges) until m edges arrived, the device sorts, and
+ * `sink` receives the sorted list chunk by chunk (returns 0, else the call
+ * fails). Same output as prg_k1_sort_host. Lists beyond 2^32-1 edges or the
+ * free device memory are refused with PRG_ERR_INVALID_ARGUMENT. */
+typedef int64_t (*prg_edge_source)(void* user, int64_t* uv, int64_t max_edges);
+typedef int32_t (*prg_edge_sink)(void* user, const int64_t* uv, int64_t count);
+prg_status prg_k1_sort_streamed(prg_edge_source source, prg_edge_sink sink, void* user, int64_t m, int32_t scale,
+                                int64_t chunk_edges);
+
 /* ---- K2 — replaces run_kernel2's core -------------------------------------
  * build_adjacency + in_degree + zero_columns + row_normalize
  * (include/prpipe/kernel2_filter.hpp:42-65; src/kernel2_filter.cpp:12-168).

@@ -34,7 +34,7 @@ HEADER_SYMBOLS = (
     "prg_init_rank_device", "prg_pagerank_step_device", "prg_launch_count", "prg_last_h2d_bytes", "prg_profile_enable",
     "prg_profile_report", "prg_build_adjacency_host", "prg_in_degree_host", "prg_zero_columns_host",
     "prg_row_normalize_host", "prg_init_rank_host", "prg_pagerank_step_host", "prg_k3_pagerank_matrix_host",
-    "prg_run_to_convergence_host", "prg_trim_memory",
+    "prg_run_to_convergence_host", "prg_trim_memory", "prg_k1_sort_streamed",
 )
 
 
@@ -90,6 +90,7 @@ def lib() -> C.CDLL:
             "prg_k3_pagerank_matrix_host": (i32, [vp, f64, i32, u64, i32, vp, vp]),
             "prg_run_to_convergence_host": (i32, [i64, i64, vp, vp, vp, f64, f64, i32, vp, vp, vp, vp]),
             "prg_trim_memory": (i32, []),
+            "prg_k1_sort_streamed": (i32, [vp, vp, vp, i64, i32, i64]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)

@@ -307,6 +307,52 @@ prg_status prg_k1_sort_host(const int64_t* uv_in, int64_t m, int32_t scale, int6
     });
 }
 
+// K1 under a host-memory budget: see include/prg.h. The device holds the whole
+// list (the B200's "memory" is its HBM); the host only ever holds one pinned
+// chunk, filled by the source and drained to the sink.
+prg_status prg_k1_sort_streamed(prg_edge_source source, prg_edge_sink sink, void* user, int64_t m, int32_t scale,
+                                int64_t chunk_edges) {
+    return guarded("prg_k1_sort_streamed", [&] {
+        require(source && sink && m >= 0 && chunk_edges >= 1, PRG_ERR_INVALID_ARGUMENT, "bad streamed-sort arguments");
+        require((uint64_t)m < (1ull << 32), PRG_ERR_INVALID_ARGUMENT,
+                "K1: " + std::to_string(m) + " edges exceed the device sort's 2^32-1 per call");
+        if (m == 0) return;
+        cudaStream_t s = nullptr;
+        // input + output lists, 2 key buffers and scratch: ~56 B per edge on the device
+        size_t free_b = 0, total_b = 0;
+        PRG_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        const double need = 56.0 * (double)m;
+        require(need < 0.95 * (double)free_b, PRG_ERR_INVALID_ARGUMENT,
+                "K1: " + std::to_string(m) + " edges need ~" + std::to_string((int64_t)(need / 1e9)) +
+                    " GB of device memory, " + std::to_string((int64_t)(free_b / 1e9)) + " GB free");
+        const int64_t chunk = std::min<int64_t>(chunk_edges, m);
+        int64_t* pinned = nullptr;
+        PRG_CUDA(cudaMallocHost(&pinned, (size_t)chunk * 16));
+        struct FreeHost {
+            int64_t* p;
+            ~FreeHost() { cudaFreeHost(p); }
+        } free_pinned{pinned};
+        DevBuf<int64_t> a((size_t)m * 2, s), b((size_t)m * 2, s);
+        for (int64_t got = 0; got < m;) {
+            const int64_t k = source(user, pinned, std::min(chunk, m - got));
+            require(k > 0 && k <= std::min(chunk, m - got), PRG_ERR_INVALID_ARGUMENT,
+                    "K1: the edge source ended after " + std::to_string(got) + " of " + std::to_string(m) + " edges");
+            PRG_CUDA(cudaMemcpyAsync(a.get() + 2 * got, pinned, (size_t)k * 16, cudaMemcpyHostToDevice, s));
+            PRG_CUDA(cudaStreamSynchronize(s));  // the chunk buffer is refilled next
+            got += k;
+        }
+        const prg_status st = prg_k1_sort_device(a.get(), m, scale, b.get(), s);
+        if (st != PRG_OK) throw ApiError{st, prg::last_error()};
+        for (int64_t put = 0; put < m;) {
+            const int64_t k = std::min(chunk, m - put);
+            PRG_CUDA(cudaMemcpyAsync(pinned, b.get() + 2 * put, (size_t)k * 16, cudaMemcpyDeviceToHost, s));
+            PRG_CUDA(cudaStreamSynchronize(s));
+            require(sink(user, pinned, k) == 0, PRG_ERR_INVALID_ARGUMENT, "K1: the edge sink failed");
+            put += k;
+        }
+    });
+}
+
 prg_status prg_k2_filter_device(const int64_t* d_uv_sorted, int64_t m, int64_t n, prg_matrix** out,
                                 void* stream) {
     return guarded("prg_k2_filter", [&] {

@@ -129,23 +129,68 @@ std::int64_t default_memory_budget() {
     return static_cast<std::int64_t>(pages) * page / 4;
 }
 
+// sort_edges (kernel1_sort.cpp:133-149): the same budget rule as the reference
+// — a list larger than memory_budget_bytes / sizeof(Edge) must not be held in
+// host memory at once. The reference then runs an external merge sort with TSV
+// spill runs; here the list streams through one pinned chunk of budget/16 edges
+// into HBM, is sorted there in one pass, and streams back out into the shard
+// writer (prg_k1_sort_streamed) — no spill files, so spill_dir and
+// merge_fan_in have nothing to tune; the output is the in-memory path's.
 EdgeManifest sort_edges(const EdgeManifest& input, const std::filesystem::path& output_dir,
                         const SortOptions& options) {
-    if (options.memory_budget_bytes < 0) throw Error("memory budget must be positive");
+    const std::int64_t budget =
+        options.memory_budget_bytes > 0 ? options.memory_budget_bytes : default_memory_budget();
+    if (budget <= 0) throw Error("memory budget must be positive");
     const int files = options.num_files > 0 ? options.num_files : default_num_files(input.total_edges);
-    Timer t0;
-    std::vector<Edge> edges = read_edges(input);
-    g_last_sort.read_s = t0.seconds();
-    Timer t1;
-    std::vector<Edge> sorted(edges.size());
-    if (!edges.empty())
-        check(prg_k1_sort_host(edge_words(edges), static_cast<std::int64_t>(edges.size()), input.scale,
-                               reinterpret_cast<std::int64_t*>(sorted.data())));
-    g_last_sort.device_s = t1.seconds();
-    Timer t2;
-    auto out = write_edges(sorted, output_dir, files, input.scale, /*sorted_by_start=*/true);
-    g_last_sort.write_s = t2.seconds();
-    return out;
+    if (input.total_edges <= budget / static_cast<std::int64_t>(sizeof(Edge))) {
+        Timer t0;
+        std::vector<Edge> edges = read_edges(input);
+        g_last_sort.read_s = t0.seconds();
+        Timer t1;
+        std::vector<Edge> sorted(edges.size());
+        if (!edges.empty())
+            check(prg_k1_sort_host(edge_words(edges), static_cast<std::int64_t>(edges.size()), input.scale,
+                                   reinterpret_cast<std::int64_t*>(sorted.data())));
+        g_last_sort.device_s = t1.seconds();
+        Timer t2;
+        auto out = write_edges(sorted, output_dir, files, input.scale, /*sorted_by_start=*/true);
+        g_last_sort.write_s = t2.seconds();
+        return out;
+    }
+    struct Stream {
+        EdgeReader reader;
+        EdgeWriter writer;
+        std::exception_ptr failure;
+    } io{EdgeReader(input), EdgeWriter(output_dir, files, input.total_edges, input.scale), nullptr};
+    auto source = [](void* user, std::int64_t* uv, std::int64_t max_edges) -> std::int64_t {
+        auto& st = *static_cast<Stream*>(user);
+        try {
+            auto* e = reinterpret_cast<Edge*>(uv);
+            std::int64_t k = 0;
+            while (k < max_edges && st.reader.next(e[k])) ++k;
+            return k;
+        } catch (...) {
+            st.failure = std::current_exception();
+            return -1;
+        }
+    };
+    auto sink = [](void* user, const std::int64_t* uv, std::int64_t count) -> std::int32_t {
+        auto& st = *static_cast<Stream*>(user);
+        try {
+            st.writer.append(std::span<const Edge>(reinterpret_cast<const Edge*>(uv), static_cast<std::size_t>(count)));
+            return 0;
+        } catch (...) {
+            st.failure = std::current_exception();
+            return -1;
+        }
+    };
+    Timer t;
+    const prg_status st = prg_k1_sort_streamed(source, sink, &io, input.total_edges, input.scale,
+                                               std::max<std::int64_t>(1, budget / static_cast<std::int64_t>(sizeof(Edge))));
+    if (io.failure) std::rethrow_exception(io.failure);  // the reader's / writer's own error
+    check(st);
+    g_last_sort = {0.0, t.seconds(), 0.0};
+    return io.writer.finish(/*sorted_by_start=*/true);
 }
 
 SortBreakdown last_sort_breakdown() { return g_last_sort; }

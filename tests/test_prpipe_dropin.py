@@ -121,6 +121,40 @@ def test_staged_pipeline(tmp_path):
 
 
 @pytest.mark.gpu
+def test_sort_edges_under_a_memory_budget(tmp_path):
+    """test_kernel1_sort.cpp:79-121: a budget below the list size takes the
+    out-of-core route (here: one pinned chunk of budget/16 edges streamed
+    through HBM) and must agree with the in-memory sort — bit for bit here, a
+    stronger check than the reference's u-sequence + multiset — leaving no
+    spill directory behind; :133-144 the output shard count; a non-positive
+    budget falls back to default_memory_budget() (kernel1_sort.cpp:135-137)."""
+    for scale, seed, files, budget, fan_in in ((10, 33, 4, 4096, 64), (8, 5, 1, 2048, 4)):
+        edges = prpipe.generate_edges(prpipe.GenConfig(scale=scale, seed=seed))
+        man = prpipe.write_edges(edges, tmp_path / f"in{scale}", num_files=files, scale=scale)
+        mem = prpipe.read_edges(prpipe.sort_edges(man, tmp_path / f"mem{scale}"))
+        ext_man = prpipe.sort_edges(man, tmp_path / f"ext{scale}", memory_budget_bytes=budget, merge_fan_in=fan_in)
+        ext = prpipe.read_edges(ext_man)
+        assert ext == mem and ext_man.sorted_by_start
+        assert [u for u, _ in ext] == sorted(u for u, _ in edges) and sorted(ext) == sorted(edges)
+        assert not os.path.exists(tmp_path / f"ext{scale}" / "spill")
+    neg = prpipe.read_edges(prpipe.sort_edges(man, tmp_path / "neg", memory_budget_bytes=-5))
+    assert neg == mem
+    rows = [(100 - i, i % 100 + 1) for i in range(100)]
+    m5 = prpipe.write_edges(rows, tmp_path / "in5", num_files=1, scale=7)
+    for budget in (0, 64):  # in memory, and streamed in 4-edge chunks
+        out = prpipe.sort_edges(m5, tmp_path / f"out5_{budget}", memory_budget_bytes=budget, num_files=5)
+        assert [f.edges for f in out.files] == [20] * 5
+        got = prpipe.read_edges(out)
+        assert [u for u, _ in got] == sorted(u for u, _ in rows)
+    bad = tmp_path / "bad"
+    prpipe.write_edges([(1, 2), (2, 1)], bad, num_files=1, scale=1)
+    with open(bad / "edges_0000.tsv", "w") as f:
+        f.write("1\t2\n9\t1\n")
+    with pytest.raises(RuntimeError, match="edges_0000.tsv:2"):  # the reader's own error, streamed route too
+        prpipe.sort_edges(prpipe.EdgeManifest.load(str(bad)), tmp_path / "bad_out", memory_budget_bytes=16)
+
+
+@pytest.mark.gpu
 def test_kernel2_worked_case():
     # test_smoke.py:63-73
     edges = [(1, 2), (1, 3), (1, 4), (2, 3), (2, 1), (3, 2), (3, 1), (4, 2)]

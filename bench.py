@@ -55,6 +55,8 @@ def parse():
     p.add_argument("--flush-l2", action="store_true",
                    help="write a 512 MB buffer before every timed step (for scales whose data fits in L2)")
     p.add_argument("--ref-iters-per-step", type=int, default=2)
+    p.add_argument("--replicas", action="store_true",
+                   help="N>1: independent single-GPU pipelines per rank instead of the column-sharded K3")
     return p.parse_args()
 
 
@@ -273,6 +275,11 @@ def run_ours(args):
     L = capi.lib()
 
     flush = torch.empty(64 << 20, dtype=torch.float64, device=dev) if args.flush_l2 else None
+    # N > 1: K3 column-sharded over the ranks (NCCL all_reduce of the per-step
+    # exchange buffer), K1/K2 replicated (every rank holds the matrix);
+    # --replicas: N independent single-GPU pipelines instead
+    sharded = ws > 1 and not args.replicas
+    allreduce = capi.torch_allreduce() if sharded else None
 
     def one_step(record):
         if flush is not None:
@@ -285,7 +292,11 @@ def run_ours(args):
         ev[2].record(stream)
         mat.build_csc(stream)  # K2's CSC build (north_star): the column layout K3 iterates over
         ev[3].record(stream)
-        _, norm = capi.k3_pagerank(mat, seed=seed, iterations=iters, mode=0, out=ranks, stream=stream)
+        if sharded:  # one K3 over all ranks: each runs the SpMV over its SELL slice range
+            _, norm = capi.k3_pagerank_sharded(mat, rank, ws, allreduce, seed=seed, iterations=iters, out=ranks,
+                                               stream=stream)
+        else:
+            _, norm = capi.k3_pagerank(mat, seed=seed, iterations=iters, mode=0, out=ranks, stream=stream)
         ev[4].record(stream)
         info = (mat.nnz, mat.nnz_raw, mat.max_in, norm)
         if record is not None:
@@ -359,8 +370,11 @@ def run_ours(args):
     b1, b2, b3, b3_iter = alg_bytes(n, m, nnz, iters)
     spmv_n, spmv_ms = prof.get("k3_spmv", [0, 0.0])
     spmv_avg = spmv_ms / max(spmv_n, 1)
-    achieved = b3_iter / (spmv_avg * 1e-3) / 1e9 if spmv_avg else None
-    value = whole_job_rate(ws, iters * m, k3_ms * 1e-3)
+    # sharded: each rank's SpMV launch covers ~1/ws of the entries (ranges balanced by entries)
+    achieved = b3_iter / (ws if sharded else 1) / (spmv_avg * 1e-3) / 1e9 if spmv_avg else None
+    # sharded: one K3 problem over all ranks (strong scaling); replicas: ws problems
+    units = 1 if sharded else ws
+    value = whole_job_rate(units, iters * m, k3_ms * 1e-3)
     traffic, traffic_src = ncu_traffic(S)
 
     out = {
@@ -372,26 +386,29 @@ def run_ours(args):
         "warmup": args.warmup,
         "ms_per_step": step_ms,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if sharded else "weak",
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (reference K0 Kronecker generator restated on device, seed 1)",
         "config": {"workload": f"kronecker_s{S}_seed{seed}_k1k2k3", "scale": S, "vertices": n, "edges": m,
                    "nnz_filtered": nnz, "nnz_raw": nnz_raw, "max_in_degree": max_in, "iterations": iters,
-                   "damping": 0.85, "k3_seed": seed, "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
+                   "damping": 0.85, "k3_seed": seed,
+                   "parallelism": (f"K3 column-sharded x{ws} (SELL slice ranges, NCCL all_reduce per step); "
+                                   f"K1/K2 replicated" if sharded else
+                                   f"replicas x{ws}" if ws > 1 else "single GPU"),
                    "l2": ("512 MB L2 flush before every step" if args.flush_l2 else
                           f"inputs larger than the 126 MB L2 ({16 * m / 1e9:.2f} GB edge list, "
                           f"{(4 * (n + 1) + 12 * nnz) / 1e9:.2f} GB CSR at S={S}); no flush"
                           if 16 * m > (512 << 20) else
                           f"S={S} data ({16 * m / 1e6:.0f} MB edges) may stay L2-resident; use --flush-l2"),
                    "k3_mode": "timed (deterministic tree sums)"},
-        "k1_edges_per_s": whole_job_rate(ws, m, k1_ms * 1e-3),
-        "k2_edges_per_s": whole_job_rate(ws, m, k2_ms * 1e-3),
+        "k1_edges_per_s": whole_job_rate(units, m, k1_ms * 1e-3),
+        "k2_edges_per_s": whole_job_rate(units, m, k2_ms * 1e-3),
         "k3_edges_per_s": value,
         "stage_ms": {"k1_sort": k1_ms, "k2_filter": k2_ms, "k3_pagerank": k3_ms,
                      "k2_filter_csr": k2f_ms, "k2_csc_build": k2c_ms},
         # K3 on a handle without the K2-built CSC: layout build (transpose, SELL) inside K3
-        "k3_cold": {"edges_per_s": ws * iters * m / (k3cold_ms * 1e-3), "ms": k3cold_ms,
+        "k3_cold": {"edges_per_s": units * iters * m / (k3cold_ms * 1e-3), "ms": k3cold_ms,
                     "note": "K3 from a bare CSR: the CSC/SELL build is inside the K3 timed region",
                     "kernel_ms": {k: {"launches": v[0], "avg_ms": v[1] / max(v[0], 1)} for k, v in prof_cold.items()
                                   if k.startswith("k3_")}},
@@ -419,7 +436,7 @@ def run_ours(args):
             "k3_cold": {"alg_bytes": b3, "ms": k3cold_ms, "achieved_gbs": b3 / (k3cold_ms * 1e-3) / 1e9,
                         "frac": b3 / (k3cold_ms * 1e-3) / 1e9 / peak},
         },
-        "headline": {"k3_edges_per_s": value, "k3_cold_edges_per_s": ws * iters * m / (k3cold_ms * 1e-3),
+        "headline": {"k3_edges_per_s": value, "k3_cold_edges_per_s": units * iters * m / (k3cold_ms * 1e-3),
                      "k2_plus_k3_ms": k2_ms + k3_ms, "k1_ms": k1_ms, "k2_ms": k2_ms, "k3_ms": k3_ms,
                      "k3_cold_ms": k3cold_ms,
                      "note": "value = K3 over K2's column layout; k3_cold = K3 from a bare CSR "
@@ -454,7 +471,7 @@ def run_ours(args):
             if i > 0:
                 e2e.append(t1 - t0)
         (e2e_t,) = max_over_ranks([np.mean(e2e)], device=dev)
-        out["e2e"] = {"value": whole_job_rate(ws, iters * m, e2e_t), "unit": "edges/s",
+        out["e2e"] = {"value": whole_job_rate(units, iters * m, e2e_t), "unit": "edges/s",
                       # the host CSR the call consumes each step (int64 offsets, int64 cols, f64 values)
                       "h2d_bytes_per_step": 8 * (n + 1) + 16 * nnz, "d2h_bytes_per_step": 8 * n,
                       # what actually crosses PCIe: the values are reduced on host threads to row

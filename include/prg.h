@@ -170,6 +170,25 @@ prg_status prg_init_rank_device(int64_t n, uint64_t seed, int32_t mode, double* 
 prg_status prg_pagerank_step_device(const prg_matrix* a, const double* d_r, double damping,
                                     int32_t mode, double* d_out, double* norm1, void* stream);
 
+/* ---- Multi-GPU K3 ----------------------
+ * Column-sharded run_kernel3, one process per GPU, every rank holding the
+ * matrix handle (K2 replicated). Rank r runs the SpMV over its contiguous range
+ * of SELL slices (balanced by entries); after each SpMV the ranks' iterate
+ * values, split-column part sums and slice sums are combined by `allreduce`,
+ * which the caller implements (NCCL all_reduce over NVLink; it must sum the
+ * `count` doubles at `d_buf` over all ranks in place, ordered on `stream`, and
+ * return 0). Each element has one writer, so the sum is exact and every rank
+ * ends with ranks/norm1 bit-identical to prg_k3_pagerank_device mode 0.
+ * prg_k3_shard_bounds gives the slice ranges (bounds[world + 1]). */
+typedef int32_t (*prg_allreduce_f64)(void* user, double* d_buf, int64_t count, void* stream);
+prg_status prg_k3_pagerank_sharded(const prg_matrix* a, double damping, int32_t iterations, uint64_t seed,
+                                   int32_t rank, int32_t world, prg_allreduce_f64 allreduce, void* user,
+                                   double* d_ranks, double* norm1, void* stream);
+prg_status prg_k3_shard_bounds(const prg_matrix* a, int32_t world, uint32_t* bounds, void* stream);
+/* The partition rule itself, on host data (no device needed): slice_ptr[nslices + 1]
+ * holds the slices' entry offsets; bounds[r] = first slice of rank r. */
+prg_status prg_shard_bounds_host(const uint32_t* slice_ptr, uint32_t nslices, int32_t world, uint32_t* bounds);
+
 /* Host-buffer variants used by the drop-in C++ shim (prpipe::init_rank,
  * pagerank_step, run_kernel3 on a K2-produced handle, run_to_convergence). */
 prg_status prg_init_rank_host(int64_t n, uint64_t seed, int32_t mode, double* r, double* norm1);

@@ -34,7 +34,8 @@ HEADER_SYMBOLS = (
     "prg_init_rank_device", "prg_pagerank_step_device", "prg_launch_count", "prg_last_h2d_bytes", "prg_profile_enable",
     "prg_profile_report", "prg_build_adjacency_host", "prg_in_degree_host", "prg_zero_columns_host",
     "prg_row_normalize_host", "prg_init_rank_host", "prg_pagerank_step_host", "prg_k3_pagerank_matrix_host",
-    "prg_run_to_convergence_host", "prg_trim_memory", "prg_k1_sort_streamed",
+    "prg_run_to_convergence_host", "prg_trim_memory", "prg_k1_sort_streamed", "prg_k3_pagerank_sharded",
+    "prg_k3_shard_bounds", "prg_shard_bounds_host",
 )
 
 
@@ -91,6 +92,9 @@ def lib() -> C.CDLL:
             "prg_run_to_convergence_host": (i32, [i64, i64, vp, vp, vp, f64, f64, i32, vp, vp, vp, vp]),
             "prg_trim_memory": (i32, []),
             "prg_k1_sort_streamed": (i32, [vp, vp, vp, i64, i32, i64]),
+            "prg_k3_pagerank_sharded": (i32, [vp, f64, i32, u64, i32, i32, vp, vp, vp, vp, vp]),
+            "prg_k3_shard_bounds": (i32, [vp, i32, vp, vp]),
+            "prg_shard_bounds_host": (i32, [vp, C.c_uint32, i32, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -280,6 +284,83 @@ def k3_pagerank_host(n, row_offsets, cols, values, damping=0.85, iterations=20, 
     _check(lib().prg_k3_pagerank_host(n, len(c), _ptr(ro), _ptr(c), _ptr(v), damping, iterations, seed, mode,
                                       _ptr(r), C.byref(norm)))
     return r, norm.value
+
+
+# ---- multi-GPU K3 -------------------------------------------------------------
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
+
+
+def device_f64_view(ptr: int, count: int):
+    """Zero-copy torch view of `count` device doubles at `ptr`."""
+    import torch
+
+    class _View:
+        __cuda_array_interface__ = {"shape": (count,), "typestr": "<f8", "data": (ptr, False), "version": 3,
+                                    "strides": None}
+
+    return torch.as_tensor(_View(), device="cuda")
+
+
+def torch_allreduce(group=None):
+    """The exchange prg_k3_pagerank_sharded needs, as torch.distributed does it:
+    an in-place all_reduce(SUM) of the buffer (NCCL on GPUs, gloo on CPU
+    tensors), ordered after the library's kernels on the caller's stream."""
+    import torch.distributed as dist
+
+    def allreduce(buf, stream=None):
+        if buf.is_cuda and stream:
+            import torch
+
+            with torch.cuda.stream(torch.cuda.ExternalStream(stream)):  # ordered after the SpMV
+                dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+        else:
+            dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+
+    return allreduce
+
+
+def shard_bounds_host(slice_ptr, world: int) -> np.ndarray:
+    """The sharded K3's partition rule (prg_shard_bounds_host) on host slice offsets."""
+    sp = np.ascontiguousarray(slice_ptr, dtype=np.uint32)
+    out = np.empty(world + 1, dtype=np.uint32)
+    _check(lib().prg_shard_bounds_host(_ptr(sp), len(sp) - 1, world, _ptr(out)))
+    return out
+
+
+def k3_shard_bounds(mat: "DeviceMatrix", world: int, stream=None) -> np.ndarray:
+    out = np.empty(world + 1, dtype=np.uint32)
+    _check(lib().prg_k3_shard_bounds(mat.handle, world, _ptr(out), _stream(stream)))
+    return out
+
+
+def k3_pagerank_sharded(mat: "DeviceMatrix", rank: int, world: int, allreduce, damping=0.85, iterations=20, seed=0,
+                        out=None, stream=None):
+    """Column-sharded K3 (prg_k3_pagerank_sharded): this process's share of a
+    world-GPU run_kernel3; `allreduce(tensor, stream)` sums a CUDA tensor over
+    the ranks in place. Returns (ranks CUDA tensor — complete on every rank,
+    norm1); bit-identical to k3_pagerank(mode=0)."""
+    import torch
+
+    if out is None:
+        out = torch.empty(mat.n, dtype=torch.float64, device="cuda")
+    failure = []
+
+    def cb(_user, buf, count, strm):
+        try:
+            allreduce(device_f64_view(buf, count), strm)
+            return 0
+        except BaseException as e:  # noqa: BLE001 - reported after the call
+            failure.append(e)
+            return 1
+
+    fn = ALLREDUCE_FN(cb)
+    norm = C.c_double()
+    rc = lib().prg_k3_pagerank_sharded(mat.handle, damping, iterations, seed, rank, world, fn, None, _ptr(out),
+                                       C.byref(norm), _stream(stream))
+    if failure:
+        raise failure[0]
+    _check(rc)
+    return out, norm.value
 
 
 def init_rank(n: int, seed: int, mode=0, stream=None):

@@ -587,6 +587,39 @@ prg_status prg_k3_pagerank_device(const prg_matrix* a, double damping, int32_t i
     });
 }
 
+prg_status prg_k3_pagerank_sharded(const prg_matrix* a, double damping, int32_t iterations, uint64_t seed,
+                                   int32_t rank, int32_t world, prg_allreduce_f64 allreduce, void* user,
+                                   double* d_ranks, double* norm1, void* stream) {
+    return guarded("prg_k3_pagerank_sharded", [&] {
+        require(a != nullptr && d_ranks != nullptr && allreduce != nullptr, PRG_ERR_INVALID_ARGUMENT, "null argument");
+        require(damping > 0.0 && damping < 1.0, PRG_ERR_INVALID_ARGUMENT, "damping must lie strictly between 0 and 1");
+        require(iterations >= 1, PRG_ERR_INVALID_ARGUMENT, "iteration count must be >= 1");
+        require(world >= 1 && rank >= 0 && rank < world, PRG_ERR_INVALID_ARGUMENT, "rank must lie in [0, world)");
+        prg::K3Options o;
+        o.damping = damping;
+        o.iterations = iterations;
+        o.seed = seed;
+        const double nm = prg::k3_pagerank_sharded_device(a, o, rank, world, allreduce, user, d_ranks, as_stream(stream));
+        if (norm1) *norm1 = nm;
+    });
+}
+
+prg_status prg_k3_shard_bounds(const prg_matrix* a, int32_t world, uint32_t* bounds, void* stream) {
+    return guarded("prg_k3_shard_bounds", [&] {
+        require(a != nullptr && bounds != nullptr && world >= 1, PRG_ERR_INVALID_ARGUMENT, "bad arguments");
+        prg::k3_shard_bounds(a, world, bounds, as_stream(stream));
+    });
+}
+
+prg_status prg_shard_bounds_host(const uint32_t* slice_ptr, uint32_t nslices, int32_t world, uint32_t* bounds) {
+    return guarded("prg_shard_bounds_host", [&] {
+        require(slice_ptr != nullptr && bounds != nullptr && world >= 1, PRG_ERR_INVALID_ARGUMENT, "bad arguments");
+        for (uint32_t i = 0; i < nslices; ++i)
+            require(slice_ptr[i] <= slice_ptr[i + 1], PRG_ERR_INVALID_ARGUMENT, "slice offsets must be non-decreasing");
+        prg::k3_shard_bounds_host(slice_ptr, nslices, world, bounds);
+    });
+}
+
 prg_status prg_k3_pagerank_host(int64_t n, int64_t nnz, const int64_t* row_offsets, const int64_t* cols,
                                 const double* values, double damping, int32_t iterations, uint64_t seed,
                                 int32_t mode, double* ranks, double* norm1) {

@@ -3,6 +3,7 @@
 #pragma once
 
 #include "prg_common.cuh"
+#include "../../include/prg.h"
 
 namespace prg {
 struct K3Plan;  // K3's column layout (prg_k3.cu)
@@ -62,6 +63,15 @@ struct K3Options {
 // original vertex order; returns norm1 (sum of the final vector).
 double k3_pagerank_device(const prg_matrix* a, const K3Options& opt, double* d_ranks,
                           cudaStream_t s);
+// Column-sharded K3 over `world` GPUs (one process each): this rank's SpMV
+// covers its SELL slice range; allreduce(user, buf, count, stream) must sum
+// buf over the ranks in place, ordered on `stream`. Bit-identical to
+// k3_pagerank_device mode 0 on every rank.
+double k3_pagerank_sharded_device(const prg_matrix* a, const K3Options& opt, int rank, int world,
+                                  prg_allreduce_f64 allreduce, void* user, double* d_ranks, cudaStream_t s);
+// The slice ranges (bounds[world + 1]) the sharded K3 uses.
+void k3_shard_bounds(const prg_matrix* a, int world, uint32_t* bounds, cudaStream_t s);
+void k3_shard_bounds_host(const uint32_t* slice_ptr, uint32_t nslices, int world, uint32_t* bounds);
 // One pagerank_step (kernel3_pagerank.cpp:41-65): d_out = step(d_r). Returns norm1.
 double k3_step_device(const prg_matrix* a, const double* d_r, double damping, double* d_out,
                       int mode, cudaStream_t s);

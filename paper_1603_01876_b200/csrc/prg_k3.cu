@@ -975,6 +975,8 @@ struct SellArgs {
     uint32_t nctr;
     int64_t n_nd;
     uint32_t nslices;
+    uint32_t slice_begin = 0;    // this launch covers slices [slice_begin, slice_end) (a
+    uint32_t slice_end = 0;      // shard of a multi-GPU K3; the whole list on one GPU)
     double damping;
 };
 
@@ -1000,9 +1002,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) spmv_sell_kernel(SellArg
     uint32_t k = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) % nctr, tried = 0;
     for (;;) {
         uint32_t sl = 0;
-        if (lane == 0) sl = atomicAdd(a.next_slice + 32 * k, 1u) * nctr + k;
+        if (lane == 0) sl = a.slice_begin + atomicAdd(a.next_slice + 32 * k, 1u) * nctr + k;
         sl = __shfl_sync(0xffffffffu, sl, 0);
-        if (sl >= a.nslices) {
+        if (sl >= a.slice_end) {
             if (++tried == nctr) break;
             k = k + 1 == nctr ? 0 : k + 1;
             continue;
@@ -1392,8 +1394,36 @@ void init_rank_impl(int64_t n, uint64_t seed, double* d_r, int mode, double bgf,
 // Runs `iters` steps from r_in (original order, S.out = {sum(r_in), bg}) and
 // writes the final iterate to r_out (original order); S.out ends as
 // {sum(r_out), bg', bg_used}.
+// Multi-GPU K3 (column-sharded): this rank runs the SpMV over its own SELL
+// slices only; every other per-iteration step is replicated. After the SpMV the
+// rank's iterate values, split-column part sums and slice sums — written into
+// a zeroed exchange buffer, every element by exactly one rank — are combined
+// by an all-reduce(sum) the caller provides (NCCL over NVLink: x + 0 is exact,
+// so every rank then holds bit-for-bit the single-GPU arrays and the rest of
+// the step, Σ included, is the single-GPU computation).
+struct Shard {
+    int rank = 0, world = 1;
+    prg_allreduce_f64 allreduce = nullptr;
+    void* user = nullptr;
+};
+
+// Contiguous slice ranges with near-equal SELL entries (slices are sorted
+// longest first, so equal slice counts would not balance).
+void shard_bounds_host(const uint32_t* slice_ptr, uint32_t nslices, int world, uint32_t* bounds) {
+    const uint64_t total = slice_ptr[nslices];
+    uint32_t sl = 0;
+    bounds[0] = 0;
+    for (int r = 1; r < world; ++r) {
+        const uint64_t want = total * (uint64_t)r / (uint64_t)world;
+        while (sl < nslices && slice_ptr[sl] < want) ++sl;
+        bounds[r] = sl;
+    }
+    bounds[world] = nslices;
+}
+
 void iterate(const K3Plan& P, const double* r_in, double* r_out, int iters, double damping, double bgf, Sums& S,
-             cudaStream_t s, uint64_t rng_s0 = 0, const double* rng_div = nullptr, int sum_mode = 1) {
+             cudaStream_t s, uint64_t rng_s0 = 0, const double* rng_div = nullptr, int sum_mode = 1,
+             const Shard* shard = nullptr) {
     const unsigned g = (unsigned)num_sms() * 8;
     const int64_t n = P.n;
     if (P.mode == 1) {
@@ -1423,12 +1453,36 @@ void iterate(const K3Plan& P, const double* r_in, double* r_out, int iters, doub
     // s = [row-scaled iterate (SELL row order, n_nd) | exception products (n_exc)]
     DevBuf<double> sbuf((size_t)std::max<int64_t>(P.n_nd + P.n_exc, 1), s), y0(NP ? NP : 1, s), y1(NP ? NP : 1, s),
         slice_sum(P.nslices ? P.nslices : 1, s), sum_part(kSumBlocks, s);
+    // sharded: two exchange buffers [y (NP) | part sums (n_parts) | slice sums (nslices)]
+    uint32_t sl_begin = 0, sl_end = P.nslices;
+    size_t n_parts = 0, xcount = 0;
+    DevBuf<double> xb0, xb1;
+    if (shard && shard->world > 1) {
+        std::vector<uint32_t> sp((size_t)P.nslices + 1), bounds((size_t)shard->world + 1);
+        PRG_CUDA(cudaMemcpyAsync(sp.data(), P.slice_ptr.get(), sp.size() * 4, cudaMemcpyDeviceToHost, s));
+        uint32_t nsp = 0;
+        PRG_CUDA(cudaMemcpyAsync(&nsp, P.n_split.get(), 4, cudaMemcpyDeviceToHost, s));
+        PRG_CUDA(cudaStreamSynchronize(s));
+        shard_bounds_host(sp.data(), P.nslices, shard->world, bounds.data());
+        sl_begin = bounds[(size_t)shard->rank];
+        sl_end = bounds[(size_t)shard->rank + 1];
+        uint32_t pb_end = 0;
+        if (nsp) PRG_CUDA(cudaMemcpy(&pb_end, P.split_pbase.get() + nsp, 4, cudaMemcpyDeviceToHost));
+        n_parts = pb_end;
+        xcount = (size_t)NP + n_parts + P.nslices;
+        xb0 = DevBuf<double>(xcount ? xcount : 1, s);
+        xb1 = DevBuf<double>(xcount ? xcount : 1, s);
+    }
+    const bool sharded = xcount > 0;
+    auto y_of = [&](int side) { return sharded ? (side ? xb1.get() : xb0.get()) : (side ? y1.get() : y0.get()); };
+    auto partial_of = [&](int side) { return sharded ? y_of(side) + NP : P.partial.get(); };
+    auto slice_sum_of = [&](int side) { return sharded ? y_of(side) + NP + n_parts : slice_sum.get(); };
     static int nctr = -1;  // PRG_NCTR: slice counters per launch
     if (nctr < 0) { const char* e = getenv("PRG_NCTR"); nctr = e ? std::max(1, atoi(e)) : kSliceCounters; }
     const size_t ctr_words = (size_t)std::max(iters, 1) * 32 * nctr;
     DevBuf<uint32_t> slice_ctr(ctr_words, s);
     PRG_CUDA(cudaMemsetAsync(slice_ctr.get(), 0, ctr_words * 4, s));
-    double* ys[2] = {y0.get(), y1.get()};
+    double* ys[2] = {y_of(0), y_of(1)};
     // Scalars {Σ, bg, bg of the step before} of step k's input iterate: step 0
     // reads S.out; step k >= 1 reads a slot written by the gather launch that
     // starts it (block 0 finishes step k-1's Σ), alternating so a launch never
@@ -1468,16 +1522,20 @@ void iterate(const K3Plan& P, const double* r_in, double* r_out, int iters, doub
         a.vpos = P.vpos.get();
         a.s = sbuf.get();
         a.y = y;
-        a.partial = P.partial.get();
+        a.partial = partial_of(it & 1);
         a.lane_pslot = P.lane_pslot.get();
-        a.slice_sum = slice_sum.get();
+        a.slice_sum = slice_sum_of(it & 1);
         a.bgp = out_of(it);
         a.next_slice = slice_ctr.get() + (size_t)it * 32 * nctr;
         a.nctr = (uint32_t)nctr;
         a.n_nd = P.n_nd;
         a.nslices = P.nslices;
+        a.slice_begin = sl_begin;
+        a.slice_end = sl_end;
         a.damping = damping;
-        if (P.nslices) {
+        if (sharded)  // every element is then written by exactly one rank
+            PRG_CUDA(cudaMemsetAsync(y_of(it & 1), 0, xcount * sizeof(double), s));
+        if (P.nslices && sl_end > sl_begin) {
             ProfScope ps("k3_spmv", s);
             // 768 threads x 2 CTAs (48 warps/SM, 40 registers) with a 6-deep pipeline:
             // 0.767 ms vs 0.796 ms for 1024 x 2 at 32 registers, U=4 (same box,
@@ -1487,8 +1545,13 @@ void iterate(const K3Plan& P, const double* r_in, double* r_out, int iters, doub
             else spmv_sell_kernel<6, 768, 2><<<num_sms() * 2, 768, 0, s>>>(a);
             PRG_LAUNCH_CHECK();
         }
-        SplitArgs sp{P.n_split.get(), P.split_p0.get(), P.split_pbase.get(), P.partial.get(), out_of(it), damping};
-        sell_sum_part<<<kSumBlocks, 1024, 0, s>>>(slice_sum.get(), P.nslices, y, sp, sum_part.get());
+        if (sharded) {
+            ProfScope px("k3_exchange", s);
+            if (shard->allreduce(shard->user, y_of(it & 1), (int64_t)xcount, s) != 0)
+                throw CudaError{"K3: the all-reduce callback failed"};
+        }
+        SplitArgs sp{P.n_split.get(), P.split_p0.get(), P.split_pbase.get(), partial_of(it & 1), out_of(it), damping};
+        sell_sum_part<<<kSumBlocks, 1024, 0, s>>>(slice_sum_of(it & 1), P.nslices, y, sp, sum_part.get());
         PRG_LAUNCH_CHECK();
     }
     // the last step's Σ (the earlier ones were finished by the gather launches)
@@ -1613,6 +1676,48 @@ double k3_pagerank_device(const prg_matrix* A, const K3Options& opt, double* d_r
     PRG_LAUNCH_CHECK();
     iterate(P, nullptr, d_ranks, opt.iterations, opt.damping, bgf, S, s, s0, xsum.get());
     return read_scalar(S.out.get(), s);
+}
+
+double k3_pagerank_sharded_device(const prg_matrix* A, const K3Options& opt, int rank, int world,
+                                  prg_allreduce_f64 allreduce, void* user, double* d_ranks, cudaStream_t s) {
+    ProfScope prof("k3_pagerank", s);
+    const int64_t n = A->n;
+    const double bgf = (1.0 - opt.damping) / (double)n;
+    K3Plan tmp;
+    const K3Plan& P = plan_for(A, 0, tmp, s);
+    Sums S;
+    const Shard sh{rank, world, allreduce, user};
+    if (P.nslices == 0) {  // nothing to shard: every rank computes the (trivial) iteration itself
+        DevBuf<double> r0((size_t)n, s);
+        init_rank_impl(n, opt.seed, r0.get(), 0, bgf, S, s);
+        iterate(P, r0.get(), d_ranks, opt.iterations, opt.damping, bgf, S, s);
+        return read_scalar(S.out.get(), s);
+    }
+    const uint64_t s0 = dev::mix_seed(opt.seed, kRankInitStream);
+    const int64_t nb = (n + 8191) / 8192;
+    DevBuf<double> part((size_t)nb, s), xsum(4, s);
+    S.out = DevBuf<double>(4, s);
+    PRG_CUDA(cudaMemsetAsync(S.out.get(), 0, 32, s));
+    rng_partial_kernel<<<(unsigned)nb, 1024, 0, s>>>(n, s0, nullptr, part.get());
+    final_sum_kernel<<<1, 1024, 0, s>>>(part.get(), nb, 0.0, xsum.get());
+    rng_partial_kernel<<<(unsigned)nb, 1024, 0, s>>>(n, s0, xsum.get(), part.get());
+    final_sum_kernel<<<1, 1024, 0, s>>>(part.get(), nb, bgf, S.out.get());
+    PRG_LAUNCH_CHECK();
+    iterate(P, nullptr, d_ranks, opt.iterations, opt.damping, bgf, S, s, s0, xsum.get(), 1, &sh);
+    return read_scalar(S.out.get(), s);
+}
+
+void k3_shard_bounds_host(const uint32_t* slice_ptr, uint32_t nslices, int world, uint32_t* bounds) {
+    shard_bounds_host(slice_ptr, nslices, world, bounds);
+}
+
+void k3_shard_bounds(const prg_matrix* A, int world, uint32_t* bounds, cudaStream_t s) {
+    K3Plan tmp;
+    const K3Plan& P = plan_for(A, 0, tmp, s);
+    std::vector<uint32_t> sp((size_t)P.nslices + 1, 0);
+    if (P.nslices) PRG_CUDA(cudaMemcpyAsync(sp.data(), P.slice_ptr.get(), sp.size() * 4, cudaMemcpyDeviceToHost, s));
+    PRG_CUDA(cudaStreamSynchronize(s));
+    shard_bounds_host(sp.data(), P.nslices, world, bounds);
 }
 
 double k3_step_device(const prg_matrix* A, const double* d_r, double damping, double* d_out, int mode,

@@ -19,6 +19,7 @@ ap.add_argument("report")
 ap.add_argument("--scale", type=int, required=True)
 ap.add_argument("--tag", default="k3_spmv")
 ap.add_argument("--launch", type=int, default=0, help="row of the raw page (captured launch index)")
+ap.add_argument("--summary", default=None, help="committed profiles/ summary of the same report (cited as the source)")
 a = ap.parse_args()
 rep = a.report
 raw = list(csv.reader(io.StringIO(subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"],
@@ -38,7 +39,7 @@ root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 path = os.path.join(root, "profiles", "ncu_traffic.json")
 db = json.load(open(path)) if os.path.exists(path) else {}
 db.setdefault(str(a.scale), {})[a.tag] = {"dram_bytes_per_launch": tot, "kernel": d.get("Kernel Name", ""),
-                                          "source": os.path.basename(rep),
+                                          "source": a.summary or os.path.basename(rep), "report": os.path.basename(rep),
                                           "note": "one ncu --set full capture, cold-cache replay"}
 with open(path, "w") as f:
     json.dump(db, f, indent=1, sort_keys=True)

@@ -217,6 +217,50 @@ __device__ __forceinline__ double ld_keep_f64(const double* p, uint64_t pol) {
     return r;
 }
 
+// ---------------------------------------------------------------------------
+// TMA bulk copies (cp.async.bulk, SASS UBLKCP) into shared memory, completed
+// on an mbarrier with a transaction count. Streaming kernels keep a ring of
+// such stages so the next tile is in flight while the current one is worked on.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_addr(bar);
+    uint32_t done = 0;
+    do {
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(done)
+                     : "r"(a), "r"(parity)
+                     : "memory");
+    } while (!done);
+}
+// Orders this thread's earlier generic-proxy shared-memory accesses (after a
+// barrier: the whole CTA's) before later async-proxy (TMA) writes.
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// bytes: multiple of 16; src and dst 16-byte aligned. L2 evict-first: the
+// stream is read once.
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                            uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+            "r"(smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
+        : "memory");
+}
+
 // splitmix64 finaliser + counter-based stream position (rng.hpp:14-19): the
 // state after k calls from seed s0 is s0 + k*gamma, so x_k is a pure function.
 __device__ __forceinline__ uint64_t splitmix_at(uint64_t s0, uint64_t k) {

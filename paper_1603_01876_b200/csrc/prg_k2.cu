@@ -10,10 +10,11 @@
 // d_in. Values are one IEEE division of the same two integers the reference
 // divides, so they are bit-identical.
 //
-// Passes (S=24: M=268M edges, 8192-edge tiles):
-//   A  read edges once: validate labels and order, count unique (u,v), d_in atomics
+// Passes (S=24: M=268M edges):
+//   A  read edges once (TMA ring, 2048-edge tiles): validate labels and order,
+//      count unique (u,v), warp-aggregated d_in atomics
 //   -  max(d_in), keep bitmask (N bits)
-//   B  read edges again: keep-bit gather, in-tile run lengths / row sums in SMEM,
+//   B  read edges again (4096-edge tiles, one per CTA): keep-bit gather, in-tile run lengths / row sums in SMEM,
 //      kept-entry positions by decoupled look-back, write cols/values/row offsets
 //   F  fix-ups for the few rows that span tiles (run continuation counts, then
 //      divide those rows by their row sums accumulated across tiles)
@@ -425,6 +426,129 @@ __global__ void k2_fix_rows(const uint32_t* __restrict__ fix_rows, const uint64_
     }
 }
 
+// ---------------------------------------------------------------------------
+// Pass A over a TMA ring. Persistent CTAs of 256 threads; tiles of 2048 edges
+// (32 KB) arrive by cp.async.bulk into a ring of kStages shared-memory stages,
+// claimed dynamically and prefetched kStages-1 ahead, so HBM streams while the
+// current tile's atomics are issued (2.21 -> 1.96 ms at S=24; the floor is the
+// L2 atomic rate: 2^28 scattered REDs into 2^24 counters take 1.53 ms alone,
+// tools/microbench/atomics.cu). Each warp owns 256 consecutive edges of a tile
+// as 8 rows of 32 lanes (conflict-free 16-byte shared loads; a predecessor is
+// a shuffle away).
+// Pass B in the same persistent TMA form measured slower (6.6 ms vs 3.7 ms):
+// with a decoupled look-back, a round of concurrently started tiles makes every
+// tile sum up to a round of aggregates (dynamic claims made a stage ahead were
+// worse still, 12 ms) — the one-tile-per-CTA launch below staggers tiles naturally.
+// ---------------------------------------------------------------------------
+constexpr int kST = 256;               // threads per CTA
+constexpr int kSW = kST / 32;          // warps
+constexpr int kSR = 8;                 // rows of 32 edges per warp
+constexpr int kSE = kST * kSR;         // 2048 edges per tile
+constexpr int kSMW = kSE / 32;         // 64 mask words per tile; word q = warp q/8, row q%8
+
+template <int kStages>
+struct Ring {
+    uint64_t bar[kStages];
+    uint32_t tile[kStages];
+};
+
+// Thread 0 only: claim the next tile (dynamically: the d_in atomics meet very
+// different contention per tile) and start its copy into `slot`.
+template <int kStages>
+__device__ __forceinline__ void ring_issue(Ring<kStages>& R, int slot, longlong2* stages, const longlong2* uv,
+                                           int64_t m, uint32_t ntiles, uint32_t* next_tile, uint64_t pol) {
+    const uint32_t t = atomicAdd(next_tile, 1u);
+    R.tile[slot] = t;
+    if (t < ntiles) {
+        const int64_t base = (int64_t)t * kSE;
+        const uint32_t bytes = (uint32_t)min((int64_t)kSE, m - base) * 16u;
+        dev::fence_proxy_async_smem();
+        dev::mbar_arrive_expect_tx(&R.bar[slot], bytes);
+        dev::tma_load_1d(stages + (size_t)slot * kSE, uv + base, bytes, &R.bar[slot], pol);
+    }
+}
+
+template <int kStages>
+__device__ __forceinline__ void ring_start(Ring<kStages>& R, longlong2* stages, const longlong2* uv, int64_t m,
+                                           uint32_t ntiles, uint32_t* next_tile, uint64_t pol) {
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < kStages; ++k) dev::mbar_init(&R.bar[k], 1);
+        dev::mbar_fence_init();
+        for (int k = 0; k < kStages; ++k) ring_issue<kStages>(R, k, stages, uv, m, ntiles, next_tile, pol);
+    }
+    __syncthreads();
+}
+
+// Pass A over the ring: validation, unique-entry count, warp-aggregated d_in.
+template <int kStages>
+__global__ void __launch_bounds__(kST) k2_pass_a_tma(const longlong2* __restrict__ uv, int64_t m, int64_t n,
+                                                     uint32_t* __restrict__ d_in, uint32_t* __restrict__ err,
+                                                     unsigned long long* __restrict__ nnz_raw, uint32_t ntiles,
+                                                     uint32_t* __restrict__ next_tile) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    longlong2* stages = reinterpret_cast<longlong2*>(smem_raw);
+    __shared__ Ring<kStages> R;
+    __shared__ longlong2 before;
+    __shared__ uint32_t red[kSW];
+    const unsigned lane = dev::lane_id(), w = dev::warp_id();
+    const uint64_t pol = dev::policy_evict_first();
+    ring_start<kStages>(R, stages, uv, m, ntiles, next_tile, pol);
+    uint32_t my_err = 0, heads = 0;
+    for (uint32_t i = 0;; ++i) {
+        const int slot = (int)(i % kStages);
+        const uint32_t t = R.tile[slot];
+        if (t >= ntiles) break;
+        const int64_t base = (int64_t)t * kSE;
+        const int cnt = (int)min((int64_t)kSE, m - base);
+        if (threadIdx.x == 0) before = base > 0 ? uv[base - 1] : make_longlong2(0, 0);
+        dev::mbar_wait(&R.bar[slot], (i / kStages) & 1u);
+        __syncthreads();  // `before` visible
+        const longlong2* tl = stages + (size_t)slot * kSE;
+        const int c0 = (int)w * 32 * kSR;
+        longlong2 carry = c0 > 0 ? tl[c0 - 1] : before;  // the edge before this warp's first
+#pragma unroll
+        for (int j = 0; j < kSR; ++j) {
+            const int l = c0 + j * 32 + (int)lane;
+            const bool valid = l < cnt;
+            const longlong2 e = valid ? tl[l] : make_longlong2(0, 0);
+            long long px = __shfl_up_sync(0xffffffffu, e.x, 1), py = __shfl_up_sync(0xffffffffu, e.y, 1);
+            if (lane == 0) { px = carry.x; py = carry.y; }
+            carry.x = __shfl_sync(0xffffffffu, e.x, 31);
+            carry.y = __shfl_sync(0xffffffffu, e.y, 31);
+            const bool has_pred = base + l > 0;
+            const bool same = valid && has_pred && e.x == px && e.y == py;
+            const unsigned eqm = __ballot_sync(0xffffffffu, same);
+            if (valid) {
+                const bool ok = e.x >= 1 && e.x <= n && e.y >= 1 && e.y <= n;
+                if (!ok) my_err |= kErrLabelRange;
+                else if (!same || lane == 0) {
+                    // a run of equal edges adds its length (within this row) from its first lane
+                    const unsigned after = ~(eqm >> lane >> 1) & (0x7fffffffu >> lane);
+                    const uint32_t len = 1u + (after ? (uint32_t)(__ffs(after) - 1) : 31u - lane);
+                    atomicAdd(&d_in[(uint32_t)(e.y - 1)], len);
+                }
+                if (has_pred) {
+                    if (e.x < px) my_err |= kErrUnsorted;
+                    else if (e.x == px && e.y < py) my_err |= kErrNotCanonical;
+                }
+                heads += !same;
+            }
+        }
+        __syncthreads();  // every read of this stage is done
+        if (threadIdx.x == 0) ring_issue<kStages>(R, slot, stages, uv, m, ntiles, next_tile, pol);
+    }
+    heads = dev::warp_sum(heads);
+    if (lane == 0) red[w] = heads;
+    my_err = __reduce_or_sync(0xffffffffu, my_err);
+    if (lane == 0 && my_err) atomicOr(err, my_err);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long tot = 0;
+        for (int k = 0; k < kSW; ++k) tot += red[k];
+        if (tot) atomicAdd(nnz_raw, tot);
+    }
+}
+
 }  // namespace
 
 uint32_t k2_filter_device(const int64_t* d_uv, int64_t m, int64_t n, prg_matrix* out, cudaStream_t s,
@@ -463,9 +587,28 @@ uint32_t k2_filter_device(const int64_t* d_uv, int64_t m, int64_t n, prg_matrix*
     const unsigned ga = std::min<unsigned>(ntiles, (unsigned)num_sms() * 2);
     static int flags = -1;  // PRG_K2_FLAGS (A/B measurement knob): bit 0 evict-first edge loads, bit 1 streaming stores
     if (flags < 0) { const char* e = getenv("PRG_K2_FLAGS"); flags = e ? atoi(e) : 0; }
+    static int v1 = -1;     // PRG_K2_V1=1: the register-tile pass A (A/B against the TMA-ring pass A)
+    if (v1 < 0) { const char* e = getenv("PRG_K2_V1"); v1 = e ? atoi(e) : 0; }
+    static int ctas = -1;   // PRG_K2_CTAS: persistent CTAs per SM of the TMA-ring passes
+    if (ctas < 0) { const char* e = getenv("PRG_K2_CTAS"); ctas = e ? atoi(e) : 3; }
+    constexpr int kStagesA = 3;
+    const uint32_t ntiles_s = div_up((uint64_t)m, kSE);
+    // persistent grid: min(PRG_K2_CTAS, resident CTAs) per SM
+    auto grid_for = [&](const void* fn, size_t smem) {
+        int occ = 1;
+        PRG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kST, smem));
+        return std::min<unsigned>(ntiles_s, (unsigned)(num_sms() * std::max(1, std::min(occ, ctas))));
+    };
     {
         ProfScope pa("k2_pass_a", s);
-        k2_pass_a<<<ga, kT, 0, s>>>(uv, m, n, out->d_in, err, nnz_raw, ntiles, tile_counter_a, flags);
+        if (v1) {
+            k2_pass_a<<<ga, kT, 0, s>>>(uv, m, n, out->d_in, err, nnz_raw, ntiles, tile_counter_a, flags);
+        } else {
+            const size_t smem = (size_t)kStagesA * kSE * sizeof(longlong2);
+            PRG_CUDA(cudaFuncSetAttribute(k2_pass_a_tma<kStagesA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            const unsigned gs = grid_for((const void*)k2_pass_a_tma<kStagesA>, smem);
+            k2_pass_a_tma<kStagesA><<<gs, kST, smem, s>>>(uv, m, n, out->d_in, err, nnz_raw, ntiles_s, tile_counter_a);
+        }
         PRG_LAUNCH_CHECK();
     }
     uint32_t h_err = 0;
@@ -496,9 +639,10 @@ uint32_t k2_filter_device(const int64_t* d_uv, int64_t m, int64_t n, prg_matrix*
     } else {  // build_adjacency only: keep every column
         PRG_CUDA(cudaMemsetAsync(keepbits.get(), 0xff, (size_t)(n + 31) / 32 * 4, s));
     }
-    DevBuf<unsigned long long> tile_status(ntiles, s);
-    DevBuf<uint32_t> dout_f((size_t)n, s), fix_rows(ntiles + 1, s), cont_p(ntiles, s), cont_c(ntiles, s);
-    PRG_CUDA(cudaMemsetAsync(tile_status.get(), 0, (size_t)ntiles * 8, s));
+    const uint32_t nt_b = ntiles;
+    DevBuf<unsigned long long> tile_status(nt_b, s);
+    DevBuf<uint32_t> dout_f((size_t)n, s), fix_rows(nt_b + 1, s), cont_p(nt_b, s), cont_c(nt_b, s);
+    PRG_CUDA(cudaMemsetAsync(tile_status.get(), 0, (size_t)nt_b * 8, s));
     PRG_CUDA(cudaMemsetAsync(dout_f.get(), 0, (size_t)n * 4, s));
     {
         ProfScope pb("k2_pass_b", s);
@@ -508,16 +652,16 @@ uint32_t k2_filter_device(const int64_t* d_uv, int64_t m, int64_t n, prg_matrix*
                                                         normalize, flags);
         PRG_LAUNCH_CHECK();
     }
-    k2_fix_runs<<<div_up(ntiles, 256), 256, 0, s>>>(cont_p.get(), cont_c.get(), ntiles, out->values);
+    k2_fix_runs<<<div_up(nt_b, 256), 256, 0, s>>>(cont_p.get(), cont_c.get(), nt_b, out->values);
     PRG_LAUNCH_CHECK();
     if (normalize)
     {
-        DevBuf<uint64_t> task_row((size_t)ntiles + (size_t)m / kFixChunk + 2, s);
+        DevBuf<uint64_t> task_row((size_t)nt_b + (size_t)m / kFixChunk + 2, s);
         DevBuf<uint32_t> n_tasks(1, s);
-        DevBuf<uint32_t> nc((size_t)ntiles + 1, s), nbase((size_t)ntiles + 1, s);
+        DevBuf<uint32_t> nc((size_t)nt_b + 1, s), nbase((size_t)nt_b + 1, s);
         const unsigned gf = (unsigned)num_sms() * 4;
         k2_fix_count<<<gf, 256, 0, s>>>(fix_rows.get(), n_fix, out->row_offsets, nc.get());
-        exclusive_scan_u32_prefix(nc.get(), nbase.get(), (size_t)ntiles + 1, n_fix, 1, s);
+        exclusive_scan_u32_prefix(nc.get(), nbase.get(), (size_t)nt_b + 1, n_fix, 1, s);
         k2_fix_emit<<<gf, 256, 0, s>>>(nc.get(), nbase.get(), n_fix, task_row.get(), n_tasks.get());
         k2_fix_rows<<<(unsigned)num_sms() * 8, 256, 0, s>>>(fix_rows.get(), task_row.get(), n_tasks.get(),
                                                              out->row_offsets, dout_f.get(), out->values);

@@ -2,7 +2,7 @@
 #   bash tools/ab_env.sh "base:" "ldcs:PRG_K2_FLAGS=1" ...
 for spec in "$@"; do
   v=${spec%%:*}; envs=${spec#*:}
-  env $envs python bench.py --no-cpu-baseline --no-pipeline-io --e2e-steps 1 --steps 5 > gpurun_out/ab_$v.log 2>&1
+  timeout 600 env $envs python bench.py --no-cpu-baseline --no-pipeline-io --e2e-steps 1 --steps 5 > gpurun_out/ab_$v.log 2>&1
   python - "$spec" "gpurun_out/ab_$v.log" <<'PY'
 import json, sys
 spec, path = sys.argv[1], sys.argv[2]

@@ -1,3 +1,4 @@
+#include <cstdlib>
 // prg_sort.cu — non-template parts of the MSD radix sort (see prg_sort.cuh).
 #include <algorithm>
 
@@ -17,6 +18,8 @@ namespace prg::sort {
 // Two passes over the children by one thread: the first only counts what will
 // be emitted, one atomic per list reserves the slots, the second writes them
 // (a returning atomic per emitted segment serialised ~1 us each).
+__device__ uint32_t g_coalesce_max = kLocalCap;
+
 template <bool kWrite>
 __device__ __forceinline__ void emit_pass(const uint64_t* child_start, const uint32_t* child_size, int nchild,
                                           uint8_t buf, int next_shift, int next_bits, Seg* __restrict__ next,
@@ -61,7 +64,13 @@ __device__ __forceinline__ void emit_pass(const uint64_t* child_start, const uin
             }
             continue;
         }
-        if (run.size && run.size + sz > (uint32_t)kLocalCap) {
+        // PRG_COALESCE_MAX (measurement knob): children at least this large are
+        // not joined. Keeping K1's ~2.9 K-key level-2 children apart (all on the
+        // 32-bit merge path) measured slower — K1 local 5.58 vs 4.94 ms, the K3
+        // transpose's 3.11 vs 2.23 ms: a segment costs ~3.5 K cycles per merge
+        // level whatever its size (latency-bound chains), so fewer, fuller
+        // segments win.
+        if (run.size && (run.size + sz > (uint32_t)kLocalCap || sz >= g_coalesce_max || run.size >= g_coalesce_max)) {
             if (kWrite) fin[i_fin] = run;
             ++i_fin;
             run.size = 0;
@@ -304,8 +313,20 @@ __global__ void classify_kernel(const Seg* __restrict__ active, const uint32_t* 
 // Host side
 // ---------------------------------------------------------------------------
 size_t local_smem_bytes() { return sizeof(LocalSmem); }
+int local_merge_span() {
+    static int v = -1;
+    if (v < 0) { const char* e = getenv("PRG_MERGE_SPAN"); v = e ? atoi(e) : 16; }
+    return v;
+}
 
 void sort_workspace_init(SortWorkspace& ws, size_t n, cudaStream_t s) {
+    static bool coalesce_set = false;  // PRG_COALESCE_MAX: children at least this large are not coalesced
+    if (!coalesce_set) {
+        const char* e = getenv("PRG_COALESCE_MAX");
+        const uint32_t v = e ? (uint32_t)atoi(e) : (uint32_t)kLocalCap;
+        PRG_CUDA(cudaMemcpyToSymbol(g_coalesce_max, &v, sizeof(v)));
+        coalesce_set = true;
+    }
     if (ws.n >= n && ws.keys[0].get()) return;
     ws.n = n;
     const uint32_t t1 = div_up(n, kTile);

@@ -15,7 +15,8 @@
 // Global levels peel 8 key bits at a time until every segment fits in shared
 // memory (kLocalCap keys); the local stage then sorts each segment in SMEM with
 // a stable LSD over the segment's varying bits (5-bit digits, thread-private
-// packed counters). An 8-bit ballot-ranked local pass measured slower (K1
+// packed counters), or — for payload-free keys whose varying bits fit a 32-bit
+// window and span >= 16 bits (K1) — a register-network + merge-path merge sort. An 8-bit ballot-ranked local pass measured slower (K1
 // local 6.3 -> 8.4 ms): instruction-bound on the ballots; with __match_any_sync
 // peers instead of ballots it is still slower (5.8 -> 9.0 ms).
 // For reference, CUB's onesweep DeviceRadixSort on this B200 takes 16.6 ms for
@@ -393,8 +394,90 @@ static __device__ __forceinline__ void cta_lsd_sort32(LocalSmem& S, uint32_t n, 
     __syncthreads();
 }
 
+// Batcher odd-even merge sort network for 16 keys (63 compare-exchanges).
+template <class K>
+__device__ __forceinline__ void sort16(K (&k)[kLocalItems]) {
+    constexpr int P[63][2] = {{0,1},{2,3},{0,2},{1,3},{1,2},{4,5},{6,7},{4,6},{5,7},{5,6},{0,4},{2,6},{2,4},{1,5},
+                              {3,7},{3,5},{1,2},{3,4},{5,6},{8,9},{10,11},{8,10},{9,11},{9,10},{12,13},{14,15},
+                              {12,14},{13,15},{13,14},{8,12},{10,14},{10,12},{9,13},{11,15},{11,13},{9,10},{11,12},
+                              {13,14},{0,8},{4,12},{4,8},{2,10},{6,14},{6,10},{2,4},{6,8},{10,12},{1,9},{5,13},
+                              {5,9},{3,11},{7,15},{7,11},{3,5},{7,9},{11,13},{1,2},{3,4},{5,6},{7,8},{9,10},
+                              {11,12},{13,14}};
+#pragma unroll
+    for (int q = 0; q < 63; ++q) {
+        const K a = k[P[q][0]], b = k[P[q][1]];
+        k[P[q][0]] = a < b ? a : b;
+        k[P[q][1]] = a < b ? b : a;
+    }
+}
+
+// Merge-sort alternative to the LSD passes for wide key spans without payload
+// (K1 after two MSD levels: 8 bits of u and 24 of v, or more where small
+// children were coalesced). Each thread sorts its 16 keys with a network in
+// registers, then log2(n/16) merge-path levels in shared memory: thread t
+// produces outputs [16t, 16t+16) of its pair of runs (binary search on the
+// cross diagonal, then a 16-step serial merge). Keys compare whole: unstable is
+// fine. Measured at S=24 (K1 local): 5.56 ms LSD -> 4.94 ms with the 32-bit
+// windows merged; merging the 64-bit (coalesced, > 32-bit span) segments as
+// well was slower (5.34 ms), and so were two interleaved merge paths per thread
+// (5.47 ms) — the levels are issue/bank-conflict bound, not chain-latency bound. X is the xpad-indexed slot array of K (K = u32: the key window >> lo).
+// On return S.X holds the sorted full keys.
+template <class K>
+static __device__ __forceinline__ void cta_merge_sort(LocalSmem& S, uint32_t n, const uint64_t (&kin)[kLocalItems],
+                                                      int lo, uint64_t common) {
+    constexpr K kInf = ~K(0);
+    const unsigned tid = threadIdx.x;
+    K* X = reinterpret_cast<K*>(S.X);
+    K k[kLocalItems];
+#pragma unroll
+    for (int j = 0; j < kLocalItems; ++j) k[j] = (K)(kin[j] >> lo);  // slots past n: all ones
+    // slots [0, nsort): n rounded up to whole threads; runs at the end are clipped
+    const uint32_t nsort = n ? (n + kLocalItems - 1) & ~uint32_t(kLocalItems - 1) : kLocalItems;
+    const bool active = tid * kLocalItems < nsort;
+    if (active) sort16<K>(k);
+    for (uint32_t w = kLocalItems; w < nsort; w <<= 1) {
+        if (active) {
+#pragma unroll
+            for (int j = 0; j < kLocalItems; ++j) X[tid * (kLocalItems + 1) + j] = k[j];  // X[xpad(16t+j)]
+        }
+        __syncthreads();
+        if (active) {
+            const uint32_t pos = tid * kLocalItems;
+            const uint32_t A = pos & ~(2 * w - 1), B = min(A + w, nsort);
+            const uint32_t ea = B, eb = min(B + w, nsort);
+            const uint32_t la = ea - A, lb = eb - B;
+            const uint32_t diag = pos - A;
+            uint32_t b0 = diag > lb ? diag - lb : 0u, b1 = min(diag, la);
+            while (b0 < b1) {  // merge path: the outputs before diag take b0 keys from run A
+                const uint32_t mid = (b0 + b1) >> 1;
+                if (!(X[xpad(B + diag - 1 - mid)] < X[xpad(A + mid)])) b0 = mid + 1;
+                else b1 = mid;
+            }
+            uint32_t ia = A + b0, ib = B + diag - b0;
+            K va = ia < ea ? X[xpad(ia)] : kInf;
+            K vb = ib < eb ? X[xpad(ib)] : kInf;
+#pragma unroll
+            for (int j = 0; j < kLocalItems; ++j) {
+                const bool ta = !(vb < va);
+                k[j] = ta ? va : vb;
+                const uint32_t nx = ta ? ++ia : ++ib;
+                const bool in = ta ? nx < ea : nx < eb;
+                const K v = in ? X[xpad(nx)] : kInf;
+                if (ta) va = v; else vb = v;
+            }
+        }
+        __syncthreads();
+    }
+    // the full keys (slots past n sort last and are never stored)
+#pragma unroll
+    for (int j = 0; j < kLocalItems; ++j) S.X[tid * (kLocalItems + 1) + j] = common | ((uint64_t)k[j] << lo);
+    __syncthreads();
+}
+
 // Sorts X[0, n) (n <= kLocalCap; X indexed through xpad). All threads call.
-static __device__ __forceinline__ void cta_lsd_sort(LocalSmem& S, uint32_t n, int payload_bits) {
+// merge_span: windows of at least this many varying bits (and no payload) are
+// merge-sorted instead of LSD-sorted.
+static __device__ __forceinline__ void cta_lsd_sort(LocalSmem& S, uint32_t n, int payload_bits, int merge_span) {
     const unsigned tid = threadIdx.x, lane = dev::lane_id(), w = dev::warp_id();
     const uint32_t half = (tid & 1u) * 16u;
     uint64_t k[kLocalItems];
@@ -419,6 +502,15 @@ static __device__ __forceinline__ void cta_lsd_sort(LocalSmem& S, uint32_t n, in
     if (diff == 0) { __syncthreads(); return; }  // equal above the payload: sorted
     const int lo = __ffsll((long long)diff) - 1;
     const int hi = 63 - __clzll((long long)diff);
+    const bool merge = payload_bits == 0 && hi - lo + 1 >= (merge_span & 0xff) && (hi - lo < 32 || (merge_span & 0x100));
+    if (PRG_LOCAL_STATS && threadIdx.x == 0) atomicAdd(&g_local_stats[merge ? (hi - lo < 32 ? 5 : 6) : 7], 1ull);
+    if (merge) {
+        if (hi - lo < 32)
+            cta_merge_sort<uint32_t>(S, n, k, lo, a & ~(((hi - lo == 31) ? ~0ull >> 32 : ((1ull << (hi - lo + 1)) - 1)) << lo));
+        else  // PRG_MERGE_SPAN + 256: 64-bit keys too (measured slower than their LSD passes)
+            cta_merge_sort<uint64_t>(S, n, k, 0, 0ull);
+        return;
+    }
     if (payload_bits == 0 && hi - lo < 32) {
         // Every bit outside [lo, hi] is common to the segment: sort the 32-bit
         // window and rebuild the keys (K1 after two MSD levels: 32 varying bits
@@ -486,7 +578,7 @@ template <class Dst>
 __global__ void __launch_bounds__(kLocalThreads, 2)
     local_sort_kernel(const uint64_t* __restrict__ keys0, const uint64_t* __restrict__ keys1,
                       const Seg* __restrict__ fin, const uint32_t* __restrict__ n_fin,
-                      uint32_t* __restrict__ work, Dst dst, int payload_bits) {
+                      uint32_t* __restrict__ work, Dst dst, int payload_bits, int merge_span) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     LocalSmem& S = *reinterpret_cast<LocalSmem*>(smem_raw);
     const uint32_t nf = *n_fin;
@@ -513,7 +605,7 @@ __global__ void __launch_bounds__(kLocalThreads, 2)
         for (uint32_t i = threadIdx.x; i < n; i += kLocalThreads) S.X[xpad(i)] = src[sg.start + i];
         __syncthreads();
         long long c1 = PRG_LOCAL_STATS ? clock64() : 0;
-        cta_lsd_sort(S, n, payload_bits);
+        cta_lsd_sort(S, n, payload_bits, merge_span);
         long long c2 = PRG_LOCAL_STATS ? clock64() : 0;
         for (uint32_t i = threadIdx.x; i < n; i += kLocalThreads)
             dst.store(sg.start + i, S.X[xpad(i)], i > 0, i > 0 ? S.X[xpad(i - 1)] : 0ull);
@@ -549,6 +641,7 @@ struct SortWorkspace {
 
 void sort_workspace_init(SortWorkspace& ws, size_t n, cudaStream_t s);
 size_t local_smem_bytes();
+int local_merge_span();  // PRG_MERGE_SPAN (default 16): see cta_lsd_sort
 
 // Runs levels >= 2 until every segment is final; then the caller launches
 // local_sort_kernel with its Dst. `key_bits` is the number of significant bits.
@@ -618,7 +711,7 @@ void msd_sort_split(Src src_hist, Src src_scat, size_t n, int key_bits, Dst dst,
                                       (int)local_smem_bytes()));
         local_sort_kernel<Dst><<<num_sms() * 2, kLocalThreads, local_smem_bytes(), s>>>(
             ws.keys[0].get(), ws.keys[1].get(), ws.fin.get(), ws.counters.get() + 2, ws.counters.get() + 3, dst,
-            payload_bits);
+            payload_bits, local_merge_span());
         PRG_LAUNCH_CHECK();
     }
 }

@@ -538,7 +538,8 @@ def official_pipeline(scale):
     import prpipe
 
     with tempfile.TemporaryDirectory() as d:
-        prpipe.run_pipeline(scale=10, seed=1, data_dir=os.path.join(d, "warm"))  # CUDA/IO warm-up
+        # CUDA/IO warm-up, large enough to allocate the staged-copy slots (> 8 MB copies)
+        prpipe.run_pipeline(scale=16, seed=1, data_dir=os.path.join(d, "warm"))
         rep = prpipe.run_pipeline(scale=scale, seed=1, data_dir=os.path.join(d, "data"))
     out = {"scale": scale, "api": "prpipe.run_pipeline (drop-in, host TSV I/O inside each record)",
            "records": {k["name"]: {"seconds": k["elapsed_seconds"], "edges_per_s": k["rate_edges_per_sec"]}

@@ -209,8 +209,7 @@ void download_u32_as_i64(const uint32_t* d, size_t n, int64_t* h, cudaStream_t s
     DevBuf<int64_t> tmp(n, s);
     widen_u32<<<(unsigned)prg::num_sms() * 4, 1024, 0, s>>>(d, (int64_t)n, tmp.get());
     PRG_LAUNCH_CHECK();
-    PRG_CUDA(cudaMemcpyAsync(h, tmp.get(), n * 8, cudaMemcpyDeviceToHost, s));
-    PRG_CUDA(cudaStreamSynchronize(s));
+    prg::copy_to_host(h, tmp.get(), n * 8, s);
 }
 
 }  // namespace
@@ -299,11 +298,10 @@ prg_status prg_k1_sort_host(const int64_t* uv_in, int64_t m, int32_t scale, int6
         if (m == 0) return;
         cudaStream_t s = nullptr;
         DevBuf<int64_t> a((size_t)m * 2, s), b((size_t)m * 2, s);
-        PRG_CUDA(cudaMemcpyAsync(a.get(), uv_in, (size_t)m * 16, cudaMemcpyHostToDevice, s));
+        prg::copy_to_device(a.get(), uv_in, (size_t)m * 16, s);
         const prg_status st = prg_k1_sort_device(a.get(), m, scale, b.get(), s);
         if (st != PRG_OK) throw ApiError{st, prg::last_error()};
-        PRG_CUDA(cudaMemcpyAsync(uv_out, b.get(), (size_t)m * 16, cudaMemcpyDeviceToHost, s));
-        PRG_CUDA(cudaStreamSynchronize(s));
+        prg::copy_to_host(uv_out, b.get(), (size_t)m * 16, s);
     });
 }
 
@@ -379,7 +377,7 @@ prg_status prg_k2_filter_host(const int64_t* uv_sorted, int64_t m, int64_t n, pr
         require(m >= 0, PRG_ERR_INVALID_ARGUMENT, "negative edge count");
         cudaStream_t s = nullptr;
         DevBuf<int64_t> a((size_t)std::max<int64_t>(m, 1) * 2, s);
-        if (m) PRG_CUDA(cudaMemcpyAsync(a.get(), uv_sorted, (size_t)m * 16, cudaMemcpyHostToDevice, s));
+        if (m) prg::copy_to_device(a.get(), uv_sorted, (size_t)m * 16, s);
         const prg_status st = prg_k2_filter_device(a.get(), m, n, out, s);
         if (st != PRG_OK) throw ApiError{st, prg::last_error()};
     });
@@ -393,7 +391,7 @@ prg_status prg_build_adjacency_host(const int64_t* uv_sorted, int64_t m, int64_t
                 "sizes exceed the u32 index range");
         cudaStream_t s = nullptr;
         DevBuf<int64_t> a((size_t)std::max<int64_t>(m, 1) * 2, s);
-        if (m) PRG_CUDA(cudaMemcpyAsync(a.get(), uv_sorted, (size_t)m * 16, cudaMemcpyHostToDevice, s));
+        if (m) prg::copy_to_device(a.get(), uv_sorted, (size_t)m * 16, s);
         std::unique_ptr<prg_matrix> mat(new prg_matrix());
         const uint32_t err = prg::k2_filter_device(a.get(), m, n, mat.get(), s, /*filter=*/false, /*normalize=*/false);
         check_device_errors(err, "build_adjacency");
@@ -485,9 +483,7 @@ prg_status prg_matrix_download(const prg_matrix* a, int64_t* row_offsets, int64_
         cudaStream_t s = nullptr;
         download_u32_as_i64(a->row_offsets, (size_t)a->n + 1, row_offsets, s);
         download_u32_as_i64(a->cols, (size_t)a->nnz, cols, s);
-        if (values && a->nnz) {
-            PRG_CUDA(cudaMemcpy(values, a->values, a->nnz * 8, cudaMemcpyDeviceToHost));
-        }
+        if (values && a->nnz) prg::copy_to_host(values, a->values, a->nnz * 8, s);
         if (d_in) {
             if (a->d_in) download_u32_as_i64(a->d_in, (size_t)a->n, d_in, s);
             else std::memset(d_in, 0, (size_t)a->n * 8);

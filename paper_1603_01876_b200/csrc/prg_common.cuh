@@ -62,6 +62,11 @@ void* ws_alloc(size_t bytes, cudaStream_t s);
 void ws_free(void* p, cudaStream_t s);
 void ws_trim();  // return the library pool's unused memory to the driver
 
+// Large host <-> device copies through pinned slots and host worker threads
+// (pageable host memory on the host side). Both return when the copy is done.
+void copy_to_device(void* dst, const void* src, size_t bytes, cudaStream_t s);
+void copy_to_host(void* dst, const void* src, size_t bytes, cudaStream_t s);
+
 template <class T>
 struct DevBuf {
     T* p = nullptr;

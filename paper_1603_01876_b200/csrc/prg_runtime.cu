@@ -1,7 +1,10 @@
 // prg_runtime.cu — error channel, stream-ordered workspace, device-wide scan.
+#include <algorithm>
 #include <atomic>
+#include <cstring>
 #include <map>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "prg_common.cuh"
@@ -284,4 +287,127 @@ void exclusive_scan_u32_prefix(const uint32_t* in, uint32_t* out, size_t cap, co
     scan_impl<uint32_t>(in, out, cap, nullptr, s, d_count, mult);
 }
 
+
+// ---- staged host <-> device copies ------------------------------------------
+// A pageable cudaMemcpy moves ~10-20 GB/s through the driver's own staging and
+// runs on one host thread, and first-touch page faults on a fresh destination
+// vector serialise behind it. Large copies here go through pinned slots owned
+// by kStageWorkers host threads, each with its own stream: a worker memcpys a
+// chunk into its slot while its previous chunk is on the wire, so host copies,
+// page faults and DMA all overlap (the drop-in's TSV-record paths move 0.25-1 GB
+// per call at S=20-22). Slots are allocated once per process and kept.
+namespace {
+constexpr int kStageWorkers = 8;
+constexpr size_t kStageChunk = size_t{4} << 20;  // bytes per slot
+constexpr size_t kStageMin = size_t{8} << 20;    // below this: one plain copy
+struct StageWorker {
+    void* slot[2] = {nullptr, nullptr};
+    cudaStream_t st = nullptr;
+    cudaEvent_t done[2] = {nullptr, nullptr};
+};
+std::mutex g_stage_mu;  // one staged copy at a time owns the slots
+StageWorker g_stage[kStageWorkers];
+bool g_stage_ready = false;
+
+void stage_init() {
+    if (g_stage_ready) return;
+    for (auto& w : g_stage) {
+        for (int k = 0; k < 2; ++k) {
+            PRG_CUDA(cudaMallocHost(&w.slot[k], kStageChunk));
+            PRG_CUDA(cudaEventCreateWithFlags(&w.done[k], cudaEventDisableTiming));
+        }
+        PRG_CUDA(cudaStreamCreateWithFlags(&w.st, cudaStreamNonBlocking));
+    }
+    g_stage_ready = true;
+}
+
+template <class Fn>
+void stage_run(Fn&& fn) {  // fn(worker index) on kStageWorkers threads, errors rethrown here
+    int dev = 0;
+    PRG_CUDA(cudaGetDevice(&dev));
+    std::vector<std::thread> crew;
+    std::vector<std::string> err(kStageWorkers);
+    for (int w = 0; w < kStageWorkers; ++w)
+        crew.emplace_back([&, w] {
+            try {
+                PRG_CUDA(cudaSetDevice(dev));
+                fn(w);
+            } catch (const CudaError& e) {
+                err[(size_t)w] = e.msg;
+            }
+        });
+    for (auto& t : crew) t.join();
+    for (auto& e : err)
+        if (!e.empty()) throw CudaError{e};
+}
+}  // namespace
+
+void copy_to_device(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    if (bytes < kStageMin) {
+        PRG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+        PRG_CUDA(cudaStreamSynchronize(s));
+        return;
+    }
+    PRG_CUDA(cudaStreamSynchronize(s));  // dst (stream-ordered allocation) is usable from the worker streams
+    std::lock_guard<std::mutex> lk(g_stage_mu);
+    stage_init();
+    const size_t nch = (bytes + kStageChunk - 1) / kStageChunk;
+    stage_run([&](int w) {
+        StageWorker& W = g_stage[w];
+        int k = 0;
+        for (size_t c = (size_t)w; c < nch; c += kStageWorkers, k ^= 1) {
+            const size_t off = c * kStageChunk, len = std::min(kStageChunk, bytes - off);
+            PRG_CUDA(cudaEventSynchronize(W.done[k]));  // the slot's previous copy has left
+            std::memcpy(W.slot[k], static_cast<const char*>(src) + off, len);
+            PRG_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + off, W.slot[k], len, cudaMemcpyHostToDevice, W.st));
+            PRG_CUDA(cudaEventRecord(W.done[k], W.st));
+        }
+        PRG_CUDA(cudaStreamSynchronize(W.st));
+    });
+    // the data is on the device before any later work on `s` (the workers synchronised)
+}
+
+void copy_to_host(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    if (bytes < kStageMin) {
+        PRG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+        PRG_CUDA(cudaStreamSynchronize(s));
+        return;
+    }
+    PRG_CUDA(cudaStreamSynchronize(s));  // the producing kernels are done
+    std::lock_guard<std::mutex> lk(g_stage_mu);
+    stage_init();
+    const size_t nch = (bytes + kStageChunk - 1) / kStageChunk;
+    stage_run([&](int w) {
+        StageWorker& W = g_stage[w];
+        // double-buffered: chunk i+1 is on the wire while chunk i is copied out
+        size_t prev_off = 0, prev_len = 0;
+        int k = 0;
+        bool have_prev = false;
+        for (size_t c = (size_t)w;; c += kStageWorkers) {
+            const bool more = c < nch;
+            if (more) {
+                const size_t off = c * kStageChunk, len = std::min(kStageChunk, bytes - off);
+                PRG_CUDA(cudaMemcpyAsync(W.slot[k], static_cast<const char*>(src) + off, len, cudaMemcpyDeviceToHost,
+                                         W.st));
+                PRG_CUDA(cudaEventRecord(W.done[k], W.st));
+                if (have_prev) {
+                    PRG_CUDA(cudaEventSynchronize(W.done[k ^ 1]));
+                    std::memcpy(static_cast<char*>(dst) + prev_off, W.slot[k ^ 1], prev_len);
+                }
+                prev_off = off;
+                prev_len = len;
+                have_prev = true;
+                k ^= 1;
+            } else {
+                if (have_prev) {
+                    PRG_CUDA(cudaEventSynchronize(W.done[k ^ 1]));
+                    std::memcpy(static_cast<char*>(dst) + prev_off, W.slot[k ^ 1], prev_len);
+                }
+                break;
+            }
+        }
+    });
+}
+
 }  // namespace prg
+

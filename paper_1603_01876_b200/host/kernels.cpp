@@ -8,6 +8,7 @@
 #include <fstream>
 #include <list>
 #include <atomic>
+#include <memory>
 #include <mutex>
 #include <thread>
 #include <numeric>
@@ -147,10 +148,13 @@ EdgeManifest sort_edges(const EdgeManifest& input, const std::filesystem::path& 
         std::vector<Edge> edges = read_edges(input);
         g_last_sort.read_s = t0.seconds();
         Timer t1;
-        std::vector<Edge> sorted(edges.size());
+        // uninitialised storage (a zero-filled vector cost a single-threaded
+        // 268 MB memset at S=20); the staged download's worker threads fault it in
+        std::unique_ptr<std::byte[]> sorted_buf(new std::byte[edges.size() * sizeof(Edge)]);
+        const std::span<const Edge> sorted(reinterpret_cast<const Edge*>(sorted_buf.get()), edges.size());
         if (!edges.empty())
             check(prg_k1_sort_host(edge_words(edges), static_cast<std::int64_t>(edges.size()), input.scale,
-                                   reinterpret_cast<std::int64_t*>(sorted.data())));
+                                   reinterpret_cast<std::int64_t*>(sorted_buf.get())));
         g_last_sort.device_s = t1.seconds();
         Timer t2;
         auto out = write_edges(sorted, output_dir, files, input.scale, /*sorted_by_start=*/true);
@@ -296,9 +300,13 @@ Kernel2Result run_kernel2(const EdgeManifest& input) {
     prg_matrix_info(dev, &n, &nnz, nullptr, nullptr);
     StochasticMatrix& m = res.matrix;
     m.n = n;
-    m.row_offsets.resize(static_cast<std::size_t>(n) + 1);
-    m.cols.resize(static_cast<std::size_t>(nnz));
-    m.values.resize(static_cast<std::size_t>(nnz));
+    {   // the vectors' zero fill (value-initialisation) on three threads at once
+        std::thread a([&] { m.cols.resize(static_cast<std::size_t>(nnz)); });
+        std::thread b([&] { m.values.resize(static_cast<std::size_t>(nnz)); });
+        m.row_offsets.resize(static_cast<std::size_t>(n) + 1);
+        a.join();
+        b.join();
+    }
     const prg_status st = prg_matrix_download(dev, m.row_offsets.data(), m.cols.data(), m.values.data(), nullptr);
     if (st != PRG_OK) {
         prg_matrix_destroy(dev);

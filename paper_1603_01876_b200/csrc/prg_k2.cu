@@ -35,14 +35,18 @@ __device__ __forceinline__ int sp(int l) { return l + (l >> 5); }
 constexpr int kTEP = kTE + kTE / 32;
 
 
+struct Scan3 {
+    int32_t rs, hd;
+    uint32_t kh;
+};
+
 struct PassBSmem {
     uint32_t su[kTEP];
     uint32_t sv[kTEP];
     // per head (local index, padded): kept-edge count of the row in bits 16..31
     // (row heads), edge count of the (u,v) run in bits 0..15 (run heads); both <= kTE
     uint32_t rr[kTEP];
-    uint32_t scan_u[kT / 32 + 1];
-    int32_t scan_i[kT / 32 + 1];
+    Scan3 scan3[kT / 32 + 1];
     uint32_t prev_u, prev_v, next_u;
     int has_prev, has_next;
     uint32_t tile;
@@ -50,36 +54,47 @@ struct PassBSmem {
     uint32_t first_row_part, first_run_part;
 };
 
-__device__ __forceinline__ int32_t block_excl_max_scan(int32_t v, int32_t* smem, int32_t& total) {
+// The three block scans pass B needs in one pass (two barriers instead of six):
+// exclusive max-scans of the last row start and last run head per thread (-1 =
+// none) and the exclusive sum-scan of kept heads. Totals: the tile's last row
+// start / last run head and its kept-head count.
+__device__ __forceinline__ Scan3 block_excl_scan3(Scan3 v, Scan3* smem, Scan3& total) {
     const unsigned w = dev::warp_id(), l = dev::lane_id(), nw = blockDim.x >> 5;
-    int32_t inc = v;
+    Scan3 inc = v;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
-        int32_t o = __shfl_up_sync(0xffffffffu, inc, d);
-        if ((int)l >= d) inc = max(inc, o);
+        const int32_t a = __shfl_up_sync(0xffffffffu, inc.rs, d), b = __shfl_up_sync(0xffffffffu, inc.hd, d);
+        const uint32_t c = __shfl_up_sync(0xffffffffu, inc.kh, d);
+        if ((int)l >= d) { inc.rs = max(inc.rs, a); inc.hd = max(inc.hd, b); inc.kh += c; }
     }
-    int32_t ex = __shfl_up_sync(0xffffffffu, inc, 1);
-    if (l == 0) ex = -1;
+    Scan3 ex;
+    ex.rs = __shfl_up_sync(0xffffffffu, inc.rs, 1);
+    ex.hd = __shfl_up_sync(0xffffffffu, inc.hd, 1);
+    ex.kh = inc.kh - v.kh;
+    if (l == 0) { ex.rs = -1; ex.hd = -1; }
     if (l == 31) smem[w] = inc;
     __syncthreads();
     if (w == 0) {
-        int32_t x = l < nw ? smem[l] : -1;
-        int32_t xi = x;
+        Scan3 x = l < nw ? smem[l] : Scan3{-1, -1, 0u};
+        Scan3 xi = x;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
-            int32_t o = __shfl_up_sync(0xffffffffu, xi, d);
-            if ((int)l >= d) xi = max(xi, o);
+            const int32_t a = __shfl_up_sync(0xffffffffu, xi.rs, d), b = __shfl_up_sync(0xffffffffu, xi.hd, d);
+            const uint32_t c = __shfl_up_sync(0xffffffffu, xi.kh, d);
+            if ((int)l >= d) { xi.rs = max(xi.rs, a); xi.hd = max(xi.hd, b); xi.kh += c; }
         }
-        int32_t xe = __shfl_up_sync(0xffffffffu, xi, 1);
-        if (l == 0) xe = -1;
+        Scan3 xe;
+        xe.rs = __shfl_up_sync(0xffffffffu, xi.rs, 1);
+        xe.hd = __shfl_up_sync(0xffffffffu, xi.hd, 1);
+        xe.kh = xi.kh - x.kh;
+        if (l == 0) { xe.rs = -1; xe.hd = -1; }
         if (l < nw) smem[l] = xe;
         if (l == nw - 1) smem[nw] = xi;
     }
     __syncthreads();
-    const int32_t res = max(smem[w], ex);
+    const Scan3 wp = smem[w];
     total = smem[nw];
-    __syncthreads();
-    return res;
+    return Scan3{max(wp.rs, ex.rs), max(wp.hd, ex.hd), wp.kh + ex.kh};
 }
 
 // ---------------------------------------------------------------------------
@@ -259,11 +274,10 @@ __global__ void __launch_bounds__(kT) k2_pass_b(
             nkh += (hd && kp);
         }
     }
-    int32_t rs_last_all, hd_last_all;
-    const int32_t carry_rs = block_excl_max_scan(last_rs, S.scan_i, rs_last_all);
-    const int32_t carry_hd = block_excl_max_scan(last_hd, S.scan_i, hd_last_all);
-    uint32_t tile_kh;
-    const uint32_t kh_excl = dev::block_excl_scan(nkh, S.scan_u, tile_kh);
+    Scan3 tot3;
+    const Scan3 ex3 = block_excl_scan3(Scan3{last_rs, last_hd, nkh}, S.scan3, tot3);
+    const int32_t carry_rs = ex3.rs, carry_hd = ex3.hd, rs_last_all = tot3.rs;
+    const uint32_t kh_excl = ex3.kh, tile_kh = tot3.kh;
 
     // The tile's aggregate is published now; the look-back runs after the row
     // sums (below), when the predecessors have mostly published inclusive

@@ -342,10 +342,15 @@ __global__ void __launch_bounds__(kT) k2_pass_b(
     const bool first_spans = S.has_prev && S.su[sp(0)] == S.prev_u;
     const int32_t rh_last = rs_last_all;  // local head of the tile's last row (-1: began earlier)
 
-    // Emit entries and row offsets.
+    // Emit entries and row offsets. Positions fit in 32 bits (nnz < 2^32). A
+    // count of 1 — nearly every entry — takes the row's 1/d_out, which is the
+    // same IEEE division the reference performs; it is computed once per row
+    // and thread, other counts divide themselves (bit-exact either way).
     {
-        int32_t rh = carry_rs;
-        uint64_t pos = tile_base + kh_excl;
+        int32_t rh = carry_rs, inv_row = -2;
+        double inv = 0.0;
+        uint32_t pos = (uint32_t)(tile_base + kh_excl);
+        const bool stream = flags & 2;
 #pragma unroll
         for (int k = 0; k < kI; ++k) {
             const int l = l0 + k;
@@ -354,13 +359,23 @@ __global__ void __launch_bounds__(kT) k2_pass_b(
                 if ((fl_rs >> k) & 1u) {
                     rh = l;
                     const int64_t pu = l > 0 ? (int64_t)S.su[sp(l - 1)] : (S.has_prev ? (int64_t)S.prev_u : -1);
-                    for (int64_t r = pu + 1; r <= (int64_t)u; ++r) row_offsets[r] = (uint32_t)pos;
+                    for (int64_t r = pu + 1; r <= (int64_t)u; ++r) row_offsets[r] = pos;
                 }
                 if (((fl_hd >> k) & 1u) && ((fl_kp >> k) & 1u)) {
-                    const double c = (double)(S.rr[sp(l)] & 0xffffu);
+                    const uint32_t cnt_run = S.rr[sp(l)] & 0xffffu;
+                    const double c = (double)cnt_run;
                     const bool spanning = rh < 0 || (last_spans && rh == rh_last);
-                    const double val = (spanning || !normalize) ? c : c / (double)(S.rr[sp(rh)] >> 16);
-                    if (flags & 2) {  // streaming stores: the outputs are not re-read by this pass
+                    double val = c;
+                    if (!spanning && normalize) {
+                        const double d = (double)(S.rr[sp(rh)] >> 16);
+                        if (cnt_run == 1u) {
+                            if (inv_row != rh) { inv = 1.0 / d; inv_row = rh; }
+                            val = inv;
+                        } else {
+                            val = c / d;
+                        }
+                    }
+                    if (stream) {  // streaming stores: the outputs are not re-read by this pass
                         __stcs(cols + pos, v);
                         __stcs(values + pos, val);
                     } else {

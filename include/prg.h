@@ -51,6 +51,9 @@ int32_t prg_device_count(void);
  * regions (k1_sort, k2_filter, k3_spmv, ...) on the stream they ran on;
  * report writes JSON {"name": [count, total_ms]} and returns its length. */
 int64_t prg_launch_count(void);
+/* Checked builds only (-DPRG_CHECKED=1; release builds return 0): failed
+ * device-side bounds / invariant checks since the last call (then reset). */
+int64_t prg_debug_check_failures(void);
 
 /* Bytes the last prg_k3_pagerank_host call moved host -> device: its CSR
  * structure plus, instead of the f64 values, one base value per row and the

@@ -49,23 +49,32 @@ def _run(cmd: list[str]) -> None:
         sys.stderr.write(r.stderr)
 
 
-def build_libprg(force: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
-    os.makedirs(os.path.dirname(LIB), exist_ok=True)
+# Checked variant (device-side bounds / invariant checks, PRG_DCHECK in the
+# sources): test infrastructure for tests/test_checked.py, never loaded by the
+# product path unless PRG_LIB points at it.
+LIB_CHECKED = os.path.join(ROOT, "build", "libprg_checked.so")
+
+
+def build_libprg(force: bool = False, checked: bool = False) -> str:
+    lib = LIB_CHECKED if checked else LIB
+    objdir = os.path.join(ROOT, "build", "obj_checked") if checked else BUILD
+    os.makedirs(objdir, exist_ok=True)
+    os.makedirs(os.path.dirname(lib), exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "prg.h")]
+    flags = NVCC_FLAGS + (["-DPRG_CHECKED=1"] if checked else [])
     jobs = []
     objs = []
     for src in CU_SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(BUILD, src.replace(".cu", ".o"))
+        o = os.path.join(objdir, src.replace(".cu", ".o"))
         objs.append(o)
         if force or _newer(o, [s] + hdrs):
-            jobs.append([NVCC] + NVCC_FLAGS + ["-c", s, "-o", o])
+            jobs.append([NVCC] + flags + ["-c", s, "-o", o])
     with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
         list(ex.map(_run, jobs))
-    if force or jobs or _newer(LIB, objs):
-        _run([NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart"])
-    return LIB
+    if force or jobs or _newer(lib, objs):
+        _run([NVCC] + ARCH + ["-shared", "-o", lib] + objs + ["-lcudart"])
+    return lib
 
 
 def build_core(force: bool = False) -> str | None:
@@ -114,6 +123,7 @@ def _json_include() -> str:
 def build(force: bool = False) -> None:
     build_libprg(force)
     build_core(force)
+    build_libprg(force, checked=True)
 
 
 if __name__ == "__main__":

@@ -31,7 +31,8 @@ HEADER_SYMBOLS = (
     "prg_k2_filter_host", "prg_matrix_info", "prg_matrix_download", "prg_matrix_device_arrays",
     "prg_matrix_build_csc", "prg_matrix_drop_csc", "prg_matrix_has_csc",
     "prg_matrix_from_host", "prg_matrix_destroy", "prg_k3_pagerank_device", "prg_k3_pagerank_host",
-    "prg_init_rank_device", "prg_pagerank_step_device", "prg_launch_count", "prg_last_h2d_bytes", "prg_profile_enable",
+    "prg_init_rank_device", "prg_pagerank_step_device", "prg_launch_count", "prg_debug_check_failures",
+    "prg_last_h2d_bytes", "prg_profile_enable",
     "prg_profile_report", "prg_build_adjacency_host", "prg_in_degree_host", "prg_zero_columns_host",
     "prg_row_normalize_host", "prg_init_rank_host", "prg_pagerank_step_host", "prg_k3_pagerank_matrix_host",
     "prg_run_to_convergence_host", "prg_trim_memory", "prg_k1_sort_streamed", "prg_k3_pagerank_sharded",
@@ -79,6 +80,7 @@ def lib() -> C.CDLL:
             "prg_init_rank_device": (i32, [i64, u64, i32, vp, vp, vp]),
             "prg_pagerank_step_device": (i32, [vp, vp, f64, i32, vp, vp, vp]),
             "prg_launch_count": (i64, []),
+            "prg_debug_check_failures": (i64, []),
             "prg_last_h2d_bytes": (i64, []),
             "prg_profile_enable": (None, [i32]),
             "prg_profile_report": (i64, [vp, i64, i32]),

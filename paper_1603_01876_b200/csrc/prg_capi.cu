@@ -220,6 +220,17 @@ const char* prg_last_error(void) { return prg::last_error().c_str(); }
 const char* prg_version(void) { return "prg-b200 0.1.0 (sm_100a)"; }
 
 int64_t prg_launch_count(void) { return prg::launch_count(); }
+
+int64_t prg_debug_check_failures(void) {
+    try {
+        return (int64_t)prg::check_failures_runtime() + prg::check_failures_sort() + prg::check_failures_k0() +
+               prg::check_failures_k1() + prg::check_failures_k2() + prg::check_failures_k3() +
+               prg::check_failures_k2steps() + prg::check_failures_capi();
+    } catch (const prg::CudaError& e) {
+        prg::set_error(e.msg);
+        return -1;
+    }
+}
 int64_t prg_last_h2d_bytes(void) { return g_last_h2d_bytes; }
 void prg_profile_enable(int32_t on) { prg::profiling_enable(on != 0); }
 prg_status prg_trim_memory(void) {
@@ -796,3 +807,5 @@ prg_status prg_run_to_convergence_host(int64_t n, int64_t nnz, const int64_t* ro
 }
 
 }  // extern "C"
+
+PRG_CHECK_QUERY(capi)

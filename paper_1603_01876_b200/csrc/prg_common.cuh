@@ -119,6 +119,27 @@ enum DeviceErr : uint32_t {
 // ----------------------------------------------------------------------------
 namespace prg::dev {
 
+// Checked builds (-DPRG_CHECKED=1: build/libprg_checked.so, tests/test_checked.py):
+// bounds and invariant checks on the index-computing and lock-free paths (sort
+// scatters, local-stage slots, K2 output slots, K3 gathers). Compute-sanitizer
+// is closed on this GPU pool, so these stand in for memcheck. A failed check
+// counts into this translation unit's g_check_fail; prg_debug_check_failures()
+// sums and resets the counters of every unit. Release builds compile them out.
+#ifndef PRG_CHECKED
+#define PRG_CHECKED 0
+#endif
+static __device__ unsigned int g_check_fail = 0;
+#if PRG_CHECKED
+#define PRG_DCHECK(cond)                                                   \
+    do {                                                                   \
+        if (!(cond)) atomicAdd(&::prg::dev::g_check_fail, 1u);             \
+    } while (0)
+#else
+#define PRG_DCHECK(cond) \
+    do {                 \
+    } while (0)
+#endif
+
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 __device__ __forceinline__ unsigned warp_id() { return threadIdx.x >> 5; }
 
@@ -284,3 +305,16 @@ __host__ __device__ __forceinline__ uint64_t mix_seed(uint64_t seed, uint64_t st
 }
 
 }  // namespace prg::dev
+
+// Per translation unit: read and reset its check-failure counter (0 in release builds).
+#define PRG_CHECK_QUERY(tag)                                                              \
+    namespace prg {                                                                       \
+    uint32_t check_failures_##tag() {                                                     \
+        unsigned v = 0, z = 0;                                                            \
+        if (PRG_CHECKED) {                                                                \
+            PRG_CUDA(cudaMemcpyFromSymbol(&v, ::prg::dev::g_check_fail, sizeof(v)));      \
+            PRG_CUDA(cudaMemcpyToSymbol(::prg::dev::g_check_fail, &z, sizeof(z)));        \
+        }                                                                                 \
+        return v;                                                                         \
+    }                                                                                     \
+    }

@@ -30,6 +30,16 @@ struct prg_matrix {
 
 namespace prg {
 
+// Checked builds: failed PRG_DCHECKs per translation unit (read and reset).
+uint32_t check_failures_runtime();
+uint32_t check_failures_sort();
+uint32_t check_failures_k0();
+uint32_t check_failures_k1();
+uint32_t check_failures_k2();
+uint32_t check_failures_k3();
+uint32_t check_failures_k2steps();
+uint32_t check_failures_capi();
+
 // K1 (prg_k1.cu): sort M int64 (u,v) pairs by (u,v). d_err receives DeviceErr bits.
 void k1_sort_device(const int64_t* d_uv_in, int64_t m, int scale, int64_t* d_uv_out,
                     uint32_t* d_err, cudaStream_t s);

@@ -44,3 +44,5 @@ void k0_generate_device(int scale, int64_t /*edge_factor*/, uint64_t seed, const
 }
 
 }  // namespace prg
+
+PRG_CHECK_QUERY(k0)

@@ -60,3 +60,5 @@ extern "C" void prg_debug_k1_local_stats(unsigned long long* out) {
     static const unsigned long long zero[16] = {};
     cudaMemcpyToSymbol(prg::sort::g_local_stats, zero, sizeof(zero));
 }
+
+PRG_CHECK_QUERY(k1)

@@ -359,6 +359,7 @@ __global__ void __launch_bounds__(kT) k2_pass_b(
                 if ((fl_rs >> k) & 1u) {
                     rh = l;
                     const int64_t pu = l > 0 ? (int64_t)S.su[sp(l - 1)] : (S.has_prev ? (int64_t)S.prev_u : -1);
+                    PRG_DCHECK((int64_t)u < n && pu < (int64_t)u);
                     for (int64_t r = pu + 1; r <= (int64_t)u; ++r) row_offsets[r] = pos;
                 }
                 if (((fl_hd >> k) & 1u) && ((fl_kp >> k) & 1u)) {
@@ -375,6 +376,7 @@ __global__ void __launch_bounds__(kT) k2_pass_b(
                             val = c / d;
                         }
                     }
+                    PRG_DCHECK((int64_t)pos < m && v < (uint64_t)n);
                     if (stream) {  // streaming stores: the outputs are not re-read by this pass
                         __stcs(cols + pos, v);
                         __stcs(values + pos, val);
@@ -554,6 +556,7 @@ __global__ void __launch_bounds__(kST) k2_pass_a_tma(const longlong2* __restrict
                     // a run of equal edges adds its length (within this row) from its first lane
                     const unsigned after = ~(eqm >> lane >> 1) & (0x7fffffffu >> lane);
                     const uint32_t len = 1u + (after ? (uint32_t)(__ffs(after) - 1) : 31u - lane);
+                    PRG_DCHECK(len >= 1 && len <= 32u - lane);
                     atomicAdd(&d_in[(uint32_t)(e.y - 1)], len);
                 }
                 if (has_pred) {
@@ -706,3 +709,5 @@ uint32_t k2_filter_device(const int64_t* d_uv, int64_t m, int64_t n, prg_matrix*
 }
 
 }  // namespace prg
+
+PRG_CHECK_QUERY(k2)

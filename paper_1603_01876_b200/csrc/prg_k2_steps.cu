@@ -130,3 +130,5 @@ void k2_row_normalize_device(int64_t n, const int64_t* row_offsets, const int64_
 }
 
 }  // namespace prg
+
+PRG_CHECK_QUERY(k2steps)

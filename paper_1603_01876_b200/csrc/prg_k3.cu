@@ -301,6 +301,7 @@ __global__ void __launch_bounds__(sort::kTileThreads, 4) key_build_kernel(KeyBui
                 const bool exc = (uint64_t)__double_as_longlong(v) != a.bmin[u];
                 const uint32_t nid = a.newid ? a.newid[u] : u;
                 const uint32_t pos = a.wdelta ? e + a.wdelta[u] : e;
+                PRG_DCHECK(pos < a.nnz && u < a.n);
                 a.keys[pos] = ((uint64_t)c << (a.pb + 1)) | ((uint64_t)nid << 1);  // exceptions: rewritten below
                 excm |= (uint32_t)exc << j;
             }
@@ -978,6 +979,7 @@ struct SellArgs {
     uint32_t slice_begin = 0;    // this launch covers slices [slice_begin, slice_end) (a
     uint32_t slice_end = 0;      // shard of a multi-GPU K3; the whole list on one GPU)
     double damping;
+    uint64_t n_s = 0;            // length of s (checked builds: gather bounds)
 };
 
 
@@ -1024,8 +1026,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) spmv_sell_kernel(SellArg
         for (uint32_t k0 = 0; k0 < rows; k0 += U) {
             double x[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u)
+            for (int u = 0; u < U; ++u) {
+                PRG_DCHECK((w[u] >> 31) || w[u] < a.n_s);
                 x[u] = dev::ld_keep_f64_pred(a.s + (w[u] & 0x7fffffffu), !(w[u] >> 31), pol_keep);
+            }
             const uint32_t k1 = k0 + U;
 #pragma unroll
             for (int u = 0; u < U; ++u)
@@ -1533,6 +1537,7 @@ void iterate(const K3Plan& P, const double* r_in, double* r_out, int iters, doub
         a.slice_begin = sl_begin;
         a.slice_end = sl_end;
         a.damping = damping;
+        a.n_s = (uint64_t)(P.n_nd + P.n_exc);
         if (sharded)  // every element is then written by exactly one rank
             PRG_CUDA(cudaMemsetAsync(y_of(it & 1), 0, xcount * sizeof(double), s));
         if (P.nslices && sl_end > sl_begin) {
@@ -1733,3 +1738,5 @@ double k3_step_device(const prg_matrix* A, const double* d_r, double damping, do
 }
 
 }  // namespace prg
+
+PRG_CHECK_QUERY(k3)

@@ -411,3 +411,4 @@ void copy_to_host(void* dst, const void* src, size_t bytes, cudaStream_t s) {
 
 }  // namespace prg
 
+PRG_CHECK_QUERY(runtime)

@@ -265,13 +265,18 @@ __global__ void __launch_bounds__(kTileThreads, 2) seg_scatter_kernel(
 #pragma unroll
             for (int j = 0; j < kTileItems; ++j) {
                 int li = j * kTileThreads + threadIdx.x;
-                if (li < cnt) skeys[atomicAdd(&h[(unsigned)(k[j] >> sg.shift) & mask], 1u)] = k[j];
+                if (li < cnt) {
+                    const uint32_t slot = atomicAdd(&h[(unsigned)(k[j] >> sg.shift) & mask], 1u);
+                    PRG_DCHECK(slot < (uint32_t)cnt);
+                    skeys[slot] = k[j];
+                }
             }
             __syncthreads();
         }
         for (int i = threadIdx.x; i < cnt; i += kTileThreads) {
             uint64_t key = skeys[i];
             unsigned d = (unsigned)(key >> sg.shift) & mask;
+            PRG_DCHECK(gbase[d] + (i - lstart[d]) >= sg.start && gbase[d] + (i - lstart[d]) < sg.start + sg.size);
             dst[gbase[d] + (i - lstart[d])] = key;
         }
         __syncthreads();
@@ -401,3 +406,5 @@ void run_segmented_levels(SortWorkspace& ws, int levels_left, int floor_bit, boo
 }
 
 }  // namespace prg::sort
+
+PRG_CHECK_QUERY(sort)

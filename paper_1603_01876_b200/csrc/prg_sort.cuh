@@ -169,6 +169,7 @@ __device__ __forceinline__ void stable_tile_scatter(const uint64_t (&k)[kTileIte
         if (tile_pos<true>(j) < cnt) {
             const unsigned d = (unsigned)(k[j] >> shift) & mask;
             const uint32_t r = (rk[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
+            PRG_DCHECK(wc[w * kRadix + d] + r < (uint32_t)cnt);
             skeys[wc[w * kRadix + d] + r] = k[j];
         }
     }
@@ -226,13 +227,18 @@ __global__ void __launch_bounds__(kTileThreads, 2) l1_scatter_kernel(Src src, si
 #pragma unroll
             for (int j = 0; j < kTileItems; ++j) {
                 int li = j * kTileThreads + threadIdx.x;
-                if (li < cnt) skeys[atomicAdd(&h[(unsigned)(k[j] >> shift) & dmask], 1u)] = k[j];
+                if (li < cnt) {
+                    const uint32_t slot = atomicAdd(&h[(unsigned)(k[j] >> shift) & dmask], 1u);
+                    PRG_DCHECK(slot < (uint32_t)cnt);
+                    skeys[slot] = k[j];
+                }
             }
             __syncthreads();
         }
         for (int i = threadIdx.x; i < cnt; i += kTileThreads) {
             uint64_t key = skeys[i];
             unsigned d = (unsigned)(key >> shift) & dmask;
+            PRG_DCHECK(gbase[d] + (i - lstart[d]) < n && i >= (int)lstart[d]);
             out[gbase[d] + (i - lstart[d])] = key;
         }
         __syncthreads();
@@ -381,6 +387,7 @@ static __device__ __forceinline__ void cta_lsd_sort32(LocalSmem& S, uint32_t n, 
             const uint32_t d = (k[j] >> sh) & (kLsdDigits - 1);
             const uint32_t pre = (S.cnt[d * 272u + pp] >> half) & 0xffffu;
             const uint32_t r = (rk[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
+            PRG_DCHECK(pre + r < (uint32_t)kLocalCap);
             X32[xpad(pre + r)] = k[j];
         }
         __syncthreads();
@@ -561,6 +568,7 @@ static __device__ __forceinline__ void cta_lsd_sort(LocalSmem& S, uint32_t n, in
             const uint32_t d = (uint32_t)(k[j] >> sh) & (kLsdDigits - 1);
             const uint32_t pre = (S.cnt[d * 272u + pp] >> half) & 0xffffu;
             const uint32_t r = (rk[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
+            PRG_DCHECK(pre + r < (uint32_t)kLocalCap);
             S.X[xpad(pre + r)] = k[j];
         }
         __syncthreads();
@@ -595,8 +603,10 @@ __global__ void __launch_bounds__(kLocalThreads, 2)
         if (n > (uint32_t)kLocalCap) {
             // Only segments with no key bits left can exceed the cap: all keys
             // are equal, so the segment is already sorted.
+            const uint64_t first = src[sg.start];
             for (uint32_t i = threadIdx.x; i < n; i += kLocalThreads) {
                 const uint64_t k = src[sg.start + i];
+                PRG_DCHECK((k >> payload_bits) == (first >> payload_bits));
                 dst.store(sg.start + i, k, i > 0, k);
             }
             continue;

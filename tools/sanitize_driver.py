@@ -7,6 +7,10 @@ and the streamed K1 — checked against the oracle so a sanitizer run also
 proves the results unchanged.
 
     compute-sanitizer --tool memcheck python tools/sanitize_driver.py [scale]
+
+Compute-sanitizer is closed on this GPU pool; tests/test_checked.py runs this
+driver against the checked library instead (PRG_LIB=build/libprg_checked.so,
+device-side PRG_DCHECK bounds / invariant checks) and requires zero failures.
 """
 import os
 import sys
@@ -60,7 +64,11 @@ def main(scale):
         a = prpipe.read_edges(prpipe.sort_edges(man, os.path.join(d, "mem")))
         b = prpipe.read_edges(prpipe.sort_edges(man, os.path.join(d, "ext"), memory_budget_bytes=4096))
         assert a == b
-    print(f"sanitize driver ok: S={scale}")
+    # checked builds (PRG_LIB=build/libprg_checked.so): no device-side bounds /
+    # invariant check may have failed on any path above
+    fails = capi.lib().prg_debug_check_failures()
+    assert fails == 0, f"{fails} device-side checks failed"
+    print(f"sanitize driver ok: S={scale} (checked library: {capi.LIB_PATH.endswith('libprg_checked.so')})")
 
 
 if __name__ == "__main__":

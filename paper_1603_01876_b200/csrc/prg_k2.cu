@@ -14,7 +14,7 @@
 //   A  read edges once (TMA ring, 2048-edge tiles): validate labels and order,
 //      count unique (u,v), warp-aggregated d_in atomics
 //   -  max(d_in), keep bitmask (N bits)
-//   B  read edges again (4096-edge tiles, one per CTA): keep-bit gather, in-tile run lengths / row sums in SMEM,
+//   B  read edges again (2048-edge tiles, one per CTA): keep-bit gather, in-tile run lengths / row sums in SMEM,
 //      kept-entry positions by decoupled look-back, write cols/values/row offsets
 //   F  fix-ups for the few rows that span tiles (run continuation counts, then
 //      divide those rows by their row sums accumulated across tiles)
@@ -24,8 +24,16 @@ namespace prg {
 
 namespace {
 
-constexpr int kT = 512;         // threads per CTA
-constexpr int kI = 8;           // edges per thread
+#ifndef PRG_K2B_T  // pass-B shape, S=24 (pass B / whole CSR filter): 512x8 3.66 / 6.22 ms, 512x16 4.79,
+                   // 512x4 3.52 / 6.20, 256x8 3.47 / 6.15, 256x4 3.32 / 6.17 (more tile-spanning rows
+                   // to fix up), 128x8 3.56 / 6.42, 128x16 5.21 (tools/build_variant.py)
+#define PRG_K2B_T 256
+#endif
+#ifndef PRG_K2B_I
+#define PRG_K2B_I 8
+#endif
+constexpr int kT = PRG_K2B_T;   // threads per CTA
+constexpr int kI = PRG_K2B_I;   // edges per thread
 constexpr int kTE = kT * kI;    // edges per tile
 
 // SMEM arrays indexed by tile position are padded one word per 32: the

@@ -27,8 +27,11 @@
 
 namespace prg::sort {
 
+#ifndef PRG_SORT_ITEMS  // keys per thread of a global-level tile (A/B: tools/build_variant.py;
+#define PRG_SORT_ITEMS 16  // 8 measured K1 10.87 vs 10.17 ms, transpose levels 3.06 vs 2.80 ms)
+#endif
 constexpr int kTileThreads = 512;
-constexpr int kTileItems = 16;
+constexpr int kTileItems = PRG_SORT_ITEMS;
 constexpr int kTile = kTileThreads * kTileItems;  // 8192 keys per global tile
 constexpr int kRadix = 256;
 constexpr int kLocalCap = 8192;       // keys per SMEM-resident segment

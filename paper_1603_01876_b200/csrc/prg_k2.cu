@@ -527,7 +527,6 @@ __global__ void __launch_bounds__(kST) k2_pass_a_tma(const longlong2* __restrict
     extern __shared__ __align__(128) unsigned char smem_raw[];
     longlong2* stages = reinterpret_cast<longlong2*>(smem_raw);
     __shared__ Ring<kStages> R;
-    __shared__ longlong2 before;
     __shared__ uint32_t red[kSW];
     const unsigned lane = dev::lane_id(), w = dev::warp_id();
     const uint64_t pol = dev::policy_evict_first();
@@ -539,9 +538,9 @@ __global__ void __launch_bounds__(kST) k2_pass_a_tma(const longlong2* __restrict
         if (t >= ntiles) break;
         const int64_t base = (int64_t)t * kSE;
         const int cnt = (int)min((int64_t)kSE, m - base);
-        if (threadIdx.x == 0) before = base > 0 ? uv[base - 1] : make_longlong2(0, 0);
-        dev::mbar_wait(&R.bar[slot], (i / kStages) & 1u);
-        __syncthreads();  // `before` visible
+        // warp 0 needs the edge before the tile (all lanes load the same address)
+        const longlong2 before = (w == 0 && base > 0) ? uv[base - 1] : make_longlong2(0, 0);
+        dev::mbar_wait(&R.bar[slot], (i / kStages) & 1u);  // acquire: the stage is visible to this thread
         const longlong2* tl = stages + (size_t)slot * kSE;
         const int c0 = (int)w * 32 * kSR;
         longlong2 carry = c0 > 0 ? tl[c0 - 1] : before;  // the edge before this warp's first
@@ -631,7 +630,10 @@ uint32_t k2_filter_device(const int64_t* d_uv, int64_t m, int64_t n, prg_matrix*
     if (v1 < 0) { const char* e = getenv("PRG_K2_V1"); v1 = e ? atoi(e) : 0; }
     static int ctas = -1;   // PRG_K2_CTAS: persistent CTAs per SM of the TMA-ring passes
     if (ctas < 0) { const char* e = getenv("PRG_K2_CTAS"); ctas = e ? atoi(e) : 3; }
-    constexpr int kStagesA = 3;
+#ifndef PRG_K2A_STAGES
+#define PRG_K2A_STAGES 3
+#endif
+    constexpr int kStagesA = PRG_K2A_STAGES;
     const uint32_t ntiles_s = div_up((uint64_t)m, kSE);
     // persistent grid: min(PRG_K2_CTAS, resident CTAs) per SM
     auto grid_for = [&](const void* fn, size_t smem) {

@@ -461,7 +461,22 @@ __global__ void k2_fix_rows(const uint32_t* __restrict__ fix_rows, const uint64_
         const uint32_t b = row_offsets[r] + c * kFixChunk;
         const uint32_t e = min(row_offsets[r + 1], b + kFixChunk);
         const double d = (double)dout_f[r];
-        for (uint32_t p = b + lane; p < e; p += 32) values[p] = values[p] / d;
+        const double inv = 1.0 / d;  // count 1 -> 1/d_out: the same IEEE division as c / d
+        // 8 entries per lane in flight (a dependent load -> divide -> store per
+        // step left the kernel latency-bound: 0.39 ms at S=24)
+        for (uint32_t p0 = b + lane; p0 < e; p0 += 32 * 8) {
+            double v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const uint32_t p = p0 + 32 * k;
+                v[k] = p < e ? values[p] : 0.0;
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const uint32_t p = p0 + 32 * k;
+                if (p < e) values[p] = v[k] == 1.0 ? inv : v[k] / d;
+            }
+        }
     }
 }
 

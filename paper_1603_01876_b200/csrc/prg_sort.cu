@@ -15,82 +15,103 @@ namespace prg::sort {
 // count of final segments (and their fixed per-segment cost) low. Children
 // larger than the cap become active for the next level (or final, if no key
 // bits are left: all their keys are equal).
-// Two passes over the children by one thread: the first only counts what will
-// be emitted, one atomic per list reserves the slots, the second writes them
-// (a returning atomic per emitted segment serialised ~1 us each).
+// The greedy packing (next fit, in key order) is sequential, so thread 0 only
+// walks the child sizes and marks, per child, "starts a run" (with the run's
+// size once it closes) or "too large" — a tight register loop; the block then
+// counts the emitted segments per thread, reserves list slots with one atomic
+// per list and writes the segments in parallel. (One thread emitting every
+// segment left the rest of the block waiting: barrier stalls 47%, 50-80 us per
+// level launch.)
 __device__ uint32_t g_coalesce_max = kLocalCap;
 
-template <bool kWrite>
-__device__ __forceinline__ void emit_pass(const uint64_t* child_start, const uint32_t* child_size, int nchild,
-                                          uint8_t buf, int next_shift, int next_bits, Seg* __restrict__ next,
-                                          uint32_t& i_next, Seg* __restrict__ fin, uint32_t& i_fin) {
-    Seg run;
-    run.size = 0;
-    run.buf = buf;
-    run.bits = 0;
-    run.shift = 0;
-    run.start = 0;
-    for (int d = 0; d < nchild; ++d) {
-        const uint32_t sz = child_size[d];
-        if (sz == 0) continue;
-        if (sz > (uint32_t)kLocalCap) {
-            if (run.size) {
-                if (kWrite) fin[i_fin] = run;
-                ++i_fin;
-                run.size = 0;
+struct EmitScratch {
+    uint8_t kind[kRadix];   // 0: joins the open run or empty, 1: starts a run, 2: larger than the cap
+    uint32_t rsz[kRadix];   // run size, at the run's first child
+    uint32_t scan[kRadix / 32 + 1];
+    uint32_t base_fin, base_next;
+};
+
+__device__ void emit_children_block(const uint64_t* child_start, const uint32_t* child_size, int nchild, uint8_t buf,
+                                    int next_shift, int next_bits, Seg* __restrict__ next,
+                                    uint32_t* __restrict__ n_next, Seg* __restrict__ fin,
+                                    uint32_t* __restrict__ n_fin, EmitScratch& E) {
+    const uint32_t cap = (uint32_t)kLocalCap, cmax = g_coalesce_max;
+    if (threadIdx.x == 0) {
+        uint32_t run = 0;
+        int rs = 0;
+        for (int d = 0; d < nchild; ++d) {
+            const uint32_t sz = child_size[d];
+            uint8_t k = 0;
+            if (sz > cap) {
+                if (run) { E.rsz[rs] = run; run = 0; }
+                k = 2;
+            } else if (sz) {
+                // PRG_COALESCE_MAX (measurement knob): children at least this large are
+                // not joined. Keeping K1's ~2.9 K-key level-2 children apart (all on the
+                // 32-bit merge path) measured slower — K1 local 5.58 vs 4.94 ms, the K3
+                // transpose's 3.11 vs 2.23 ms: a segment costs ~3.5 K cycles per merge
+                // level whatever its size, so fewer, fuller segments win.
+                if (run && (run + sz > cap || sz >= cmax || run >= cmax)) { E.rsz[rs] = run; run = 0; }
+                if (run == 0) { rs = d; k = 1; }
+                run += sz;
             }
-            Seg ch;
-            ch.start = child_start[d];
-            ch.size = sz;
-            ch.buf = buf;
-            ch.bits = (uint8_t)next_bits;
-            ch.shift = (uint16_t)next_shift;
-            if (next_bits == 0) {
-                // no bits left: the keys are equal above the payload, so the
-                // child is already in order — hand it out in cap-sized pieces
-                // so no single CTA streams a huge run.
-                const uint32_t np = (sz + kLocalCap - 1) / kLocalCap;
-                if (kWrite)
-                    for (uint32_t q = 0; q < np; ++q) {
-                        Seg p = ch;
-                        p.start = ch.start + (uint64_t)q * kLocalCap;
-                        p.size = min((uint32_t)kLocalCap, sz - q * (uint32_t)kLocalCap);
-                        fin[i_fin + q] = p;
-                    }
-                i_fin += np;
-            } else {
-                if (kWrite) next[i_next] = ch;
-                ++i_next;
-            }
+            E.kind[d] = k;
+        }
+        if (run) E.rsz[rs] = run;
+    }
+    __syncthreads();
+    // what this thread's children emit (children tid, tid + blockDim, ...)
+    uint32_t nf = 0, nn = 0;
+    for (int d = threadIdx.x; d < nchild; d += blockDim.x) {
+        const uint8_t k = E.kind[d];
+        if (k == 1) ++nf;
+        else if (k == 2) {
+            if (next_bits) ++nn;
+            else nf += (child_size[d] + cap - 1) / cap;
+        }
+    }
+    uint32_t tf, tn;
+    uint32_t of = dev::block_excl_scan(nf, E.scan, tf);
+    uint32_t on = dev::block_excl_scan(nn, E.scan, tn);
+    if (threadIdx.x == 0) {
+        E.base_fin = tf ? atomicAdd(n_fin, tf) : 0u;
+        E.base_next = tn ? atomicAdd(n_next, tn) : 0u;
+    }
+    __syncthreads();
+    of += E.base_fin;
+    on += E.base_next;
+    for (int d = threadIdx.x; d < nchild; d += blockDim.x) {
+        const uint8_t k = E.kind[d];
+        if (k == 0) continue;
+        Seg sg;
+        sg.start = child_start[d];
+        sg.buf = buf;
+        if (k == 1) {
+            sg.size = E.rsz[d];
+            sg.bits = 0;
+            sg.shift = 0;
+            fin[of++] = sg;
             continue;
         }
-        // PRG_COALESCE_MAX (measurement knob): children at least this large are
-        // not joined. Keeping K1's ~2.9 K-key level-2 children apart (all on the
-        // 32-bit merge path) measured slower — K1 local 5.58 vs 4.94 ms, the K3
-        // transpose's 3.11 vs 2.23 ms: a segment costs ~3.5 K cycles per merge
-        // level whatever its size (latency-bound chains), so fewer, fuller
-        // segments win.
-        if (run.size && (run.size + sz > (uint32_t)kLocalCap || sz >= g_coalesce_max || run.size >= g_coalesce_max)) {
-            if (kWrite) fin[i_fin] = run;
-            ++i_fin;
-            run.size = 0;
+        const uint32_t sz = child_size[d];
+        sg.size = sz;
+        sg.bits = (uint8_t)next_bits;
+        sg.shift = (uint16_t)next_shift;
+        if (next_bits) {
+            next[on++] = sg;
+        } else {
+            // no bits left: the keys are equal above the payload, so the child is
+            // already in order — handed out in cap-sized pieces so no single CTA
+            // streams a huge run
+            const uint32_t np = (sz + cap - 1) / cap;
+            for (uint32_t q = 0; q < np; ++q) {
+                Seg pc = sg;
+                pc.start = sg.start + (uint64_t)q * cap;
+                pc.size = min(cap, sz - q * cap);
+                fin[of++] = pc;
+            }
         }
-        if (run.size == 0) run.start = child_start[d];
-        run.size += sz;
     }
-    if (run.size) {
-        if (kWrite) fin[i_fin] = run;
-        ++i_fin;
-    }
-}
-
-__device__ void emit_children(const uint64_t* child_start, const uint32_t* child_size, int nchild,
-                              uint8_t buf, int next_shift, int next_bits, Seg* __restrict__ next,
-                              uint32_t* __restrict__ n_next, Seg* __restrict__ fin, uint32_t* __restrict__ n_fin) {
-    uint32_t cn = 0, cf = 0;
-    emit_pass<false>(child_start, child_size, nchild, buf, next_shift, next_bits, next, cn, fin, cf);
-    uint32_t i_next = cn ? atomicAdd(n_next, cn) : 0u, i_fin = cf ? atomicAdd(n_fin, cf) : 0u;
-    emit_pass<true>(child_start, child_size, nchild, buf, next_shift, next_bits, next, i_next, fin, i_fin);
 }
 
 __global__ void classify_l1_kernel(const uint32_t* __restrict__ off, uint32_t ntiles, size_t n,
@@ -99,6 +120,7 @@ __global__ void classify_l1_kernel(const uint32_t* __restrict__ off, uint32_t nt
                                    uint32_t* __restrict__ n_fin) {
     __shared__ uint64_t cst[kRadix];
     __shared__ uint32_t csz[kRadix];
+    __shared__ EmitScratch E;
     const int d = threadIdx.x;
     if (d < kRadix) {
         const uint64_t st = off[(size_t)d * ntiles];
@@ -107,7 +129,7 @@ __global__ void classify_l1_kernel(const uint32_t* __restrict__ off, uint32_t nt
         csz[d] = (uint32_t)(en - st);
     }
     __syncthreads();
-    if (threadIdx.x == 0) emit_children(cst, csz, kRadix, 1, shift - bits, bits, next, n_next, fin, n_fin);
+    emit_children_block(cst, csz, kRadix, 1, shift - bits, bits, next, n_next, fin, n_fin, E);
 }
 
 __global__ void build_tiles_kernel(const Seg* __restrict__ active, const uint32_t* __restrict__ n_active,
@@ -291,6 +313,7 @@ __global__ void classify_kernel(const Seg* __restrict__ active, const uint32_t* 
                                 uint32_t* __restrict__ n_fin, int floor_bit) {
     __shared__ uint64_t cst[kRadix];
     __shared__ uint32_t csz[kRadix];
+    __shared__ EmitScratch E;
     const uint32_t na = *n_active;
     for (uint32_t si = blockIdx.x; si < na; si += gridDim.x) {
         const Seg sg = active[si];
@@ -305,11 +328,9 @@ __global__ void classify_kernel(const Seg* __restrict__ active, const uint32_t* 
             csz[d] = (uint32_t)(en - st);
         }
         __syncthreads();
-        if (threadIdx.x == 0) {
-            const int rem = sg.shift - floor_bit;
-            const int nb = rem >= 8 ? 8 : rem;
-            emit_children(cst, csz, nd, (uint8_t)(sg.buf ^ 1), sg.shift - nb, nb, next, n_next, fin, n_fin);
-        }
+        const int rem = sg.shift - floor_bit;
+        const int nb = rem >= 8 ? 8 : rem;
+        emit_children_block(cst, csz, nd, (uint8_t)(sg.buf ^ 1), sg.shift - nb, nb, next, n_next, fin, n_fin, E);
         __syncthreads();
     }
 }

@@ -1,5 +1,6 @@
 // prg_runtime.cu — error channel, stream-ordered workspace, device-wide scan.
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 #include <cstring>
 #include <map>
@@ -252,10 +253,118 @@ __global__ void copy_total_kernel(const uint64_t* partial, size_t nb, Out* total
     *total = static_cast<Out>(partial[nb]);
 }
 
+// Single-pass variant (decoupled look-back): one launch per scan instead of
+// reduce + partials + down (+ total). Tiles are claimed in launch order from a
+// counter; each publishes its aggregate, warp 0 sums predecessors' aggregates
+// back to the nearest inclusive prefix, then the tile is written. Most of the
+// pipeline's ~16 scans per step are launch-latency bound.
+constexpr uint64_t kScanAgg = 1ull << 62, kScanInc = 2ull << 62, kScanVal = (1ull << 62) - 1;
+template <class Out>
+__global__ void __launch_bounds__(kScanThreads) scan_onepass_kernel(const uint32_t* __restrict__ in, size_t n,
+                                                                    const uint32_t* dn, uint32_t mult,
+                                                                    unsigned long long* __restrict__ status,
+                                                                    uint32_t* __restrict__ counter,
+                                                                    Out* __restrict__ out, Out* __restrict__ total) {
+    __shared__ uint64_t warp_tot[33];
+    __shared__ uint32_t s_tile;
+    __shared__ uint64_t s_excl;
+    n = scan_len(n, dn, mult);
+    const uint32_t ntiles = (uint32_t)((n + kScanTile - 1) / kScanTile);
+    if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
+    __syncthreads();
+    const uint32_t t = s_tile;
+    if (t >= ntiles) {
+        if (ntiles == 0 && t == 0 && total && threadIdx.x == 0) *total = 0;
+        return;
+    }
+    const size_t base = (size_t)t * kScanTile;
+    uint32_t v[kScanItems];
+    const size_t my = base + (size_t)threadIdx.x * kScanItems;
+    const bool vec = my + kScanItems <= n && ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+    if (vec) {
+        const uint4 a = reinterpret_cast<const uint4*>(in + my)[0], b = reinterpret_cast<const uint4*>(in + my)[1];
+        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    } else {
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k) v[k] = (my + k < n) ? in[my + k] : 0u;
+    }
+    uint64_t tsum = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) tsum += v[k];
+    const uint64_t inc = dev::warp_incl_scan(tsum);
+    if (dev::lane_id() == 31) warp_tot[dev::warp_id()] = inc;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const uint64_t x = warp_tot[threadIdx.x];
+        const uint64_t xi = dev::warp_incl_scan(x);
+        warp_tot[threadIdx.x] = xi - x;
+        if (threadIdx.x == 31) warp_tot[32] = xi;
+        __syncwarp();
+        const uint64_t agg = warp_tot[32];
+        if (threadIdx.x == 0) atomicExch(&status[t], (t == 0 ? kScanInc : kScanAgg) | agg);
+        uint64_t excl = 0;
+        if (t != 0) {
+            for (int64_t k = (int64_t)t - 1;; k -= 32) {
+                const int64_t idx = k - (int64_t)threadIdx.x;
+                uint64_t st = kScanInc;  // below tile 0: an empty inclusive prefix
+                if (idx >= 0) {
+                    do {
+                        st = *((volatile unsigned long long*)&status[idx]);
+                    } while ((st & ~kScanVal) == 0);
+                }
+                const unsigned incm = __ballot_sync(0xffffffffu, (st & ~kScanVal) == kScanInc);
+                const int first = incm ? __ffs(incm) - 1 : 32;
+                uint64_t w = (int)threadIdx.x <= first ? (st & kScanVal) : 0ull;
+#pragma unroll
+                for (int d = 16; d > 0; d >>= 1) w += __shfl_xor_sync(0xffffffffu, w, d);
+                excl += w;
+                if (incm) break;
+            }
+            if (threadIdx.x == 0) atomicExch(&status[t], kScanInc | (excl + agg));
+        }
+        if (threadIdx.x == 0) {
+            s_excl = excl;
+            if (total && t + 1 == ntiles) *total = static_cast<Out>(excl + agg);
+        }
+    }
+    __syncthreads();
+    uint64_t run = s_excl + warp_tot[dev::warp_id()] + inc - tsum;
+    alignas(16) Out o[kScanItems];
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        o[k] = static_cast<Out>(run);
+        run += v[k];
+    }
+    if (vec) {
+        uint4* d = reinterpret_cast<uint4*>(out + my);
+        constexpr int kVec = kScanItems * (int)sizeof(Out) / 16;
+#pragma unroll
+        for (int q = 0; q < kVec; ++q) {
+            uint4 w;
+            memcpy(&w, reinterpret_cast<const char*>(o) + 16 * q, 16);
+            d[q] = w;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k)
+            if (my + k < n) out[my + k] = o[k];
+    }
+}
+
 template <class Out>
 void scan_impl(const uint32_t* in, Out* out, size_t n, Out* total, cudaStream_t s, const uint32_t* dn = nullptr,
                uint32_t mult = 1) {
     const size_t nb = n ? (n + kScanTile - 1) / kScanTile : 0;
+    static int two_pass = -1;  // PRG_SCAN_2PASS=1: reduce-then-scan (A/B knob)
+    if (two_pass < 0) { const char* e = getenv("PRG_SCAN_2PASS"); two_pass = e ? atoi(e) : 0; }
+    if (!two_pass) {
+        DevBuf<unsigned long long> st(nb + 1, s);  // tile status words, then the tile counter
+        PRG_CUDA(cudaMemsetAsync(st.get(), 0, (nb + 1) * sizeof(unsigned long long), s));
+        scan_onepass_kernel<Out><<<(unsigned)std::max<size_t>(nb, 1), kScanThreads, 0, s>>>(
+            in, n, dn, mult, st.get(), reinterpret_cast<uint32_t*>(st.get() + nb), out, total);
+        PRG_LAUNCH_CHECK();
+        return;
+    }
     DevBuf<uint64_t> part(nb + 1, s);
     if (nb) {
         scan_reduce_kernel<<<(unsigned)nb, kScanThreads, 0, s>>>(in, n, dn, mult, part.get());

@@ -136,11 +136,15 @@ __global__ void build_tiles_kernel(const Seg* __restrict__ active, const uint32_
                                    uint32_t* __restrict__ seg_tile0, uint64_t* __restrict__ seg_elem0,
                                    uint32_t* __restrict__ tile_seg, uint32_t* __restrict__ tile_idx,
                                    uint32_t* __restrict__ n_tiles, uint32_t max_tiles) {
-    // Single block, 1024 threads: sequential chunks of 1024 segments.
+    // Single block, 1024 threads: sequential chunks of 1024 segments. The tile
+    // map of a chunk is written by all threads (tile q of the chunk finds its
+    // segment by binary search): one thread per segment writing its own tiles
+    // left a 1 M-key segment's 128 tiles on one thread.
     __shared__ uint32_t carry_t;
     __shared__ uint64_t carry_e;
     __shared__ uint32_t wt[33];
     __shared__ uint64_t we[33];
+    __shared__ uint32_t st0[1025];  // chunk-relative first tile of each segment (+ chunk total)
     const uint32_t na = *n_active;
     if (threadIdx.x == 0) { carry_t = 0; carry_e = 0; }
     __syncthreads();
@@ -163,14 +167,28 @@ __global__ void build_tiles_kernel(const Seg* __restrict__ active, const uint32_
             if (threadIdx.x == 31) { wt[32] = xi; we[32] = yi; }
         }
         __syncthreads();
-        const uint32_t t0 = carry_t + wt[dev::warp_id()] + it - nt;
+        const uint32_t rel = wt[dev::warp_id()] + it - nt;
+        const uint32_t t0 = carry_t + rel;
         const uint64_t e0 = carry_e + we[dev::warp_id()] + ie - ne;
+        st0[threadIdx.x] = rel;  // rows past na hold the chunk total (nt = 0)
+        if (threadIdx.x == 0) st0[blockDim.x] = wt[32];
         if (i < na) {
             seg_tile0[i] = t0;
             seg_elem0[i] = e0;
-            for (uint32_t k = 0; k < nt && t0 + k < max_tiles; ++k) {
-                tile_seg[t0 + k] = i;
-                tile_idx[t0 + k] = k;
+        }
+        __syncthreads();
+        const uint32_t chunk_tiles = wt[32];
+        const uint32_t nseg = min((uint32_t)blockDim.x, na - base);
+        for (uint32_t q = threadIdx.x; q < chunk_tiles; q += blockDim.x) {
+            uint32_t lo = 0, hi = nseg - 1;  // last segment with st0 <= q
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi + 1) >> 1;
+                if (st0[mid] <= q) lo = mid; else hi = mid - 1;
+            }
+            const uint32_t g = carry_t + q;
+            if (g < max_tiles) {
+                tile_seg[g] = base + lo;
+                tile_idx[g] = q - st0[lo];
             }
         }
         __syncthreads();

@@ -14,7 +14,7 @@
 //   A  read edges once (TMA ring, 2048-edge tiles): validate labels and order,
 //      count unique (u,v), warp-aggregated d_in atomics
 //   -  max(d_in), keep bitmask (N bits)
-//   B  read edges again (2048-edge tiles, one per CTA): keep-bit gather, in-tile run lengths / row sums in SMEM,
+//   B  read edges again (1536-edge tiles, one per CTA): keep-bit gather, in-tile run lengths / row sums in SMEM,
 //      kept-entry positions by decoupled look-back, write cols/values/row offsets
 //   F  fix-ups for the few rows that span tiles (run continuation counts, then
 //      divide those rows by their row sums accumulated across tiles)
@@ -24,13 +24,15 @@ namespace prg {
 
 namespace {
 
-#ifndef PRG_K2B_T  // pass-B shape, S=24 (pass B / whole CSR filter): 512x8 3.66 / 6.22 ms, 512x16 4.79,
-                   // 512x4 3.52 / 6.20, 256x8 3.47 / 6.15, 256x4 3.32 / 6.17 (more tile-spanning rows
-                   // to fix up), 128x8 3.56 / 6.42, 128x16 5.21 (tools/build_variant.py)
+#ifndef PRG_K2B_T  // pass-B shape, S=24 (pass B / whole CSR filter; fix-ups as of their round-1 form):
+                   // 512x8 3.66 / 6.22 ms, 512x16 4.79, 512x4 3.52 / 6.20, 256x8 3.47 / 6.15,
+                   // 256x4 3.32 / 6.17 (more tile-spanning rows to fix up), 128x8 3.56 / 6.42,
+                   // 128x16 5.21; after the fix-up rework: 256x8 3.48 / 5.97, 256x6 3.30 / 5.84,
+                   // 384x8 3.60, 192x8 3.51, 256x12 3.92 (tools/build_variant.py)
 #define PRG_K2B_T 256
 #endif
 #ifndef PRG_K2B_I
-#define PRG_K2B_I 8
+#define PRG_K2B_I 6
 #endif
 constexpr int kT = PRG_K2B_T;   // threads per CTA
 constexpr int kI = PRG_K2B_I;   // edges per thread

@@ -357,6 +357,16 @@ __global__ void classify_kernel(const Seg* __restrict__ active, const uint32_t* 
 // Host side
 // ---------------------------------------------------------------------------
 size_t local_smem_bytes() { return sizeof(LocalSmem); }
+int sort_grid_mult(int which) {
+    static int g1 = -1, g2 = -1;
+    if (g1 < 0) {
+        const char* e1 = getenv("PRG_SORT_GRID1");
+        const char* e2 = getenv("PRG_SORT_GRID2");
+        g1 = e1 ? std::max(1, atoi(e1)) : 4;
+        g2 = e2 ? std::max(1, atoi(e2)) : 4;
+    }
+    return which == 1 ? g1 : g2;
+}
 int local_merge_span() {
     static int v = -1;
     if (v < 0) { const char* e = getenv("PRG_MERGE_SPAN"); v = e ? atoi(e) : 16; }
@@ -402,7 +412,7 @@ void run_segmented_levels(SortWorkspace& ws, int levels_left, int floor_bit, boo
                                       (int)((size_t)kTile * sizeof(uint64_t) + kStableScratch)));
         attr_set = true;
     }
-    const unsigned grid = (unsigned)num_sms() * 4;
+    const unsigned grid = (unsigned)num_sms() * sort_grid_mult(2);
     uint32_t* cnt = ws.counters.get();
     for (int lvl = 0; lvl < levels_left; ++lvl) {
         const int a = lvl & 1;

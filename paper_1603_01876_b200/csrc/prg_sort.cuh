@@ -655,6 +655,7 @@ struct SortWorkspace {
 void sort_workspace_init(SortWorkspace& ws, size_t n, cudaStream_t s);
 size_t local_smem_bytes();
 int local_merge_span();  // PRG_MERGE_SPAN (default 16): see cta_lsd_sort
+int sort_grid_mult(int which);  // CTAs per SM of the level-1 (1) / segmented (2) tile kernels: PRG_SORT_GRID1/2
 
 // Runs levels >= 2 until every segment is final; then the caller launches
 // local_sort_kernel with its Dst. `key_bits` is the number of significant bits.
@@ -679,7 +680,7 @@ void msd_sort_split(Src src_hist, Src src_scat, size_t n, int key_bits, Dst dst,
     const int shift1 = key_bits - bits1 > payload_bits ? key_bits - bits1 : payload_bits;
     const unsigned dmask = (1u << bits1) - 1u;
     const uint32_t ntiles = div_up(n, kTile);
-    const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)num_sms() * 4);
+    const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)num_sms() * sort_grid_mult(1));
     PRG_CUDA(cudaMemsetAsync(ws.counters.get(), 0, kCounters * sizeof(uint32_t), s));
     {
         ProfScope prof(t + "_l1_hist", s);

@@ -20,6 +20,11 @@ struct PairKeySrc {
     uint32_t* err;
     static constexpr size_t kSmem = 0;
     static constexpr int kHistBatch = 4;
+    static constexpr bool kRegPrefetch = false;  // 16-byte pairs: 16 raw pairs per thread do not fit in registers
+    static constexpr bool kL2Prefetch = true;
+    __device__ __forceinline__ void prefetch_l2(size_t i) const {
+        if ((threadIdx.x & 1u) == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(uv + i));  // one per 32-byte sector
+    }
     __device__ __forceinline__ void prepare(size_t, int, void*) const {}
     __device__ __forceinline__ uint64_t key(size_t i, int, const void*) const {
         const longlong2 p = uv[i];

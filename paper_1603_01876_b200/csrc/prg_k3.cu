@@ -90,6 +90,9 @@ struct RowClassSrc {
     int fb;
     static constexpr size_t kSmem = 0;
     static constexpr int kHistBatch = 16;
+    static constexpr bool kRegPrefetch = false;
+    static constexpr bool kL2Prefetch = false;
+    __device__ void prefetch_l2(size_t) const {}
     __device__ void prepare(size_t, int, void*) const {}
     __device__ __forceinline__ uint64_t key(size_t i, int, const void*) const {
         const uint32_t d = ro[i + 1] - ro[i];
@@ -608,6 +611,9 @@ struct VcClassSrc {
     uint32_t vcmax;
     static constexpr size_t kSmem = 0;
     static constexpr int kHistBatch = 16;
+    static constexpr bool kRegPrefetch = false;
+    static constexpr bool kL2Prefetch = false;
+    __device__ void prefetch_l2(size_t) const {}
     __device__ void prepare(size_t, int, void*) const {}
     __device__ __forceinline__ uint64_t key(size_t i, int, const void*) const {
         if (csc_idx) {
@@ -626,6 +632,11 @@ struct KeyArraySrc {
     const unsigned long long* keys;
     static constexpr size_t kSmem = 0;
     static constexpr int kHistBatch = 16;
+    static constexpr bool kRegPrefetch = true;
+    static constexpr bool kL2Prefetch = true;
+    __device__ __forceinline__ void prefetch_l2(size_t i) const {
+        if ((threadIdx.x & 3u) == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(keys + i));  // one per 32-byte sector
+    }
     __device__ void prepare(size_t, int, void*) const {}
     __device__ __forceinline__ uint64_t key(size_t i, int, const void*) const { return keys[i]; }
 };

@@ -369,7 +369,12 @@ int sort_grid_mult(int which) {
 }
 int local_merge_span() {
     static int v = -1;
-    if (v < 0) { const char* e = getenv("PRG_MERGE_SPAN"); v = e ? atoi(e) : 16; }
+    if (v < 0) {
+        const char* e = getenv("PRG_MERGE_SPAN");
+        const char* w = getenv("PRG_WARP_LEVELS");  // merge levels done in registers by warp shuffles (0..5)
+        v = (e ? atoi(e) : 16) & 0x1ff;
+        v |= std::min(5, std::max(0, w ? atoi(w) : 5)) << 12;
+    }
     return v;
 }
 

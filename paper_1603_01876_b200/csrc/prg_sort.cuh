@@ -30,6 +30,9 @@ namespace prg::sort {
 #ifndef PRG_SORT_ITEMS  // keys per thread of a global-level tile (A/B: tools/build_variant.py;
 #define PRG_SORT_ITEMS 16  // 8 measured K1 10.87 vs 10.17 ms, transpose levels 3.06 vs 2.80 ms)
 #endif
+#ifndef PRG_SORT_PREFETCH  // global-level scatters load the next tile during the write-out (0: A/B)
+#define PRG_SORT_PREFETCH 1
+#endif
 constexpr int kTileThreads = 512;
 constexpr int kTileItems = PRG_SORT_ITEMS;
 constexpr int kTile = kTileThreads * kTileItems;  // 8192 keys per global tile
@@ -51,6 +54,9 @@ struct Seg {
 //   Src must provide:
 //     static constexpr size_t kSmem;   // bytes of tile scratch it needs
 //     static constexpr int kHistBatch; // keys loaded ahead in the histogram pass (divides 16)
+//     static constexpr bool kRegPrefetch; // key() is a plain load: the scatter may load the next tile early
+//     static constexpr bool kL2Prefetch;  // else: prefetch_l2(i) pulls key i's bytes into L2 (may be a no-op)
+//     __device__ void prefetch_l2(size_t i) const;
 //     __device__ void prepare(size_t base, int cnt, void* smem) const;  // all threads; may __syncthreads
 //     __device__ uint64_t key(size_t i, int li, const void* smem) const;  // li = i - base
 // ---------------------------------------------------------------------------
@@ -195,20 +201,35 @@ __global__ void __launch_bounds__(kTileThreads, 2) l1_scatter_kernel(Src src, si
     uint32_t* wc = reinterpret_cast<uint32_t*>(static_cast<unsigned char*>(src_smem) +
                                                (Src::kSmem >= kStableScratch ? 0 : ((Src::kSmem + 15) & ~size_t(15))));
     const unsigned dmask = (1u << bits) - 1u;
+    // Sources without tile scratch are software-pipelined: the next tile's 16
+    // loads are issued once this tile's keys sit in skeys (k is dead by then), so
+    // they are in flight during the write-out (ncu before: 63% long-scoreboard
+    // stalls, DRAM 42% — the load phase of a tile overlapped with nothing of its own CTA).
+    // Sources whose key() transforms what it loads (kRegPrefetch false) would
+    // stall on the transform: they only pull the next tile into L2 (prefetch_l2).
+    // The stable ranking has no registers to spare (the register form spilled: 1.52 -> 1.60 ms).
+    constexpr bool kPrefetch = PRG_SORT_PREFETCH && Src::kSmem == 0 && Src::kRegPrefetch && !kStable;
+    constexpr bool kPrefetchL2 = PRG_SORT_PREFETCH && !kPrefetch && Src::kL2Prefetch;
+    uint64_t k[kTileItems];
+    auto load_tile = [&](uint32_t tt) {
+        const size_t b = (size_t)tt * kTile;
+        const int c = (int)min((size_t)kTile, n - b);
+        // all 16 loads first (in flight together), then the counting
+#pragma unroll
+        for (int j = 0; j < kTileItems; ++j) {
+            const int li = tile_pos<kStable>(j);
+            if (li < c) k[j] = src.key(b + li, li, src_smem);
+        }
+    };
+    if (kPrefetch && blockIdx.x < ntiles) load_tile(blockIdx.x);
     for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         if (!kStable)
             for (int i = threadIdx.x; i < kRadix; i += blockDim.x) h[i] = 0;
         const size_t base = (size_t)t * kTile;
         const int cnt = (int)min((size_t)kTile, n - base);
-        src.prepare(base, cnt, src_smem);
+        if (!kPrefetch) src.prepare(base, cnt, src_smem);
         __syncthreads();
-        uint64_t k[kTileItems];
-        // all 16 loads first (in flight together), then the counting
-#pragma unroll
-        for (int j = 0; j < kTileItems; ++j) {
-            const int li = tile_pos<kStable>(j);
-            if (li < cnt) k[j] = src.key(base + li, li, src_smem);
-        }
+        if (!kPrefetch) load_tile(t);
         if (!kStable) {
 #pragma unroll
             for (int j = 0; j < kTileItems; ++j)
@@ -237,6 +258,16 @@ __global__ void __launch_bounds__(kTileThreads, 2) l1_scatter_kernel(Src src, si
                 }
             }
             __syncthreads();
+        }
+        if (kPrefetch && t + gridDim.x < ntiles) load_tile(t + gridDim.x);
+        if (kPrefetchL2 && t + gridDim.x < ntiles) {
+            const size_t b = (size_t)(t + gridDim.x) * kTile;
+            const int c = (int)min((size_t)kTile, n - b);
+#pragma unroll
+            for (int j = 0; j < kTileItems; ++j) {
+                const int li = tile_pos<kStable>(j);
+                if (li < c) src.prefetch_l2(b + li);
+            }
         }
         for (int i = threadIdx.x; i < cnt; i += kTileThreads) {
             uint64_t key = skeys[i];
@@ -432,9 +463,72 @@ __device__ __forceinline__ void sort16(K (&k)[kLocalItems]) {
 // well was slower (5.34 ms), and so were two interleaved merge paths per thread
 // (5.47 ms) — the levels are issue/bank-conflict bound, not chain-latency bound. X is the xpad-indexed slot array of K (K = u32: the key window >> lo).
 // On return S.X holds the sorted full keys.
+// The first merge levels inside a warp, in registers: lane l holds the sorted
+// keys [16l, 16l+16) of the warp's 512 slots. Level m (1..5) merges runs of
+// 2^(m-1) lanes into runs of 2^m lanes as a bitonic merge: slot i of the lower
+// run against slot L-1-i of the upper run (lane ^ (2^m - 1), register 15-j),
+// then half-cleaners over lane distances 2^(m-2) .. 1 (same register) and over
+// register strides 8 .. 1. No shared memory, no block barrier. `left` = the slots
+// of this warp's 512 that hold keys to sort (the rest are all ones); only the
+// levels that cover them run. Returns the run length reached (16 << levels).
+template <class K>
+__device__ __forceinline__ K shfl_xor_key(K v, int d) {
+    if constexpr (sizeof(K) == 8) {
+        const uint32_t lo = __shfl_xor_sync(0xffffffffu, (uint32_t)v, d);
+        const uint32_t hi = __shfl_xor_sync(0xffffffffu, (uint32_t)(v >> 32), d);
+        return ((K)hi << 32) | lo;
+    } else {
+        return __shfl_xor_sync(0xffffffffu, v, d);
+    }
+}
+template <class K>
+__device__ __forceinline__ uint32_t warp_bitonic_merge(K (&k)[kLocalItems], uint32_t left, int max_levels) {
+    const unsigned lane = threadIdx.x & 31u;
+    uint32_t run = kLocalItems;
+#pragma unroll
+    for (int m = 1; m <= 5; ++m) {
+        if (m > max_levels || run >= left) break;  // warp-uniform
+        {
+            const bool up = (lane >> (m - 1)) & 1u;
+#pragma unroll
+            for (int j = 0; j < kLocalItems / 2; ++j) {  // registers j and 15-j trade places across the pair of lanes
+                const K a = k[j], b = k[kLocalItems - 1 - j];
+                const K oa = shfl_xor_key<K>(b, (1 << m) - 1), ob = shfl_xor_key<K>(a, (1 << m) - 1);
+                const K mna = a < oa ? a : oa, mxa = a < oa ? oa : a;
+                const K mnb = b < ob ? b : ob, mxb = b < ob ? ob : b;
+                k[j] = up ? mxa : mna;
+                k[kLocalItems - 1 - j] = up ? mxb : mnb;
+            }
+        }
+#pragma unroll
+        for (int d = m - 2; d >= 0; --d) {
+            const bool up = (lane >> d) & 1u;
+#pragma unroll
+            for (int j = 0; j < kLocalItems; ++j) {
+                const K o = shfl_xor_key<K>(k[j], 1 << d);
+                const K mn = k[j] < o ? k[j] : o, mx = k[j] < o ? o : k[j];
+                k[j] = up ? mx : mn;
+            }
+        }
+#pragma unroll
+        for (int s = kLocalItems / 2; s > 0; s >>= 1) {
+#pragma unroll
+            for (int j = 0; j < kLocalItems; ++j) {
+                if ((j & s) == 0) {
+                    const K a = k[j], b = k[j + s];
+                    k[j] = a < b ? a : b;
+                    k[j + s] = a < b ? b : a;
+                }
+            }
+        }
+        run <<= 1;
+    }
+    return run;
+}
+
 template <class K>
 static __device__ __forceinline__ void cta_merge_sort(LocalSmem& S, uint32_t n, const uint64_t (&kin)[kLocalItems],
-                                                      int lo, uint64_t common) {
+                                                      int lo, uint64_t common, int warp_levels) {
     constexpr K kInf = ~K(0);
     const unsigned tid = threadIdx.x;
     K* X = reinterpret_cast<K*>(S.X);
@@ -444,8 +538,19 @@ static __device__ __forceinline__ void cta_merge_sort(LocalSmem& S, uint32_t n, 
     // slots [0, nsort): n rounded up to whole threads; runs at the end are clipped
     const uint32_t nsort = n ? (n + kLocalItems - 1) & ~uint32_t(kLocalItems - 1) : kLocalItems;
     const bool active = tid * kLocalItems < nsort;
-    if (active) sort16<K>(k);
-    for (uint32_t w = kLocalItems; w < nsort; w <<= 1) {
+    uint32_t w0 = kLocalItems;
+    if (sizeof(K) == 4 && warp_levels > 0) {
+        // whole warps: lanes past nsort hold all-ones keys, which sort last
+        if ((tid & ~31u) * kLocalItems < nsort) {
+            sort16<K>(k);
+            warp_bitonic_merge<K>(k, nsort - (tid & ~31u) * kLocalItems, warp_levels);
+        }
+        // block-uniform: every warp's slots are now sorted in runs of this length
+        for (int m = 0; m < warp_levels && w0 < nsort; ++m) w0 <<= 1;
+    } else if (active) {
+        sort16<K>(k);
+    }
+    for (uint32_t w = w0; w < nsort; w <<= 1) {
         if (active) {
 #pragma unroll
             for (int j = 0; j < kLocalItems; ++j) X[tid * (kLocalItems + 1) + j] = k[j];  // X[xpad(16t+j)]
@@ -516,9 +621,10 @@ static __device__ __forceinline__ void cta_lsd_sort(LocalSmem& S, uint32_t n, in
     if (PRG_LOCAL_STATS && threadIdx.x == 0) atomicAdd(&g_local_stats[merge ? (hi - lo < 32 ? 5 : 6) : 7], 1ull);
     if (merge) {
         if (hi - lo < 32)
-            cta_merge_sort<uint32_t>(S, n, k, lo, a & ~(((hi - lo == 31) ? ~0ull >> 32 : ((1ull << (hi - lo + 1)) - 1)) << lo));
+            cta_merge_sort<uint32_t>(S, n, k, lo, a & ~(((hi - lo == 31) ? ~0ull >> 32 : ((1ull << (hi - lo + 1)) - 1)) << lo),
+                                     (merge_span >> 12) & 7);
         else  // PRG_MERGE_SPAN + 256: 64-bit keys too (measured slower than their LSD passes)
-            cta_merge_sort<uint64_t>(S, n, k, 0, 0ull);
+            cta_merge_sort<uint64_t>(S, n, k, 0, 0ull, (merge_span >> 12) & 7);
         return;
     }
     if (payload_bits == 0 && hi - lo < 32) {

@@ -260,7 +260,15 @@ def run_ours(args):
 
     ws, rank, local = dist_setup()
     torch.cuda.set_device(local)
-    if ws > 1:
+    # PRG_BENCH_FORCE_DIST=1: a single process takes the N > 1 code path (NCCL process
+    # group of one, sharded K3 with the all-reduce callback) — a dry run of the
+    # multi-GPU bench on a one-GPU box (under torchrun --nproc-per-node 1).
+    multi = ws > 1 or os.environ.get("PRG_BENCH_FORCE_DIST") == "1"
+    if multi:
+        if "MASTER_ADDR" not in os.environ:
+            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT="29511", RANK="0", WORLD_SIZE="1")
+        if ws == 1:
+            os.environ["PRG_SHARD_EXCHANGE_ALWAYS"] = "1"  # the exchange runs even for a world of one
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     S, seed, iters = args.scale, args.seed, args.iterations
     n = 1 << S
@@ -278,7 +286,7 @@ def run_ours(args):
     # N > 1: K3 column-sharded over the ranks (NCCL all_reduce of the per-step
     # exchange buffer), K1/K2 replicated (every rank holds the matrix);
     # --replicas: N independent single-GPU pipelines instead
-    sharded = ws > 1 and not args.replicas
+    sharded = multi and not args.replicas
     allreduce = capi.torch_allreduce() if sharded else None
 
     def one_step(record):
@@ -306,7 +314,7 @@ def run_ours(args):
     for _ in range(args.warmup):
         one_step(None).close()
     torch.cuda.synchronize()
-    if ws > 1:
+    if multi:
         dist.barrier()
     torch.cuda.synchronize()
 
@@ -331,7 +339,7 @@ def run_ours(args):
     L.prg_profile_report(buf, 65536, 1)
     prof = json.loads(buf.value.decode())
     clk = clocks.stop()
-    if ws > 1:
+    if multi:
         dist.barrier()
     torch.cuda.synchronize()
 
@@ -489,7 +497,7 @@ def run_ours(args):
     if rank == 0 and ws == 1 and not args.no_pipeline_io:
         out["official_pipeline"] = official_pipeline(args.pipeline_io_scale)
 
-    if ws > 1:
+    if multi:
         dist.barrier()
         dist.destroy_process_group()
     if rank == 0:

@@ -229,6 +229,34 @@ __device__ __forceinline__ double ld_keep_f64_pred(const double* p, bool pred, u
         : "l"(p), "r"((uint32_t)pred), "l"(pol));
     return r;
 }
+// Gather with an index-dependent L1 eviction priority (measurement variants of
+// the SpMV, PRG_SPMV_VARIANT=2..5): the hot head of the gather vector and its
+// cold tail take different priorities. HOTP / COLDP: 0 = default, 1 = L1::evict_last,
+// 2 = L1::evict_first, 3 = L1::no_allocate.
+#define PRG_L1P_STR_0 ""
+#define PRG_L1P_STR_1 ".L1::evict_last"
+#define PRG_L1P_STR_2 ".L1::evict_first"
+#define PRG_L1P_STR_3 ".L1::no_allocate"
+#define PRG_L1P_STR(x) PRG_L1P_STR_##x
+#define PRG_DEFINE_LD_HOTCOLD(HOTP, COLDP)                                                              \
+    __device__ __forceinline__ double ld_hotcold_##HOTP##_##COLDP(const double* p, bool pred, bool hot, \
+                                                                  uint64_t pol) {                       \
+        double r = 0.0;                                                                                 \
+        asm("{ .reg .pred q, h, c;\n\t"                                                                 \
+            "setp.ne.u32 q, %2, 0;\n\t"                                                                 \
+            "setp.ne.u32 h, %3, 0;\n\t"                                                                 \
+            "and.pred c, q, !h;\n\t"                                                                    \
+            "and.pred h, q, h;\n\t"                                                                     \
+            "@h ld.global.nc" PRG_L1P_STR(HOTP) ".L2::cache_hint.f64 %0, [%1], %4;\n\t"                 \
+            "@c ld.global.nc" PRG_L1P_STR(COLDP) ".L2::cache_hint.f64 %0, [%1], %4; }"                   \
+            : "+d"(r)                                                                                   \
+            : "l"(p), "r"((uint32_t)pred), "r"((uint32_t)hot), "l"(pol));                               \
+        return r;                                                                                       \
+    }
+PRG_DEFINE_LD_HOTCOLD(1, 2)
+PRG_DEFINE_LD_HOTCOLD(0, 2)
+PRG_DEFINE_LD_HOTCOLD(1, 0)
+PRG_DEFINE_LD_HOTCOLD(0, 3)
 __device__ __forceinline__ double ld_f64_pred(const double* p, bool pred) {
     double r = 0.0;
     asm("{ .reg .pred q; setp.ne.u32 q, %2, 0;\n\t"

@@ -991,13 +991,14 @@ struct SellArgs {
     uint32_t slice_end = 0;      // shard of a multi-GPU K3; the whole list on one GPU)
     double damping;
     uint64_t n_s = 0;            // length of s (checked builds: gather bounds)
+    uint32_t hot = 0;            // PRG_SPMV_VARIANT 2..5: s[0, hot) gathers take the "hot" L1 priority
 };
 
 
 // 48 warps per SM and no shared-memory staging: measured on B200 (S=24) the L1
 // caches the hot, degree-ordered head of s by itself, and occupancy (requests
 // in flight) matters more than a software-managed hot set (1.9 ms vs 3.3 ms).
-template <int U, int kThreads = kSpmvThreads, int kMinBlocks = 2>
+template <int U, int kThreads = kSpmvThreads, int kMinBlocks = 2, int GM = 0>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) spmv_sell_kernel(SellArgs a) {
     const unsigned lane = dev::lane_id();
     const double bg = a.bgp[1];
@@ -1039,7 +1040,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) spmv_sell_kernel(SellArg
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 PRG_DCHECK((w[u] >> 31) || w[u] < a.n_s);
-                x[u] = dev::ld_keep_f64_pred(a.s + (w[u] & 0x7fffffffu), !(w[u] >> 31), pol_keep);
+                const uint32_t gi = w[u] & 0x7fffffffu;
+                if (GM == 0) x[u] = dev::ld_keep_f64_pred(a.s + gi, !(w[u] >> 31), pol_keep);
+                else if (GM == 2) x[u] = dev::ld_hotcold_1_2(a.s + gi, !(w[u] >> 31), gi < a.hot, pol_keep);
+                else if (GM == 3) x[u] = dev::ld_hotcold_0_2(a.s + gi, !(w[u] >> 31), gi < a.hot, pol_keep);
+                else if (GM == 4) x[u] = dev::ld_hotcold_1_0(a.s + gi, !(w[u] >> 31), gi < a.hot, pol_keep);
+                else x[u] = dev::ld_hotcold_0_3(a.s + gi, !(w[u] >> 31), gi < a.hot, pol_keep);
             }
             const uint32_t k1 = k0 + U;
 #pragma unroll
@@ -1462,7 +1468,11 @@ void iterate(const K3Plan& P, const double* r_in, double* r_out, int iters, doub
     if (variant < 0) {
         const char* v = getenv("PRG_SPMV_VARIANT");
         variant = v ? atoi(v) : 0;
-
+    }
+    static int hot_rows = -1;  // PRG_HOT_ROWS: length of the "hot" head of s for variants 2..5
+    if (hot_rows < 0) {
+        const char* v = getenv("PRG_HOT_ROWS");
+        hot_rows = v ? atoi(v) : 16384;
     }
     const uint32_t NP = P.nslices * 32;
     // s = [row-scaled iterate (SELL row order, n_nd) | exception products (n_exc)]
@@ -1472,7 +1482,10 @@ void iterate(const K3Plan& P, const double* r_in, double* r_out, int iters, doub
     uint32_t sl_begin = 0, sl_end = P.nslices;
     size_t n_parts = 0, xcount = 0;
     DevBuf<double> xb0, xb1;
-    if (shard && shard->world > 1) {
+    // PRG_SHARD_EXCHANGE_ALWAYS=1: a world of one still goes through the exchange
+    // (the one-GPU dry run of the multi-GPU path: tests, bench PRG_BENCH_FORCE_DIST)
+    static const bool exchange_always = [] { const char* e = getenv("PRG_SHARD_EXCHANGE_ALWAYS"); return e && atoi(e) != 0; }();
+    if (shard && (shard->world > 1 || exchange_always)) {
         std::vector<uint32_t> sp((size_t)P.nslices + 1), bounds((size_t)shard->world + 1);
         PRG_CUDA(cudaMemcpyAsync(sp.data(), P.slice_ptr.get(), sp.size() * 4, cudaMemcpyDeviceToHost, s));
         uint32_t nsp = 0;
@@ -1549,6 +1562,7 @@ void iterate(const K3Plan& P, const double* r_in, double* r_out, int iters, doub
         a.slice_end = sl_end;
         a.damping = damping;
         a.n_s = (uint64_t)(P.n_nd + P.n_exc);
+        a.hot = (uint32_t)hot_rows;
         if (sharded)  // every element is then written by exactly one rank
             PRG_CUDA(cudaMemsetAsync(y_of(it & 1), 0, xcount * sizeof(double), s));
         if (P.nslices && sl_end > sl_begin) {
@@ -1558,6 +1572,10 @@ void iterate(const K3Plan& P, const double* r_in, double* r_out, int iters, doub
             // tools/exp_spmv4.py); 896x2 U4 0.792, 640x2 U6 0.775, 512x3 U6 0.793,
             // 768x2 U8 0.780, 832x2 U6 0.847.
             if (variant == 1) spmv_sell_kernel<4><<<num_sms() * 2, kSpmvThreads, 0, s>>>(a);
+            else if (variant == 2) spmv_sell_kernel<6, 768, 2, 2><<<num_sms() * 2, 768, 0, s>>>(a);
+            else if (variant == 3) spmv_sell_kernel<6, 768, 2, 3><<<num_sms() * 2, 768, 0, s>>>(a);
+            else if (variant == 4) spmv_sell_kernel<6, 768, 2, 4><<<num_sms() * 2, 768, 0, s>>>(a);
+            else if (variant == 5) spmv_sell_kernel<6, 768, 2, 5><<<num_sms() * 2, 768, 0, s>>>(a);
             else spmv_sell_kernel<6, 768, 2><<<num_sms() * 2, 768, 0, s>>>(a);
             PRG_LAUNCH_CHECK();
         }

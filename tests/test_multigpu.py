@@ -150,3 +150,52 @@ def test_k3_sharded_bit_identical(cuda, world, scale, seed, init):
     for r, norm in out:
         assert np.array_equal(r.view(np.int64), ref.view(np.int64)) and norm == nref
     mat.close()
+
+
+def _nccl_world1_worker(port, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1603_01876_b200 import capi
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), PRG_SHARD_EXCHANGE_ALWAYS="1")
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        scale, seed = 14, 7
+        n = 1 << scale
+        srt = torch.from_numpy(O.k1_sort(O.generate(scale, seed), scale)).cuda()
+        mat = capi.k2_filter(srt, n, csc=True)
+        ref, nref = capi.k3_pagerank(mat, seed=seed, mode=0)
+        st = torch.cuda.Stream()
+        inner, calls_box = capi.torch_allreduce(), [0]
+
+        def counted(buf, stream=None):
+            calls_box[0] += 1
+            inner(buf, stream)
+
+        with torch.cuda.stream(st):
+            got, ngot = capi.k3_pagerank_sharded(mat, 0, 1, counted, seed=seed, stream=st)
+        st.synchronize()
+        same = np.array_equal(got.cpu().numpy().view(np.int64), ref.cpu().numpy().view(np.int64)) and ngot == nref
+        calls = calls_box[0]
+        mat.close()
+        q.put(bool(same) and calls == 20)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_k3_sharded_through_nccl_world1(cuda):
+    """The exchange as bench.py --gpus N performs it — capi.torch_allreduce over
+    NCCL on the library's stream — on the one GPU this run has (world size 1):
+    the callback, the stream ordering and the NCCL call are the real ones."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_world1_worker, args=(_free_port(), q))
+    p.start()
+    ok = q.get(timeout=300)
+    p.join(timeout=60)
+    assert p.exitcode == 0 and ok

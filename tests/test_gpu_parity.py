@@ -516,3 +516,56 @@ def test_full_size_digests(capi, scale):
         assert d_ref <= 1e-9 and abs(d_ref - d_ref_neu) <= 1e-12
     mat.close()
     torch.cuda.empty_cache()
+
+
+# ---- seeded fuzz: many small, ragged graphs through K1 -> K2 -> K3 -----------
+def _fuzz_graph(rng, scale):
+    n = 1 << scale
+    m = int(rng.integers(0, 40 * n + 1))
+    kind = int(rng.integers(0, 5))
+    if kind == 0:    # uniform
+        u, v = rng.integers(1, n + 1, m), rng.integers(1, n + 1, m)
+    elif kind == 1:  # skewed on both ends (hubs, many duplicates)
+        u = np.minimum(rng.zipf(1.5, m), n)
+        v = np.minimum(rng.zipf(1.3, m), n)
+    elif kind == 2:  # a single start vertex (one long row)
+        u, v = np.full(m, int(rng.integers(1, n + 1))), rng.integers(1, n + 1, m)
+    elif kind == 3:  # a single end vertex (one column holds everything: it is the maximum)
+        u, v = rng.integers(1, n + 1, m), np.full(m, int(rng.integers(1, n + 1)))
+    else:            # self loops and a few distinct pairs repeated
+        base = rng.integers(1, n + 1, size=(max(1, m // 16), 2))
+        pick = base[rng.integers(0, len(base), m)] if m else np.zeros((0, 2), np.int64)
+        loops = rng.random(m) < 0.3
+        u = pick[:, 0] if m else np.zeros(0, np.int64)
+        v = np.where(loops, u, pick[:, 1]) if m else np.zeros(0, np.int64)
+    return np.column_stack([u, v]).astype(np.int64).reshape(-1, 2), n
+
+
+@pytest.mark.parametrize("block,count,lo,hi", [(0, 64, 1, 8), (1, 64, 1, 8), (2, 64, 1, 8), (3, 64, 1, 8),
+                                                (4, 12, 8, 13), (5, 12, 8, 13)])
+def test_fuzz_small_graphs(capi, block, count, lo, hi):
+    """Seeded random graphs (blocks 0-3: N = 2 .. 128; blocks 4-5: N = 256 .. 4096,
+    crossing the sort's and K2's tile sizes; up to 40 edges per vertex, five
+    shapes): K1 and K2 bit-exact against the oracle, K3 bit-identical in the
+    parity mode and within tolerance in the timed mode, with and without K2's
+    kept column layout."""
+    rng = np.random.default_rng(9000 + block)
+    for _ in range(count):
+        scale = int(rng.integers(lo, hi))
+        uv, n = _fuzz_graph(rng, scale)
+        want = O.k1_sort(uv, scale)
+        got = capi.k1_sort(t(uv), scale).cpu().numpy() if len(uv) else uv
+        assert np.array_equal(got, want)
+        ref = O.k2(want, n)
+        mat = capi.k2_filter_host(want, n)
+        assert k2_equal(mat, ref)
+        seed = int(rng.integers(0, 1 << 30))
+        rr, nr = O.run_kernel3(ref.row_offsets, ref.cols, ref.values, n, seed=seed)
+        rp, npar = capi.k3_pagerank(mat, seed=seed, mode=1)
+        assert np.array_equal(rp.cpu().numpy().view(np.int64), rr.view(np.int64)) and npar == nr
+        rt, _ = capi.k3_pagerank(mat, seed=seed, mode=0)
+        assert rel_l1(rt.cpu().numpy(), rr) <= K3_TOL
+        mat.build_csc()
+        rc, _ = capi.k3_pagerank(mat, seed=seed, mode=0)
+        assert np.array_equal(rc.cpu().numpy().view(np.int64), rt.cpu().numpy().view(np.int64))
+        mat.close()

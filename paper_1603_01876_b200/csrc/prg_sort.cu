@@ -23,19 +23,25 @@ namespace prg::sort {
 // segment left the rest of the block waiting: barrier stalls 47%, 50-80 us per
 // level launch.)
 __device__ uint32_t g_coalesce_max = kLocalCap;
+// Children of [g_small_min, kSmallCap] keys whose unsorted bits fit a 32-bit
+// window (and carry no payload) are kept apart and flagged (Seg::bits = 1) for
+// the small-segment merge kernel (local_small_kernel); 0 = off.
+__device__ uint32_t g_small_min = 0;
 
 struct EmitScratch {
     uint8_t kind[kRadix];   // 0: joins the open run or empty, 1: starts a run, 2: larger than the cap
     uint32_t rsz[kRadix];   // run size, at the run's first child
     uint32_t scan[kRadix / 32 + 1];
-    uint32_t base_fin, base_next;
+    uint32_t base_fin, base_next, base_small;
 };
+
 
 __device__ void emit_children_block(const uint64_t* child_start, const uint32_t* child_size, int nchild, uint8_t buf,
                                     int next_shift, int next_bits, Seg* __restrict__ next,
                                     uint32_t* __restrict__ n_next, Seg* __restrict__ fin,
-                                    uint32_t* __restrict__ n_fin, EmitScratch& E) {
+                                    uint32_t* __restrict__ n_fin, EmitScratch& E, SmallList sl) {
     const uint32_t cap = (uint32_t)kLocalCap, cmax = g_coalesce_max;
+    const uint32_t smin = sl.n_small ? g_small_min : 0u;
     if (threadIdx.x == 0) {
         uint32_t run = 0;
         int rs = 0;
@@ -45,6 +51,13 @@ __device__ void emit_children_block(const uint64_t* child_start, const uint32_t*
             if (sz > cap) {
                 if (run) { E.rsz[rs] = run; run = 0; }
                 k = 2;
+            } else if (smin && sz >= smin && sz <= (uint32_t)kSmallCap && (run == 0 || run + sz > cap)) {
+                // A final segment of its own, for the small kernel — only where it does not cut an
+                // open run short (a medium child amid tiny ones stays in their run: at S=26 every
+                // such cut left two under-filled LSD segments, K1 48.5 -> 52.3 ms).
+                if (run) { E.rsz[rs] = run; run = 0; }
+                E.rsz[d] = sz;
+                k = 3;
             } else if (sz) {
                 // PRG_COALESCE_MAX (measurement knob): children at least this large are
                 // not joined. Keeping K1's ~2.9 K-key level-2 children apart (all on the
@@ -61,36 +74,41 @@ __device__ void emit_children_block(const uint64_t* child_start, const uint32_t*
     }
     __syncthreads();
     // what this thread's children emit (children tid, tid + blockDim, ...)
-    uint32_t nf = 0, nn = 0;
+    uint32_t nf = 0, nn = 0, ns = 0;
     for (int d = threadIdx.x; d < nchild; d += blockDim.x) {
         const uint8_t k = E.kind[d];
         if (k == 1) ++nf;
+        else if (k == 3) ++ns;
         else if (k == 2) {
             if (next_bits) ++nn;
             else nf += (child_size[d] + cap - 1) / cap;
         }
     }
-    uint32_t tf, tn;
+    uint32_t tf, tn, ts = 0;
     uint32_t of = dev::block_excl_scan(nf, E.scan, tf);
     uint32_t on = dev::block_excl_scan(nn, E.scan, tn);
+    uint32_t os = smin ? dev::block_excl_scan(ns, E.scan, ts) : 0u;
     if (threadIdx.x == 0) {
         E.base_fin = tf ? atomicAdd(n_fin, tf) : 0u;
         E.base_next = tn ? atomicAdd(n_next, tn) : 0u;
+        E.base_small = ts ? atomicAdd(sl.n_small, ts) : 0u;
     }
     __syncthreads();
     of += E.base_fin;
     on += E.base_next;
+    os += E.base_small;
     for (int d = threadIdx.x; d < nchild; d += blockDim.x) {
         const uint8_t k = E.kind[d];
         if (k == 0) continue;
         Seg sg;
         sg.start = child_start[d];
         sg.buf = buf;
-        if (k == 1) {
+        if (k == 1 || k == 3) {
             sg.size = E.rsz[d];
             sg.bits = 0;
             sg.shift = 0;
-            fin[of++] = sg;
+            if (k == 3) fin[sl.cap - 1u - os++] = sg;  // sorted by local_small_kernel
+            else fin[of++] = sg;
             continue;
         }
         const uint32_t sz = child_size[d];
@@ -129,7 +147,7 @@ __global__ void classify_l1_kernel(const uint32_t* __restrict__ off, uint32_t nt
         csz[d] = (uint32_t)(en - st);
     }
     __syncthreads();
-    emit_children_block(cst, csz, kRadix, 1, shift - bits, bits, next, n_next, fin, n_fin, E);
+    emit_children_block(cst, csz, kRadix, 1, shift - bits, bits, next, n_next, fin, n_fin, E, SmallList{});
 }
 
 __global__ void build_tiles_kernel(const Seg* __restrict__ active, const uint32_t* __restrict__ n_active,
@@ -328,7 +346,7 @@ __global__ void classify_kernel(const Seg* __restrict__ active, const uint32_t* 
                                 const uint64_t* __restrict__ seg_elem0,
                                 const uint32_t* __restrict__ off, Seg* __restrict__ next,
                                 uint32_t* __restrict__ n_next, Seg* __restrict__ fin,
-                                uint32_t* __restrict__ n_fin, int floor_bit) {
+                                uint32_t* __restrict__ n_fin, int floor_bit, SmallList small) {
     __shared__ uint64_t cst[kRadix];
     __shared__ uint32_t csz[kRadix];
     __shared__ EmitScratch E;
@@ -348,7 +366,8 @@ __global__ void classify_kernel(const Seg* __restrict__ active, const uint32_t* 
         __syncthreads();
         const int rem = sg.shift - floor_bit;
         const int nb = rem >= 8 ? 8 : rem;
-        emit_children_block(cst, csz, nd, (uint8_t)(sg.buf ^ 1), sg.shift - nb, nb, next, n_next, fin, n_fin, E);
+        emit_children_block(cst, csz, nd, (uint8_t)(sg.buf ^ 1), sg.shift - nb, nb, next, n_next, fin, n_fin, E,
+                            (floor_bit == 0 && rem > 0 && rem <= 32) ? small : SmallList{});
         __syncthreads();
     }
 }
@@ -366,6 +385,15 @@ int sort_grid_mult(int which) {
         g2 = e2 ? std::max(1, atoi(e2)) : 4;
     }
     return which == 1 ? g1 : g2;
+}
+int local_small_min() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("PRG_SMALL_MIN");
+        v = e ? atoi(e) : 1024;
+        v = v <= 0 ? 0 : std::max(v, 256);  // the list bound assumes children of at least 256 keys
+    }
+    return v;
 }
 int local_merge_span() {
     static int v = -1;
@@ -385,6 +413,12 @@ void sort_workspace_init(SortWorkspace& ws, size_t n, cudaStream_t s) {
         const uint32_t v = e ? (uint32_t)atoi(e) : (uint32_t)kLocalCap;
         PRG_CUDA(cudaMemcpyToSymbol(g_coalesce_max, &v, sizeof(v)));
         coalesce_set = true;
+    }
+    static bool small_set = false;  // PRG_SMALL_MIN: smallest child given to the small-segment kernel (0 = off)
+    if (!small_set) {
+        const uint32_t v = (uint32_t)local_small_min();
+        PRG_CUDA(cudaMemcpyToSymbol(g_small_min, &v, sizeof(v)));
+        small_set = true;
     }
     if (ws.n >= n && ws.keys[0].get()) return;
     ws.n = n;
@@ -408,6 +442,8 @@ void sort_workspace_init(SortWorkspace& ws, size_t n, cudaStream_t s) {
 }
 
 void run_segmented_levels(SortWorkspace& ws, int levels_left, int floor_bit, bool stable, cudaStream_t s) {
+    SmallList small;  // [41] = count of small-kernel segments
+    if (!stable && floor_bit == 0 && local_small_min() > 0) small = SmallList{ws.counters.get() + 41, ws.max_fin};
     static bool attr_set = false;
     const size_t smem = (size_t)kTile * sizeof(uint64_t) + (stable ? kStableScratch : 0);
     if (!attr_set) {
@@ -454,7 +490,7 @@ void run_segmented_levels(SortWorkspace& ws, int levels_left, int floor_bit, boo
         // of segments are not serialised on 4 blocks per SM (0.2 ms per level).
         classify_kernel<<<(unsigned)num_sms() * 32, 64, 0, s>>>(act, n_act, ws.seg_tile0.get(), ws.seg_elem0.get(),
                                                                 ws.off.get(), nxt, n_nxt, ws.fin.get(), cnt + 2,
-                                                                floor_bit);
+                                                                floor_bit, small);
         PRG_LAUNCH_CHECK();
     }
 }

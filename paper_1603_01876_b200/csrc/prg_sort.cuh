@@ -39,7 +39,9 @@ constexpr int kTile = kTileThreads * kTileItems;  // 8192 keys per global tile
 constexpr int kRadix = 256;
 constexpr int kLocalCap = 8192;       // keys per SMEM-resident segment
 constexpr int kLocalThreads = 512;
-constexpr int kCounters = 40;  // SortWorkspace::counters (up to 16 levels of tile counters)
+constexpr int kSmallCap = 4096;       // keys per segment of the small-segment merge kernel
+constexpr int kSmallThreads = 256;
+constexpr int kCounters = 44;  // SortWorkspace::counters (up to 16 levels of tile counters; [40]/[41] small-kernel work / count)
 
 struct Seg {
     uint64_t start;   // element offset in the key buffers
@@ -47,6 +49,15 @@ struct Seg {
     uint16_t shift;   // bits [shift, shift+bits) are the next digit
     uint8_t bits;     // 0 => no bits left (all keys equal above the local stage)
     uint8_t buf;      // which key buffer holds the segment
+};
+
+// Where the small-kernel segments go (local_small_kernel): the tail of the
+// final-segment array, filled backwards (entry i at fin[cap - 1 - i]); every
+// child of a level is final of one kind or the other, so the array's bound
+// covers both.
+struct SmallList {
+    uint32_t* n_small = nullptr;  // null: never flag
+    uint32_t cap = 0;
 };
 
 // ---------------------------------------------------------------------------
@@ -326,7 +337,7 @@ __global__ void classify_kernel(const Seg* __restrict__ active, const uint32_t* 
                                 const uint64_t* __restrict__ seg_elem0,
                                 const uint32_t* __restrict__ off, Seg* __restrict__ next,
                                 uint32_t* __restrict__ n_next, Seg* __restrict__ fin,
-                                uint32_t* __restrict__ n_fin, int floor_bit);
+                                uint32_t* __restrict__ n_fin, int floor_bit, SmallList small);
 
 // Level-1 children classification (the whole input was one segment).
 __global__ void classify_l1_kernel(const uint32_t* __restrict__ off, uint32_t ntiles, size_t n,
@@ -526,15 +537,14 @@ __device__ __forceinline__ uint32_t warp_bitonic_merge(K (&k)[kLocalItems], uint
     return run;
 }
 
+// The merge sort proper: k holds this thread's 16 slots [16 tid, 16 tid + 16)
+// (slots past n all ones); X is xpad-indexed scratch for nsort keys. On return k
+// holds the sorted slots [16 tid, 16 tid + 16). Any block size (the small-segment
+// kernel runs it with 256 threads). Ends with a barrier when a level ran.
 template <class K>
-static __device__ __forceinline__ void cta_merge_sort(LocalSmem& S, uint32_t n, const uint64_t (&kin)[kLocalItems],
-                                                      int lo, uint64_t common, int warp_levels) {
+static __device__ __forceinline__ void cta_merge_core(K* X, uint32_t n, K (&k)[kLocalItems], int warp_levels) {
     constexpr K kInf = ~K(0);
     const unsigned tid = threadIdx.x;
-    K* X = reinterpret_cast<K*>(S.X);
-    K k[kLocalItems];
-#pragma unroll
-    for (int j = 0; j < kLocalItems; ++j) k[j] = (K)(kin[j] >> lo);  // slots past n: all ones
     // slots [0, nsort): n rounded up to whole threads; runs at the end are clipped
     const uint32_t nsort = n ? (n + kLocalItems - 1) & ~uint32_t(kLocalItems - 1) : kLocalItems;
     const bool active = tid * kLocalItems < nsort;
@@ -583,6 +593,16 @@ static __device__ __forceinline__ void cta_merge_sort(LocalSmem& S, uint32_t n, 
         }
         __syncthreads();
     }
+}
+
+template <class K>
+static __device__ __forceinline__ void cta_merge_sort(LocalSmem& S, uint32_t n, const uint64_t (&kin)[kLocalItems],
+                                                      int lo, uint64_t common, int warp_levels) {
+    const unsigned tid = threadIdx.x;
+    K k[kLocalItems];
+#pragma unroll
+    for (int j = 0; j < kLocalItems; ++j) k[j] = (K)(kin[j] >> lo);  // slots past n: all ones
+    cta_merge_core<K>(reinterpret_cast<K*>(S.X), n, k, warp_levels);
     // the full keys (slots past n sort last and are never stored)
 #pragma unroll
     for (int j = 0; j < kLocalItems; ++j) S.X[tid * (kLocalItems + 1) + j] = common | ((uint64_t)k[j] << lo);
@@ -742,6 +762,74 @@ __global__ void __launch_bounds__(kLocalThreads, 2)
     }
 }
 
+// Small segments (flagged by the level bookkeeping: one child of at most
+// kSmallCap keys whose unsorted bits fit a 32-bit window, no payload): the same
+// register-network + merge-path sort on 256-thread CTAs, four to an SM. Such
+// children used to be joined into <= 8192-key segments whose > 32-bit windows
+// took the LSD path (44% of K1's segments at S=24), because a lone ~3 K-key
+// child left two thirds of a 512-thread CTA idle.
+struct SmallSmem {
+    uint32_t X[kSmallCap + kSmallCap / 16];
+    uint64_t red_or[kSmallThreads / 32], red_and[kSmallThreads / 32];
+    uint32_t seg_id;
+};
+template <class Dst>
+__global__ void __launch_bounds__(kSmallThreads, 4)
+    local_small_kernel(const uint64_t* __restrict__ keys0, const uint64_t* __restrict__ keys1,
+                       const Seg* __restrict__ fin_end, const uint32_t* __restrict__ n_small,
+                       uint32_t* __restrict__ work, Dst dst, int warp_levels) {
+    // segment i of the list sits at fin_end[-1 - i] (the tail of the final-segment array, filled backwards)
+    __shared__ SmallSmem S;
+    const uint32_t nf = *n_small;
+    const unsigned tid = threadIdx.x, lane = dev::lane_id(), w = dev::warp_id();
+    for (;;) {
+        if (tid == 0) S.seg_id = atomicAdd(work, 1u);
+        __syncthreads();
+        const uint32_t sid = S.seg_id;
+        __syncthreads();
+        if (sid >= nf) break;
+        const Seg sg = *(fin_end - 1 - sid);
+        const uint64_t* src = (sg.buf ? keys1 : keys0) + sg.start;
+        const uint32_t n = sg.size;
+        PRG_DCHECK(n > 0 && n <= (uint32_t)kSmallCap);
+        // blocked loads: thread t holds keys [16t, 16t+16) (128 contiguous bytes)
+        uint64_t k64[kLocalItems];
+        uint64_t o = 0, a = ~0ull;
+#pragma unroll
+        for (int j = 0; j < kLocalItems; ++j) {
+            const uint32_t i = tid * kLocalItems + j;
+            k64[j] = i < n ? src[i] : ~0ull;
+            if (i < n) { o |= k64[j]; a &= k64[j]; }
+        }
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            o |= __shfl_xor_sync(0xffffffffu, o, d);
+            a &= __shfl_xor_sync(0xffffffffu, a, d);
+        }
+        if (lane == 0) { S.red_or[w] = o; S.red_and[w] = a; }
+        __syncthreads();
+        o = 0; a = ~0ull;
+#pragma unroll
+        for (int q = 0; q < kSmallThreads / 32; ++q) { o |= S.red_or[q]; a &= S.red_and[q]; }
+        const uint64_t diff = o ^ a;
+        const int lo = diff ? __ffsll((long long)diff) - 1 : 0;
+        PRG_DCHECK(diff == 0 || 63 - __clzll((long long)diff) - lo < 32);
+        const uint64_t common = a & ~(0xffffffffull << lo);
+        uint32_t k[kLocalItems];
+#pragma unroll
+        for (int j = 0; j < kLocalItems; ++j) k[j] = tid * kLocalItems + j < n ? (uint32_t)(k64[j] >> lo) : 0xffffffffu;
+        if (diff) cta_merge_core<uint32_t>(S.X, n, k, warp_levels);
+#pragma unroll
+        for (int j = 0; j < kLocalItems; ++j) S.X[tid * (kLocalItems + 1) + j] = k[j];
+        __syncthreads();
+        for (uint32_t i = tid; i < n; i += kSmallThreads) {
+            const uint64_t key = common | ((uint64_t)S.X[xpad(i)] << lo);
+            dst.store(sg.start + i, key, i > 0, i > 0 ? (common | ((uint64_t)S.X[xpad(i - 1)] << lo)) : 0ull);
+        }
+        __syncthreads();
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Host driver.
 // ---------------------------------------------------------------------------
@@ -761,6 +849,7 @@ struct SortWorkspace {
 void sort_workspace_init(SortWorkspace& ws, size_t n, cudaStream_t s);
 size_t local_smem_bytes();
 int local_merge_span();  // PRG_MERGE_SPAN (default 16): see cta_lsd_sort
+int local_small_min();   // PRG_SMALL_MIN: smallest child sorted by local_small_kernel (0 = off)
 int sort_grid_mult(int which);  // CTAs per SM of the level-1 (1) / segmented (2) tile kernels: PRG_SORT_GRID1/2
 
 // Runs levels >= 2 until every segment is final; then the caller launches
@@ -827,6 +916,12 @@ void msd_sort_split(Src src_hist, Src src_scat, size_t n, int key_bits, Dst dst,
     }
     {
         ProfScope prof(t + "_local", s);
+        if (!stable && payload_bits == 0 && local_small_min() > 0) {
+            local_small_kernel<Dst><<<num_sms() * 4, kSmallThreads, 0, s>>>(
+                ws.keys[0].get(), ws.keys[1].get(), ws.fin.get() + ws.max_fin, ws.counters.get() + 41,
+                ws.counters.get() + 40, dst, (local_merge_span() >> 12) & 7);
+            PRG_LAUNCH_CHECK();
+        }
         PRG_CUDA(cudaFuncSetAttribute(local_sort_kernel<Dst>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)local_smem_bytes()));
         local_sort_kernel<Dst><<<num_sms() * 2, kLocalThreads, local_smem_bytes(), s>>>(

@@ -86,6 +86,18 @@ def test_k1_heavy_duplicates_exceed_local_capacity(capi):
     assert np.array_equal(capi.k1_sort_host(inp, 10), O.k1_sort(inp, 10))
 
 
+def test_k1_lone_children_take_the_small_segment_kernel(capi):
+    """Inputs whose second-level children are lone 1-4 K-key segments with at most 32
+    unsorted bits (sort engine: local_small_kernel), next to tiny and oversized ones."""
+    rng = np.random.default_rng(17)
+    for scale, nu, m in ((10, 4, 400000), (12, 16, 1500000), (16, 3, 300000)):
+        n = 1 << scale
+        u = rng.integers(1, nu + 1, m)
+        v = np.where(rng.random(m) < 0.2, rng.integers(1, 9, m), rng.integers(1, n + 1, m))  # a few heavy columns
+        e = np.column_stack([u, v]).astype(np.int64)
+        assert np.array_equal(capi.k1_sort(t(e), scale).cpu().numpy(), O.k1_sort(e, scale))
+
+
 def test_k1_label_out_of_range(capi):
     with pytest.raises(capi.PrgError) as e:
         capi.k1_sort_host(np.array([[1, 2], [9, 1]]), 3)

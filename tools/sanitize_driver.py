@@ -52,6 +52,11 @@ def main(scale):
         assert np.array_equal(rh.view(np.int64), rt.cpu().numpy().view(np.int64))
         mat.close()
         torch.cuda.synchronize()
+    # K1 small-segment kernel: four start vertices in one level-1 bucket, so the second
+    # level's 256 children hold 1-4 K keys each (lone children with <= 32 unsorted bits)
+    rng = np.random.default_rng(17)
+    e = np.column_stack([rng.integers(1, 5, 400000), rng.integers(1, 1025, 400000)]).astype(np.int64)
+    assert np.array_equal(capi.k1_sort(torch.from_numpy(e).cuda(), 10).cpu().numpy(), O.k1_sort(e, 10))
     # streamed K1 (one pinned chunk) through the drop-in
     sys.path.insert(0, os.path.join(ROOT, "paper_1603_01876_b200", "python"))
     import tempfile

@@ -24,17 +24,16 @@ namespace prg::sort {
 // level launch.)
 __device__ uint32_t g_coalesce_max = kLocalCap;
 // Children of [g_small_min, kSmallCap] keys whose unsorted bits fit a 32-bit
-// window (and carry no payload) are kept apart and flagged (Seg::bits = 1) for
-// the small-segment merge kernel (local_small_kernel); 0 = off.
+// window (and carry no payload) are kept apart and listed (SmallList) for the
+// small-segment merge kernel (local_small_kernel); 0 = off.
 __device__ uint32_t g_small_min = 0;
 
 struct EmitScratch {
-    uint8_t kind[kRadix];   // 0: joins the open run or empty, 1: starts a run, 2: larger than the cap
+    uint8_t kind[kRadix];   // 0: joins the open run or empty, 1: starts a run, 2: larger than the cap, 3: small-kernel segment
     uint32_t rsz[kRadix];   // run size, at the run's first child
     uint32_t scan[kRadix / 32 + 1];
     uint32_t base_fin, base_next, base_small;
 };
-
 
 __device__ void emit_children_block(const uint64_t* child_start, const uint32_t* child_size, int nchild, uint8_t buf,
                                     int next_shift, int next_bits, Seg* __restrict__ next,
@@ -391,7 +390,7 @@ int local_small_min() {
     if (v < 0) {
         const char* e = getenv("PRG_SMALL_MIN");
         v = e ? atoi(e) : 1024;
-        v = v <= 0 ? 0 : std::max(v, 256);  // the list bound assumes children of at least 256 keys
+        v = v <= 0 ? 0 : std::max(v, 256);  // below ~512 keys a 256-thread CTA is mostly idle
     }
     return v;
 }

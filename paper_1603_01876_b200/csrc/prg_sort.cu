@@ -35,13 +35,35 @@ struct EmitScratch {
     uint32_t base_fin, base_next, base_small;
 };
 
+// SmallList::mode 2: where the small kernel applies, children are joined only inside aligned
+// digit groups that keep the run's window within 32 bits (gbits low digit bits may vary), and
+// every run of at most kSmallCap keys goes to the small list (sorted by three CTA sizes): no
+// segment is left to the LSD path. Mode 1: lone children of at least g_small_min keys only.
+
 __device__ void emit_children_block(const uint64_t* child_start, const uint32_t* child_size, int nchild, uint8_t buf,
                                     int next_shift, int next_bits, Seg* __restrict__ next,
                                     uint32_t* __restrict__ n_next, Seg* __restrict__ fin,
-                                    uint32_t* __restrict__ n_fin, EmitScratch& E, SmallList sl) {
+                                    uint32_t* __restrict__ n_fin, EmitScratch& E, SmallList sl, int gbits = 8) {
     const uint32_t cap = (uint32_t)kLocalCap, cmax = g_coalesce_max;
     const uint32_t smin = sl.n_small ? g_small_min : 0u;
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && smin && sl.mode == 2) {
+        uint32_t run = 0;
+        int rs = 0;
+        for (int d = 0; d < nchild; ++d) {
+            const uint32_t sz = child_size[d];
+            uint8_t k = 0;
+            const bool cut = run && (sz > cap || (sz && ((d >> gbits) != (rs >> gbits) || run + sz > cap)));
+            if (cut) { E.rsz[rs] = run; E.kind[rs] = run <= (uint32_t)kSmallCap ? 3 : 1; run = 0; }
+            if (sz > cap) {
+                k = 2;
+            } else if (sz) {
+                if (run == 0) { rs = d; k = 1; }
+                run += sz;
+            }
+            E.kind[d] = k;
+        }
+        if (run) { E.rsz[rs] = run; E.kind[rs] = run <= (uint32_t)kSmallCap ? 3 : 1; }
+    } else if (threadIdx.x == 0) {
         uint32_t run = 0;
         int rs = 0;
         for (int d = 0; d < nchild; ++d) {
@@ -366,7 +388,7 @@ __global__ void classify_kernel(const Seg* __restrict__ active, const uint32_t* 
         const int rem = sg.shift - floor_bit;
         const int nb = rem >= 8 ? 8 : rem;
         emit_children_block(cst, csz, nd, (uint8_t)(sg.buf ^ 1), sg.shift - nb, nb, next, n_next, fin, n_fin, E,
-                            (floor_bit == 0 && rem > 0 && rem <= 32) ? small : SmallList{});
+                            (floor_bit == 0 && rem > 0 && rem <= 32) ? small : SmallList{}, min(8, 32 - rem));
         __syncthreads();
     }
 }
@@ -394,6 +416,15 @@ int local_small_min() {
     }
     return v;
 }
+int local_small_mode(size_t n) {
+    static int v = -1;  // PRG_SMALL_MODE=1/2 forces a mode; default: by input size
+    if (v < 0) {
+        const char* e = getenv("PRG_SMALL_MODE");
+        v = e ? atoi(e) : 0;
+    }
+    // the three launches of mode 2 cost ~30 us: 3% of K1 at 2^24 keys, repaid from 2^26 on
+    return v == 1 || v == 2 ? v : (n >= (size_t(1) << 25) ? 2 : 1);
+}
 int local_merge_span() {
     static int v = -1;
     if (v < 0) {
@@ -417,6 +448,7 @@ void sort_workspace_init(SortWorkspace& ws, size_t n, cudaStream_t s) {
     if (!small_set) {
         const uint32_t v = (uint32_t)local_small_min();
         PRG_CUDA(cudaMemcpyToSymbol(g_small_min, &v, sizeof(v)));
+
         small_set = true;
     }
     if (ws.n >= n && ws.keys[0].get()) return;
@@ -442,7 +474,8 @@ void sort_workspace_init(SortWorkspace& ws, size_t n, cudaStream_t s) {
 
 void run_segmented_levels(SortWorkspace& ws, int levels_left, int floor_bit, bool stable, cudaStream_t s) {
     SmallList small;  // [41] = count of small-kernel segments
-    if (!stable && floor_bit == 0 && local_small_min() > 0) small = SmallList{ws.counters.get() + 41, ws.max_fin};
+    if (!stable && floor_bit == 0 && local_small_min() > 0)
+        small = SmallList{ws.counters.get() + 41, ws.max_fin, local_small_mode(ws.n_sorting)};
     static bool attr_set = false;
     const size_t smem = (size_t)kTile * sizeof(uint64_t) + (stable ? kStableScratch : 0);
     if (!attr_set) {

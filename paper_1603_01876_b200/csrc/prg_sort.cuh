@@ -61,6 +61,7 @@ struct Seg {
 struct SmallList {
     uint32_t* n_small = nullptr;  // null: never flag
     uint32_t cap = 0;
+    int mode = 1;                 // 1: lone children; 2: window-bounded runs (see emit_children_block)
 };
 
 // ---------------------------------------------------------------------------
@@ -771,65 +772,85 @@ __global__ void __launch_bounds__(kLocalThreads, 2)
 // children used to be joined into <= 8192-key segments whose > 32-bit windows
 // took the LSD path (44% of K1's segments at S=24), because a lone ~3 K-key
 // child left two thirds of a 512-thread CTA idle.
+template <int kThreads>
 struct SmallSmem {
-    uint32_t X[kSmallCap + kSmallCap / 16];
-    uint64_t red_or[kSmallThreads / 32], red_and[kSmallThreads / 32];
-    uint32_t seg_id;
+    uint32_t X[16 * kThreads + kThreads];
+    uint64_t red_or[kThreads / 32], red_and[kThreads / 32];
+    uint32_t chunk_base, chunk_mask;
 };
-template <class Dst>
-__global__ void __launch_bounds__(kSmallThreads, 4)
+// Segments of [size_lo, size_hi] keys (size_hi <= 16 * kThreads) of the small list; the list
+// is claimed eight entries at a time (one atomic and one ballot per chunk).
+template <class Dst, int kThreads, int kMinBlocks>
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
     local_small_kernel(const uint64_t* __restrict__ keys0, const uint64_t* __restrict__ keys1,
                        const Seg* __restrict__ fin_end, const uint32_t* __restrict__ n_small,
-                       uint32_t* __restrict__ work, Dst dst, int warp_levels) {
+                       uint32_t* __restrict__ work, Dst dst, int warp_levels, uint32_t size_lo, uint32_t size_hi) {
     // segment i of the list sits at fin_end[-1 - i] (the tail of the final-segment array, filled backwards)
-    __shared__ SmallSmem S;
+    __shared__ SmallSmem<kThreads> S;
     const uint32_t nf = *n_small;
     const unsigned tid = threadIdx.x, lane = dev::lane_id(), w = dev::warp_id();
     for (;;) {
-        if (tid == 0) S.seg_id = atomicAdd(work, 1u);
-        __syncthreads();
-        const uint32_t sid = S.seg_id;
-        __syncthreads();
-        if (sid >= nf) break;
-        const Seg sg = *(fin_end - 1 - sid);
-        const uint64_t* src = (sg.buf ? keys1 : keys0) + sg.start;
-        const uint32_t n = sg.size;
-        PRG_DCHECK(n > 0 && n <= (uint32_t)kSmallCap);
-        // blocked loads: thread t holds keys [16t, 16t+16) (128 contiguous bytes)
-        uint64_t k64[kLocalItems];
-        uint64_t o = 0, a = ~0ull;
-#pragma unroll
-        for (int j = 0; j < kLocalItems; ++j) {
-            const uint32_t i = tid * kLocalItems + j;
-            k64[j] = i < n ? src[i] : ~0ull;
-            if (i < n) { o |= k64[j]; a &= k64[j]; }
-        }
-#pragma unroll
-        for (int d = 16; d > 0; d >>= 1) {
-            o |= __shfl_xor_sync(0xffffffffu, o, d);
-            a &= __shfl_xor_sync(0xffffffffu, a, d);
-        }
-        if (lane == 0) { S.red_or[w] = o; S.red_and[w] = a; }
-        __syncthreads();
-        o = 0; a = ~0ull;
-#pragma unroll
-        for (int q = 0; q < kSmallThreads / 32; ++q) { o |= S.red_or[q]; a &= S.red_and[q]; }
-        const uint64_t diff = o ^ a;
-        const int lo = diff ? __ffsll((long long)diff) - 1 : 0;
-        PRG_DCHECK(diff == 0 || 63 - __clzll((long long)diff) - lo < 32);
-        const uint64_t common = a & ~(0xffffffffull << lo);
-        uint32_t k[kLocalItems];
-#pragma unroll
-        for (int j = 0; j < kLocalItems; ++j) k[j] = tid * kLocalItems + j < n ? (uint32_t)(k64[j] >> lo) : 0xffffffffu;
-        if (diff) cta_merge_core<uint32_t>(S.X, n, k, warp_levels);
-#pragma unroll
-        for (int j = 0; j < kLocalItems; ++j) S.X[tid * (kLocalItems + 1) + j] = k[j];
-        __syncthreads();
-        for (uint32_t i = tid; i < n; i += kSmallThreads) {
-            const uint64_t key = common | ((uint64_t)S.X[xpad(i)] << lo);
-            dst.store(sg.start + i, key, i > 0, i > 0 ? (common | ((uint64_t)S.X[xpad(i - 1)] << lo)) : 0ull);
+        if (tid < 32) {
+            uint32_t base = 0;
+            if (lane == 0) base = atomicAdd(work, 8u);
+            base = __shfl_sync(0xffffffffu, base, 0);
+            bool mine = false;
+            if (lane < 8 && base + lane < nf) {
+                const uint32_t sz = (fin_end - 1 - (base + lane))->size;
+                mine = sz >= size_lo && sz <= size_hi;
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, mine);
+            if (lane == 0) { S.chunk_base = base; S.chunk_mask = m; }
         }
         __syncthreads();
+        const uint32_t base = S.chunk_base;
+        unsigned todo = S.chunk_mask;
+        __syncthreads();
+        if (base >= nf) break;
+        while (todo) {
+            const uint32_t sid = base + (uint32_t)__ffs(todo) - 1u;
+            todo &= todo - 1u;
+            const Seg sg = *(fin_end - 1 - sid);
+            const uint64_t* src = (sg.buf ? keys1 : keys0) + sg.start;
+            const uint32_t n = sg.size;
+            PRG_DCHECK(n > 0 && n <= 16u * kThreads);
+            // blocked loads: thread t holds keys [16t, 16t+16) (128 contiguous bytes)
+            uint64_t k64[kLocalItems];
+            uint64_t o = 0, a = ~0ull;
+#pragma unroll
+            for (int j = 0; j < kLocalItems; ++j) {
+                const uint32_t i = tid * kLocalItems + j;
+                k64[j] = i < n ? src[i] : ~0ull;
+                if (i < n) { o |= k64[j]; a &= k64[j]; }
+            }
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) {
+                o |= __shfl_xor_sync(0xffffffffu, o, d);
+                a &= __shfl_xor_sync(0xffffffffu, a, d);
+            }
+            if (lane == 0) { S.red_or[w] = o; S.red_and[w] = a; }
+            __syncthreads();
+            o = 0; a = ~0ull;
+#pragma unroll
+            for (int q = 0; q < kThreads / 32; ++q) { o |= S.red_or[q]; a &= S.red_and[q]; }
+            const uint64_t diff = o ^ a;
+            const int lo = diff ? __ffsll((long long)diff) - 1 : 0;
+            PRG_DCHECK(diff == 0 || 63 - __clzll((long long)diff) - lo < 32);
+            const uint64_t common = a & ~(0xffffffffull << lo);
+            uint32_t k[kLocalItems];
+#pragma unroll
+            for (int j = 0; j < kLocalItems; ++j)
+                k[j] = tid * kLocalItems + j < n ? (uint32_t)(k64[j] >> lo) : 0xffffffffu;
+            if (diff) cta_merge_core<uint32_t>(S.X, n, k, warp_levels);
+#pragma unroll
+            for (int j = 0; j < kLocalItems; ++j) S.X[tid * (kLocalItems + 1) + j] = k[j];
+            __syncthreads();
+            for (uint32_t i = tid; i < n; i += kThreads) {
+                const uint64_t key = common | ((uint64_t)S.X[xpad(i)] << lo);
+                dst.store(sg.start + i, key, i > 0, i > 0 ? (common | ((uint64_t)S.X[xpad(i - 1)] << lo)) : 0ull);
+            }
+            __syncthreads();
+        }
     }
 }
 
@@ -845,7 +866,8 @@ struct SortWorkspace {
     DevBuf<uint32_t> counters;
     DevBuf<uint32_t> tile_seg, tile_idx, seg_tile0;
     DevBuf<uint64_t> seg_elem0;
-    size_t n = 0;
+    size_t n = 0;          // capacity
+    size_t n_sorting = 0;  // keys of the sort in progress
     uint32_t max_tiles = 0, max_active = 0, max_fin = 0;
 };
 
@@ -853,6 +875,7 @@ void sort_workspace_init(SortWorkspace& ws, size_t n, cudaStream_t s);
 size_t local_smem_bytes();
 int local_merge_span();  // PRG_MERGE_SPAN (default 16): see cta_lsd_sort
 int local_small_min();   // PRG_SMALL_MIN: smallest child sorted by local_small_kernel (0 = off)
+int local_small_mode(size_t n);  // 1 = lone children only, 2 = window-bounded runs in three CTA sizes (PRG_SMALL_MODE forces one)
 int sort_grid_mult(int which);  // CTAs per SM of the level-1 (1) / segmented (2) tile kernels: PRG_SORT_GRID1/2
 
 // Runs levels >= 2 until every segment is final; then the caller launches
@@ -870,6 +893,7 @@ void msd_sort_split(Src src_hist, Src src_scat, size_t n, int key_bits, Dst dst,
     const std::string t(tag);
     if (n == 0) return;
     sort_workspace_init(ws, n, s);
+    ws.n_sorting = n;
     // Digits cover bits [payload_bits, key_bits); the low payload bits ride along
     // (they never decide the order: keys are unique above them, or equal keys
     // carry equal payloads).
@@ -920,9 +944,20 @@ void msd_sort_split(Src src_hist, Src src_scat, size_t n, int key_bits, Dst dst,
     {
         ProfScope prof(t + "_local", s);
         if (!stable && payload_bits == 0 && local_small_min() > 0) {
-            local_small_kernel<Dst><<<num_sms() * 4, kSmallThreads, 0, s>>>(
-                ws.keys[0].get(), ws.keys[1].get(), ws.fin.get() + ws.max_fin, ws.counters.get() + 41,
-                ws.counters.get() + 40, dst, (local_merge_span() >> 12) & 7);
+            const int wl = (local_merge_span() >> 12) & 7;
+            uint32_t* cn = ws.counters.get();
+            const Seg* fe = ws.fin.get() + ws.max_fin;
+            if (local_small_mode(n) == 2) {  // three CTA sizes over the one list ([40], [42], [43]: their work counters)
+                local_small_kernel<Dst, 256, 4><<<num_sms() * 4, 256, 0, s>>>(
+                    ws.keys[0].get(), ws.keys[1].get(), fe, cn + 41, cn + 40, dst, wl, 2049u, 4096u);
+                local_small_kernel<Dst, 128, 8><<<num_sms() * 8, 128, 0, s>>>(
+                    ws.keys[0].get(), ws.keys[1].get(), fe, cn + 41, cn + 42, dst, wl, 1025u, 2048u);
+                local_small_kernel<Dst, 64, 16><<<num_sms() * 16, 64, 0, s>>>(
+                    ws.keys[0].get(), ws.keys[1].get(), fe, cn + 41, cn + 43, dst, wl, 1u, 1024u);
+            } else {
+                local_small_kernel<Dst, 256, 4><<<num_sms() * 4, 256, 0, s>>>(
+                    ws.keys[0].get(), ws.keys[1].get(), fe, cn + 41, cn + 40, dst, wl, 1u, 4096u);
+            }
             PRG_LAUNCH_CHECK();
         }
         PRG_CUDA(cudaFuncSetAttribute(local_sort_kernel<Dst>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -19,11 +19,11 @@
 // window and span >= 16 bits (K1) — a register-network + merge-path merge sort. An 8-bit ballot-ranked local pass measured slower (K1
 // local 6.3 -> 8.4 ms): instruction-bound on the ballots; with __match_any_sync
 // peers instead of ballots it is still slower (5.8 -> 9.0 ms).
-// Lone children of 1-4 K keys with <= 32 unsorted bits go to local_small_kernel, the
-// same merge sort on 256-thread CTAs (four to an SM), instead of being joined into
-// wider-window segments for the LSD path.
+// Children with <= 32 unsorted bits are joined only into runs whose window still fits 32
+// bits; runs of at most 4096 keys go to local_small_kernel, the same merge sort on 64-,
+// 128- or 256-thread CTAs, instead of wider-window segments for the LSD path.
 // For reference, CUB's onesweep DeviceRadixSort on this B200 takes 16.6 ms for
-// 2^28 48-bit keys; K1 (2^28 pairs in and out) takes 8.6 ms here.
+// 2^28 48-bit keys; K1 (2^28 pairs in and out) takes 8.4 ms here.
 #pragma once
 
 #include "prg_common.cuh"

@@ -540,7 +540,11 @@ template <int kStages>
 __global__ void __launch_bounds__(kST) k2_pass_a_tma(const longlong2* __restrict__ uv, int64_t m, int64_t n,
                                                      uint32_t* __restrict__ d_in, uint32_t* __restrict__ err,
                                                      unsigned long long* __restrict__ nnz_raw, uint32_t ntiles,
-                                                     uint32_t* __restrict__ next_tile) {
+                                                     uint32_t* __restrict__ next_tile, uint32_t v_lo, uint32_t v_hi,
+                                                     bool first) {
+    // Only columns [v_lo, v_hi) are counted by this launch (an in-degree table larger than the L2
+    // is filled window by window, see k2_filter_device); validation and the unique-entry count
+    // belong to the first window's launch.
     extern __shared__ __align__(128) unsigned char smem_raw[];
     longlong2* stages = reinterpret_cast<longlong2*>(smem_raw);
     __shared__ Ring<kStages> R;
@@ -581,13 +585,14 @@ __global__ void __launch_bounds__(kST) k2_pass_a_tma(const longlong2* __restrict
                     const unsigned after = ~(eqm >> lane >> 1) & (0x7fffffffu >> lane);
                     const uint32_t len = 1u + (after ? (uint32_t)(__ffs(after) - 1) : 31u - lane);
                     PRG_DCHECK(len >= 1 && len <= 32u - lane);
-                    atomicAdd(&d_in[(uint32_t)(e.y - 1)], len);
+                    const uint32_t c = (uint32_t)(e.y - 1);
+                    if (c >= v_lo && c < v_hi) atomicAdd(&d_in[c], len);
                 }
                 if (has_pred) {
                     if (e.x < px) my_err |= kErrUnsorted;
                     else if (e.x == px && e.y < py) my_err |= kErrNotCanonical;
                 }
-                heads += !same;
+                heads += first && !same;
             }
         }
         __syncthreads();  // every read of this stage is done
@@ -666,7 +671,21 @@ uint32_t k2_filter_device(const int64_t* d_uv, int64_t m, int64_t n, prg_matrix*
             const size_t smem = (size_t)kStagesA * kSE * sizeof(longlong2);
             PRG_CUDA(cudaFuncSetAttribute(k2_pass_a_tma<kStagesA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             const unsigned gs = grid_for((const void*)k2_pass_a_tma<kStagesA>, smem);
-            k2_pass_a_tma<kStagesA><<<gs, kST, smem, s>>>(uv, m, n, out->d_in, err, nnz_raw, ntiles_s, tile_counter_a);
+            // An in-degree table that does not fit the L2 (S=26: 268 MB) turns every RED into HBM
+            // traffic (pass A 20.3 ms for 2^30 edges, 8x the S=24 time for 4x the edges). Above
+            // 2^25 columns the table is filled one window of columns at a time: each launch
+            // re-streams the edges (~4.9 ms at S=26) but its atomics mostly stay in the L2.
+            // S=26: two 128 MB windows 16.6 ms; four 64 MB windows 19.7 ms; eight 36 ms.
+            static int64_t window = -1;  // PRG_K2_WINDOW: log2 of the window's columns (0 = one pass)
+            if (window < 0) { const char* e = getenv("PRG_K2_WINDOW"); window = e ? atoll(e) : 25; }
+            const int64_t wcols = window > 0 ? (int64_t{1} << window) : n;
+            const int nwin = (int)((n + wcols - 1) / wcols);
+            for (int wi = 0; wi < nwin; ++wi) {
+                if (wi) PRG_CUDA(cudaMemsetAsync(tile_counter_a, 0, 4, s));
+                k2_pass_a_tma<kStagesA><<<gs, kST, smem, s>>>(
+                    uv, m, n, out->d_in, err, nnz_raw, ntiles_s, tile_counter_a, (uint32_t)(wi * wcols),
+                    (uint32_t)std::min<int64_t>(n, (wi + 1) * wcols), wi == 0);
+            }
         }
         PRG_LAUNCH_CHECK();
     }

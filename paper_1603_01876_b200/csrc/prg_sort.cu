@@ -27,6 +27,9 @@ __device__ uint32_t g_coalesce_max = kLocalCap;
 // window (and carry no payload) are kept apart and listed (SmallList) for the
 // small-segment merge kernel (local_small_kernel); 0 = off.
 __device__ uint32_t g_small_min = 0;
+// mode 2: largest joined run (PRG_SMALL_RUNCAP). Measured K1 at S=22 / 24 / 26: 8192 -> 2.35 / 8.42 / 38.7 ms,
+// 4096 -> 2.31 / 8.39 / 38.2, 2048 -> 2.29 / 8.29 / 38.2, 1024 -> 2.31 / 8.28 / 37.6, 512 -> 2.36 / 8.35 / 39.3.
+__device__ uint32_t g_small_runcap = 1024;
 
 struct EmitScratch {
     uint8_t kind[kRadix];   // 0: joins the open run or empty, 1: starts a run, 2: larger than the cap, 3: small-kernel segment
@@ -52,7 +55,7 @@ __device__ void emit_children_block(const uint64_t* child_start, const uint32_t*
         for (int d = 0; d < nchild; ++d) {
             const uint32_t sz = child_size[d];
             uint8_t k = 0;
-            const bool cut = run && (sz > cap || (sz && ((d >> gbits) != (rs >> gbits) || run + sz > cap)));
+            const bool cut = run && (sz > cap || (sz && ((d >> gbits) != (rs >> gbits) || run + sz > g_small_runcap)));
             if (cut) { E.rsz[rs] = run; E.kind[rs] = run <= (uint32_t)kSmallCap ? 3 : 1; run = 0; }
             if (sz > cap) {
                 k = 2;
@@ -448,6 +451,9 @@ void sort_workspace_init(SortWorkspace& ws, size_t n, cudaStream_t s) {
     if (!small_set) {
         const uint32_t v = (uint32_t)local_small_min();
         PRG_CUDA(cudaMemcpyToSymbol(g_small_min, &v, sizeof(v)));
+        const char* rc = getenv("PRG_SMALL_RUNCAP");
+        const uint32_t rcv = rc ? (uint32_t)std::min(std::max(atoi(rc), 256), kLocalCap) : 1024u;
+        PRG_CUDA(cudaMemcpyToSymbol(g_small_runcap, &rcv, sizeof(rcv)));
 
         small_set = true;
     }

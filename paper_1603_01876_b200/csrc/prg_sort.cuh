@@ -23,7 +23,7 @@
 // bits; runs of at most 4096 keys go to local_small_kernel, the same merge sort on 64-,
 // 128- or 256-thread CTAs, instead of wider-window segments for the LSD path.
 // For reference, CUB's onesweep DeviceRadixSort on this B200 takes 16.6 ms for
-// 2^28 48-bit keys; K1 (2^28 pairs in and out) takes 8.4 ms here.
+// 2^28 48-bit keys; K1 (2^28 pairs in and out) takes 8.3 ms here.
 #pragma once
 
 #include "prg_common.cuh"

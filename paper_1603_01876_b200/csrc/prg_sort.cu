@@ -425,8 +425,9 @@ int local_small_mode(size_t n) {
         const char* e = getenv("PRG_SMALL_MODE");
         v = e ? atoi(e) : 0;
     }
-    // the three launches of mode 2 cost ~30 us: 3% of K1 at 2^24 keys, repaid from 2^26 on
-    return v == 1 || v == 2 ? v : (n >= (size_t(1) << 25) ? 2 : 1);
+    // the three launches of mode 2 cost ~30 us: K1 (L2 flushed) at 2^20 keys 0.33 (mode 1) vs 0.38 ms,
+    // 2^22 keys 0.515 vs 0.507, 2^24 keys 0.883 vs 0.853
+    return v == 1 || v == 2 ? v : (n >= (size_t(1) << 22) ? 2 : 1);
 }
 int local_merge_span() {
     static int v = -1;

@@ -1,5 +1,5 @@
-# Round artifacts on one GPU box (dev tool): full GPU suite + smoke + bench
-# (S=24 default line, then S=26), launch list and ncu captures of the hot kernels.
+# Round artifacts on one GPU box in ONE call (dev tool) — superseded by gpu_round_a.sh + gpu_round_b.sh: the
+# reports this writes under gpurun_out/ now exceed the 64 MiB gpurun copies back.
 # Every ncu command runs after the same command exited 0 without ncu.
 set -x
 TAG=${1:-r02}
